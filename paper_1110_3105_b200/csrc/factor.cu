@@ -1,0 +1,345 @@
+// factor.cu -- K3 + K4: batched per-box telescoping factorization and the
+// dense top-level inverse.
+//
+// Reference work replaced: factor / factor_node (solver.py:187-276), the
+// per-box LAPACK getrf/getrs calls (solver.py:210,243,252-256), _rcond1
+// (solver.py:179-184) and the top `_lu(Shat)` (solver.py:269-274).
+//
+// One CTA per box; every operand of the box lives in shared memory:
+//   A  (n x n)  D_eff -> D^-1 (Gauss-Jordan, partial pivoting) -> Dd
+//   Lb (n x k)  L -> Ld = X Lam
+//   Rb (k x n)  R -> Rd = Lam RD
+//   X  (n x k)  D^-1 L
+//   Y  (k x n)  R D^-1
+//   M  (k x k)  R X -> Lam = M^-1
+// Gauss-Jordan with row pivoting chooses the same pivots as getrf (the rows
+// below the diagonal see the same Schur complements), so exact-zero pivots
+// (SingularBlock, solver.py:211-212) are detected identically.
+#include "common.cuh"
+
+template <class T>
+struct FacShared {
+  int status;
+  int piv_row;
+  double amax;
+  double red[32];
+  int red_i[32];
+};
+
+// 1-norm (max column abs sum) of a row-major p x q matrix
+template <class T>
+__device__ double sm_norm1(const T* A, int lda, int p, int q, FacShared<T>& sh) {
+  double best = 0.0;
+  for (int j = threadIdx.x; j < q; j += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < p; ++i) s += sk_abs(A[(int64_t)i * lda + j]);
+    best = fmax(best, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh.red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  double r = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, sh.red[w]);
+  __syncthreads();
+  return r;
+}
+
+// In-place Gauss-Jordan inverse of a row-major p x p matrix with partial
+// pivoting.  colk: p scratch entries, ipiv: p ints.  Returns 0 or 1 (zero pivot).
+template <class T>
+__device__ int sm_invert(T* A, int lda, int p, T* colk, int* ipiv, FacShared<T>& sh) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  for (int kk = 0; kk < p; ++kk) {
+    if (warp == 0) {
+      double best = -1.0;
+      int bi = p;
+      for (int i = kk + lane; i < p; i += 32) {
+        double v = sk_pivabs(A[(int64_t)i * lda + kk]);
+        if (v > best) { best = v; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (lane == 0) {
+        sh.piv_row = bi;
+        sh.amax = best;
+        ipiv[kk] = bi;
+      }
+    }
+    __syncthreads();
+    if (sh.amax == 0.0) return 1;
+    const int pr = sh.piv_row;
+    if (pr != kk) {
+      for (int j = tid; j < p; j += nt) {
+        T t = A[(int64_t)kk * lda + j];
+        A[(int64_t)kk * lda + j] = A[(int64_t)pr * lda + j];
+        A[(int64_t)pr * lda + j] = t;
+      }
+      __syncthreads();
+    }
+    const T inv = T(1.0) / A[(int64_t)kk * lda + kk];
+    for (int i = tid; i < p; i += nt) colk[i] = A[(int64_t)i * lda + kk];
+    __syncthreads();
+    for (int j = tid; j < p; j += nt) {
+      if (j == kk) A[(int64_t)kk * lda + kk] = inv;
+      else A[(int64_t)kk * lda + j] = A[(int64_t)kk * lda + j] * inv;
+    }
+    __syncthreads();
+    for (int64_t e = tid; e < (int64_t)p * p; e += nt) {
+      int i = (int)(e / p), j = (int)(e - (int64_t)i * p);
+      if (i == kk) continue;
+      T f = colk[i];
+      if (j == kk) A[(int64_t)i * lda + kk] = -(f * inv);
+      else A[(int64_t)i * lda + j] -= f * A[(int64_t)kk * lda + j];
+    }
+    __syncthreads();
+  }
+  // undo the row interchanges as column interchanges, last first
+  for (int kk = p - 1; kk >= 0; --kk) {
+    int pr = ipiv[kk];
+    if (pr != kk) {
+      for (int i = tid; i < p; i += nt) {
+        T t = A[(int64_t)i * lda + kk];
+        A[(int64_t)i * lda + kk] = A[(int64_t)i * lda + pr];
+        A[(int64_t)i * lda + pr] = t;
+      }
+    }
+    __syncthreads();
+  }
+  return 0;
+}
+
+// C (p x q, ldc) = [C -] A (p x r) * B (r x q), row-major, 4x4 register tiles.
+template <class T, bool SUB>
+__device__ void sm_gemm(T* C, int ldc, const T* A, int lda, const T* B, int ldb, int p, int q,
+                        int r) {
+  const int tp = (p + 3) >> 2, tq = (q + 3) >> 2;
+  for (int t = threadIdx.x; t < tp * tq; t += blockDim.x) {
+    const int i0 = (t / tq) * 4, j0 = (t % tq) * 4;
+    T acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = T(0.0);
+    for (int s = 0; s < r; ++s) {
+      T av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = (i0 + a < p) ? A[(int64_t)(i0 + a) * lda + s] : T(0.0);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = (j0 + b < q) ? B[(int64_t)s * ldb + j0 + b] : T(0.0);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] += av[a] * bv[b];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (i0 + a < p && j0 + b < q) {
+          T* c = C + (int64_t)(i0 + a) * ldc + j0 + b;
+          if (SUB) *c = *c - acc[a][b];
+          else *c = acc[a][b];
+        }
+  }
+}
+
+template <class T>
+__device__ void copy_out(T* dst, const T* src, int64_t cnt) {
+  for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) dst[e] = src[e];
+}
+
+template <class T>
+static __host__ __device__ inline size_t fac_elems(int n, int k) {
+  return (size_t)n * n + 4 * (size_t)n * k + (size_t)k * k + (size_t)n;
+}
+
+template <class T, bool GW>
+__global__ void __launch_bounds__(256) k_factor_level(const SkelFactorLevel F, int max_n, int max_k) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  FacShared<T>& sh = *reinterpret_cast<FacShared<T>*>(smem);
+  int* ipiv = reinterpret_cast<int*>(smem + 512);
+  const size_t hdr = 512 + ((sizeof(int) * (size_t)max_n + 15) / 16) * 16;
+  T* base = GW ? reinterpret_cast<T*>(F.scratch) + (size_t)blockIdx.x * fac_elems<T>(max_n, max_k)
+               : reinterpret_cast<T*>(smem + hdr);
+  const int a = blockIdx.x;
+  const int n = F.n[a], k = F.k[a];
+  if (n == 0) {
+    if (threadIdx.x == 0) { F.status[a] = 0; F.rcond_d[a] = 1.0; F.rcond_m[a] = 1.0; }
+    return;
+  }
+  T* A = base;
+  T* Lb = A + (size_t)n * n;
+  T* Rb = Lb + (size_t)n * k;
+  T* X = Rb + (size_t)k * n;
+  T* Y = X + (size_t)n * k;
+  T* M = Y + (size_t)k * n;
+  T* colk = M + (size_t)k * k;
+
+  const T* D = reinterpret_cast<const T*>(F.D) + F.d_off[a];
+  for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) A[e] = D[e];
+  __syncthreads();
+  if (F.child_off) {
+    // children's Lambda on the diagonal blocks (solver.py:226-233)
+    const int64_t c0 = F.child_off[a], c1 = F.child_off[a + 1];
+    int ro = 0;
+    for (int64_t c = c0; c < c1; ++c) {
+      const int kc = F.prev_k[c];
+      const T* lam = reinterpret_cast<const T*>(F.prev_lam) + F.prev_lam_off[c];
+      for (int e = threadIdx.x; e < kc * kc; e += blockDim.x) {
+        int i = e / kc, j = e - i * kc;
+        A[(int64_t)(ro + i) * n + ro + j] = lam[e];
+      }
+      ro += kc;
+    }
+  }
+  __syncthreads();
+  if (F.regularize != 0.0) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) A[(int64_t)i * n + i] += T(F.regularize);
+    __syncthreads();
+  }
+  const T* Lg = reinterpret_cast<const T*>(F.L) + F.l_off[a];
+  const T* Rg = reinterpret_cast<const T*>(F.R) + F.r_off[a];
+  for (int64_t e = threadIdx.x; e < (int64_t)n * k; e += blockDim.x) {
+    Lb[e] = Lg[e];
+    Rb[e] = Rg[e];
+  }
+  double nA = sm_norm1<T>(A, n, n, n, sh);
+  int bad = sm_invert<T>(A, n, n, colk, ipiv, sh);
+  if (bad) {
+    if (threadIdx.x == 0) { F.status[a] = 1; F.rcond_d[a] = 0.0; F.rcond_m[a] = 0.0; }
+    return;
+  }
+  double nAi = sm_norm1<T>(A, n, n, n, sh);
+  const double rcd = (nA * nAi > 0.0) ? 1.0 / (nA * nAi) : 0.0;
+  T* Dd = reinterpret_cast<T*>(F.Dd) + F.dd_off[a];
+  if (k == 0) {
+    copy_out<T>(Dd, A, (int64_t)n * n);
+    if (threadIdx.x == 0) { F.status[a] = 0; F.rcond_d[a] = rcd; F.rcond_m[a] = 1.0; }
+    return;
+  }
+  sm_gemm<T, false>(X, k, A, n, Lb, k, n, k, n);    // X = D^-1 L
+  sm_gemm<T, false>(Y, n, Rb, n, A, n, k, n, n);    // Y = R D^-1
+  __syncthreads();
+  sm_gemm<T, false>(M, k, Rb, n, X, k, k, k, n);    // M = R X
+  __syncthreads();
+  double nM = sm_norm1<T>(M, k, k, k, sh);
+  if (F.regularize != 0.0) {
+    for (int i = threadIdx.x; i < k; i += blockDim.x) M[(int64_t)i * k + i] += T(F.regularize);
+    __syncthreads();
+  }
+  bad = sm_invert<T>(M, k, k, colk, ipiv, sh);
+  if (bad) {
+    if (threadIdx.x == 0) { F.status[a] = 2; F.rcond_d[a] = rcd; F.rcond_m[a] = 0.0; }
+    return;
+  }
+  double nMi = sm_norm1<T>(M, k, k, k, sh);
+  sm_gemm<T, false>(Rb, n, M, k, Y, n, k, n, k);    // Rd = Lam RD
+  sm_gemm<T, false>(Lb, k, X, k, M, k, n, k, k);    // Ld = X Lam
+  __syncthreads();
+  sm_gemm<T, true>(A, n, X, k, Rb, n, n, n, k);     // Dd = D^-1 - X Rd
+  __syncthreads();
+  copy_out<T>(Dd, A, (int64_t)n * n);
+  copy_out<T>(reinterpret_cast<T*>(F.Ld) + F.ld_off[a], Lb, (int64_t)n * k);
+  copy_out<T>(reinterpret_cast<T*>(F.Rd) + F.rd_off[a], Rb, (int64_t)k * n);
+  copy_out<T>(reinterpret_cast<T*>(F.Lam) + F.lam_off[a], M, (int64_t)k * k);
+  if (threadIdx.x == 0) {
+    F.status[a] = 0;
+    F.rcond_d[a] = rcd;
+    F.rcond_m[a] = (nM * nMi > 0.0) ? 1.0 / (nM * nMi) : 0.0;
+  }
+}
+
+template <class T>
+static int factor_level_impl(const SkelFactorLevel* F, int max_n, int max_k, cudaStream_t st) {
+  if (F->nbox <= 0) return 0;
+  if (max_n < 1) max_n = 1;
+  size_t hdr = 512 + ((sizeof(int) * (size_t)max_n + 15) / 16) * 16;
+  size_t need = hdr + fac_elems<T>(max_n, max_k) * sizeof(T);
+  if (need <= (size_t)skel_smem_optin()) {
+    auto kern = k_factor_level<T, false>;
+    SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+    kern<<<F->nbox, 256, need, st>>>(*F, max_n, max_k);
+  } else {
+    if (!F->scratch || (size_t)F->scratch_bytes < (size_t)F->nbox * fac_elems<T>(max_n, max_k) * sizeof(T))
+      return -2;
+    auto kern = k_factor_level<T, true>;
+    SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hdr));
+    kern<<<F->nbox, 256, hdr, st>>>(*F, max_n, max_k);
+  }
+  return skel_last_error();
+}
+
+// dense K x K inverse on one CTA (top level: Shat = S + blockdiag(Lam))
+template <class T, bool GW>
+__global__ void __launch_bounds__(1024) k_dense_inverse(T* Ag, int K, double reg, int32_t* status,
+                                                        double* rcond, T* scratch) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  FacShared<T>& sh = *reinterpret_cast<FacShared<T>*>(smem);
+  int* ipiv = reinterpret_cast<int*>(smem + 512);
+  size_t hdr = 512 + ((sizeof(int) * (size_t)K + 15) / 16) * 16;
+  T* A = GW ? scratch : reinterpret_cast<T*>(smem + hdr);
+  T* colk = GW ? scratch + (size_t)K * K : A + (size_t)K * K;
+  for (int64_t e = threadIdx.x; e < (int64_t)K * K; e += blockDim.x) A[e] = Ag[e];
+  __syncthreads();
+  if (reg != 0.0) {
+    for (int i = threadIdx.x; i < K; i += blockDim.x) A[(int64_t)i * K + i] += T(reg);
+    __syncthreads();
+  }
+  double nA = sm_norm1<T>(A, K, K, K, sh);
+  int bad = sm_invert<T>(A, K, K, colk, ipiv, sh);
+  if (bad) {
+    if (threadIdx.x == 0) { *status = 1; *rcond = 0.0; }
+    return;
+  }
+  double nAi = sm_norm1<T>(A, K, K, K, sh);
+  for (int64_t e = threadIdx.x; e < (int64_t)K * K; e += blockDim.x) Ag[e] = A[e];
+  if (threadIdx.x == 0) {
+    *status = 0;
+    *rcond = (nA * nAi > 0.0) ? 1.0 / (nA * nAi) : 0.0;
+  }
+}
+
+template <class T>
+static int dense_inverse_impl(void* A, int K, double reg, int32_t* status, double* rcond,
+                              void* scratch, cudaStream_t st) {
+  if (K <= 0) return 0;
+  size_t hdr = 512 + ((sizeof(int) * (size_t)K + 15) / 16) * 16;
+  size_t need = hdr + ((size_t)K * K + K) * sizeof(T);
+  if (need <= (size_t)skel_smem_optin()) {
+    auto kern = k_dense_inverse<T, false>;
+    SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+    kern<<<1, 1024, need, st>>>((T*)A, K, reg, status, rcond, (T*)scratch);
+  } else {
+    if (!scratch) return -2;
+    auto kern = k_dense_inverse<T, true>;
+    SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hdr));
+    kern<<<1, 1024, hdr, st>>>((T*)A, K, reg, status, rcond, (T*)scratch);
+  }
+  return skel_last_error();
+}
+
+extern "C" {
+
+int skel_factor_level(const SkelFactorLevel* fl, int32_t max_n, int32_t max_k, int32_t field,
+                      void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (field == 0) return factor_level_impl<double>(fl, max_n, max_k, st);
+  return factor_level_impl<zc>(fl, max_n, max_k, st);
+}
+
+int skel_dense_inverse(void* A, void* lu, int32_t* ipiv, int32_t K, double regularize,
+                       int32_t* status, double* rcond, int32_t field, void* scratch, void* stream) {
+  (void)lu;
+  (void)ipiv;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (field == 0) return dense_inverse_impl<double>(A, K, regularize, status, rcond, scratch, st);
+  return dense_inverse_impl<zc>(A, K, regularize, status, rcond, scratch, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,220 @@
+"""Point sets and the adaptive orthtree (drop-in for skelkit/geom.py).
+
+The tree, its covers and the same-cover neighbour lists are built by native
+C++ in libskel_sm100.so (``skel_tree_*``): the reference's recursion
+(geom.py:118-184) and its O(p^2) ``level_neighbors`` (geom.py:205-219) are
+replaced by an explicit-stack build and an O(p) grid-hash search that keeps
+the reference's box-touch predicate, so every list is identical.
+"""
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .errors import InvalidInput
+
+DEFAULT_MAX_LEAF = {2: 64, 3: 128}
+
+
+@dataclass
+class PointSet:
+    """N points in 2D or 3D with optional unit normals, quadrature weights and
+    curvatures (validation as geom.py:35-61)."""
+
+    coords: np.ndarray
+    normals: np.ndarray | None = None
+    weights: np.ndarray | None = None
+    curvatures: np.ndarray | None = None
+
+    def __post_init__(self):
+        c = np.ascontiguousarray(self.coords, dtype=np.float64)
+        if c.ndim != 2 or c.shape[1] not in (2, 3):
+            raise InvalidInput(f"coords must be (N, d) with d in {{2,3}}, got {c.shape}")
+        if c.shape[0] < 1:
+            raise InvalidInput("need at least one point")
+        if not np.isfinite(c).all():
+            raise InvalidInput("non-finite coordinate")
+        self.coords = c
+        if self.normals is not None:
+            nrm = np.ascontiguousarray(self.normals, dtype=np.float64)
+            if nrm.shape != c.shape:
+                raise InvalidInput("normals must match coords shape")
+            if np.any(np.abs(np.linalg.norm(nrm, axis=1) - 1.0) > 1e-12):
+                raise InvalidInput("normals must be unit vectors (|n| = 1 within 1e-12)")
+            self.normals = nrm
+        for name in ("weights", "curvatures"):
+            v = getattr(self, name)
+            if v is None:
+                continue
+            v = np.ascontiguousarray(v, dtype=np.float64).reshape(-1)
+            if v.shape[0] != c.shape[0]:
+                raise InvalidInput(f"{name} must have one entry per point")
+            setattr(self, name, v)
+
+    @property
+    def n(self):
+        return self.coords.shape[0]
+
+    @property
+    def dim(self):
+        return self.coords.shape[1]
+
+    def subset(self, idx):
+        pick = lambda a: None if a is None else a[idx]  # noqa: E731
+        return PointSet(self.coords[idx], pick(self.normals), pick(self.weights),
+                        pick(self.curvatures))
+
+
+@dataclass
+class TreeNode:
+    center: np.ndarray
+    halfwidth: float
+    lo: int
+    hi: int
+    depth: int
+    parent: int | None = None
+    children: list = field(default_factory=list)
+
+    @property
+    def size(self):
+        return self.hi - self.lo
+
+
+class OrthTree:
+    """Adaptive 2^d tree.  ``levels[0]`` is the finest cover, ``levels[-1]``
+    the root alone; ``perm`` maps tree positions to original indices.  Node
+    arrays (``center``, ``hw``, ``lo``, ``hi``, ``node_depth``, ``parent``,
+    ``nchild``) are kept flat; ``nodes`` materialises TreeNode objects."""
+
+    def __init__(self, handle, dim, n):
+        L = _native.lib()
+        self._handle = ctypes.c_void_p(handle)
+        self.dim = dim
+        nn = ctypes.c_int64()
+        nc = ctypes.c_int32()
+        _native.check(L.skel_tree_sizes(self._handle, ctypes.byref(nn), ctypes.byref(nc)),
+                      "skel_tree_sizes")
+        nn, nc = nn.value, nc.value
+        self.center = np.empty((nn, dim))
+        self.hw = np.empty(nn)
+        self.lo = np.empty(nn, dtype=np.int64)
+        self.hi = np.empty(nn, dtype=np.int64)
+        self.node_depth = np.empty(nn, dtype=np.int64)
+        self.parent = np.empty(nn, dtype=np.int64)
+        self.nchild = np.empty(nn, dtype=np.int64)
+        self.perm = np.empty(n, dtype=np.int64)
+        a = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        _native.check(L.skel_tree_nodes(self._handle, a(self.center), a(self.hw), a(self.lo),
+                                        a(self.hi), a(self.node_depth), a(self.parent),
+                                        a(self.nchild), a(self.perm)), "skel_tree_nodes")
+        self.levels = []
+        for li in range(nc):
+            cnt = ctypes.c_int64()
+            _native.check(L.skel_tree_cover(self._handle, li, ctypes.byref(cnt), None),
+                          "skel_tree_cover")
+            ids = np.empty(cnt.value, dtype=np.int64)
+            _native.check(L.skel_tree_cover(self._handle, li, ctypes.byref(cnt), a(ids)),
+                          "skel_tree_cover")
+            self.levels.append(ids)
+        self._nodes = None
+        self._nbr_cache = {}
+
+    def __del__(self):
+        try:
+            if self._handle:
+                _native.lib().skel_tree_free(self._handle)
+                self._handle = None
+        except Exception:
+            pass
+
+    @property
+    def nodes(self):
+        if self._nodes is None:
+            out = [TreeNode(self.center[i].copy(), float(self.hw[i]), int(self.lo[i]),
+                            int(self.hi[i]), int(self.node_depth[i]),
+                            None if self.parent[i] < 0 else int(self.parent[i]))
+                   for i in range(self.hw.size)]
+            for i in range(self.hw.size):
+                if self.parent[i] >= 0:
+                    out[self.parent[i]].children.append(i)
+            self._nodes = out
+        return self._nodes
+
+    @property
+    def depth(self):
+        return len(self.levels)
+
+    @property
+    def root(self):
+        return self.nodes[int(self.levels[-1][0])]
+
+    @property
+    def n_points(self):
+        return int(self.hi[0] - self.lo[0])
+
+    def leaves(self):
+        return [int(i) for i in np.nonzero(self.nchild == 0)[0]]
+
+    def cover_neighbors(self, li):
+        """CSR (offsets, positions) of cover ``li``'s adjacency (cached)."""
+        if li not in self._nbr_cache:
+            L = _native.lib()
+            p = self.levels[li].size
+            off = np.empty(p + 1, dtype=np.int64)
+            cnt = ctypes.c_int64()
+            a = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+            _native.check(L.skel_tree_neighbors(self._handle, li, a(off), ctypes.byref(cnt), None),
+                          "skel_tree_neighbors")
+            idx = np.empty(cnt.value, dtype=np.int64)
+            _native.check(L.skel_tree_neighbors(self._handle, li, a(off), ctypes.byref(cnt), a(idx)),
+                          "skel_tree_neighbors")
+            self._nbr_cache[li] = (off, idx)
+        return self._nbr_cache[li]
+
+    def cover_children(self, li):
+        """CSR offsets of cover ``li``'s nodes into cover ``li-1`` (children
+        are contiguous runs; skel.py:252-264)."""
+        starts = self.lo[self.levels[li - 1]]
+        ends = self.hi[self.levels[li]]
+        return np.concatenate([[0], np.searchsorted(starts, ends, side="left")]).astype(np.int64)
+
+
+def build_tree(points: PointSet, max_leaf_size: int | None = None) -> OrthTree:
+    """Adaptive orthtree with contiguous per-node ranges (geom.py:118-184),
+    built natively."""
+    d = points.dim
+    if max_leaf_size is None:
+        max_leaf_size = DEFAULT_MAX_LEAF[d]
+    if max_leaf_size < 1:
+        raise InvalidInput("max_leaf_size must be >= 1")
+    coords = np.ascontiguousarray(points.coords, dtype=np.float64)
+    if not np.isfinite(coords).all():
+        raise InvalidInput("non-finite coordinate")
+    h = ctypes.c_void_p()
+    _native.check(_native.lib().skel_tree_build(coords.ctypes.data_as(ctypes.c_void_p),
+                                                points.n, d, int(max_leaf_size),
+                                                ctypes.byref(h)), "skel_tree_build")
+    return OrthTree(h.value, d, points.n)
+
+
+def _touch(tree, a, others, tol):
+    gap = np.abs(tree.center[others] - tree.center[a]) - (tree.hw[others] + tree.hw[a])[:, None]
+    return np.all(gap <= tol, axis=1)
+
+
+def neighbors(tree: OrthTree, node_id: int) -> list:
+    """Same-depth nodes touching ``node_id`` (geom.py:192-202), ascending id."""
+    if not isinstance(node_id, (int, np.integer)) or not 0 <= node_id < tree.hw.size:
+        raise InvalidInput(f"invalid node id {node_id!r}")
+    tol = 1e-9 * tree.hw[0]
+    cand = np.nonzero(tree.node_depth == tree.node_depth[node_id])[0]
+    cand = cand[cand != node_id]
+    return [int(i) for i in cand[_touch(tree, node_id, cand, tol)]]
+
+
+def level_neighbors(tree: OrthTree, level: int) -> list:
+    """Adjacency lists of cover ``level`` (geom.py:205-219), native O(p)."""
+    off, idx = tree.cover_neighbors(level)
+    return [idx[off[a]:off[a + 1]].tolist() for a in range(off.size - 1)]

@@ -1,0 +1,94 @@
+"""Interpolative decompositions on the GPU (drop-in for the deterministic
+path of skelkit/lowrank.py): the same CTA-cooperative CPQR routine the
+compression kernel uses (csrc/cpqr.cuh), exposed for explicit matrices."""
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import InvalidInput
+
+
+@dataclass
+class InterpDecomp:
+    """A ~ A[:, skel] @ proj; skel in pivot order, proj[:, skel] == I."""
+    skel: np.ndarray
+    proj: np.ndarray
+    rank: int
+    achieved_error: float
+
+    @property
+    def k(self):
+        return self.rank
+
+
+def _as_matrix(A):
+    A = np.asarray(A)
+    if A.dtype.kind not in "fc":
+        A = A.astype(np.float64)
+    if A.ndim != 2:
+        raise InvalidInput("expected a 2D matrix")
+    if not np.all(np.isfinite(A)):
+        raise InvalidInput("matrix has non-finite entries")
+    return A
+
+
+def id_fixed_precision_batched(mats, eps, min_ranks=None):
+    """Column IDs of several matrices in one launch (one CTA per matrix)."""
+    torch = _native.require_cuda()
+    if not 0 < eps < 1:
+        raise InvalidInput("eps must lie in (0, 1)")
+    mats = [_as_matrix(A) for A in mats]
+    cplx = any(A.dtype.kind == "c" for A in mats)
+    dt = np.complex128 if cplx else np.float64
+    field = int(cplx)
+    nb = len(mats)
+    ms = np.array([A.shape[0] for A in mats], dtype=np.int32)
+    ns = np.array([A.shape[1] for A in mats], dtype=np.int32)
+    a_off = np.concatenate([[0], np.cumsum(ms.astype(np.int64) * ns)]).astype(np.int64)
+    flat = np.concatenate([np.asarray(A, dtype=dt).ravel(order="F") for A in mats]) if nb else np.zeros(0, dt)
+    s_off = np.concatenate([[0], np.cumsum(ns.astype(np.int64))]).astype(np.int64)
+    p_off = np.concatenate([[0], np.cumsum(ns.astype(np.int64) ** 2)]).astype(np.int64)
+    mr = np.zeros(nb, dtype=np.int32) if min_ranks is None else np.asarray(min_ranks, dtype=np.int32)
+    dev = torch.device("cuda")
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    dA, dao, dm, dn, dmr = up(flat), up(a_off), up(ms), up(ns), up(mr)
+    rank = torch.zeros(nb, dtype=torch.int32, device=dev)
+    skel = torch.zeros(max(int(s_off[-1]), 1), dtype=torch.int32, device=dev)
+    proj = torch.zeros(max(int(p_off[-1]), 1), dtype=_native.torch_dtype(field), device=dev)
+    big = torch.zeros(nb, dtype=torch.float64, device=dev)
+    dso, dpo = up(s_off), up(p_off)
+    max_m = int(ms.max()) if nb else 1
+    max_n = int(ns.max()) if nb else 1
+    need = nb * max_m * max_n * (16 if cplx else 8)
+    scratch = torch.empty(max(need // 8, 1), dtype=torch.float64, device=dev)
+    p = _native.ptr
+    _native.check(_native.lib().skel_id_batched(
+        p(dA), p(dao), p(dm), p(dn), nb, float(eps), p(dmr), p(rank), p(skel), p(dso), p(proj),
+        p(dpo), p(big), field, p(scratch), scratch.numel() * 8, max_m, max_n,
+        _native.stream_ptr()), "skel_id_batched")
+    rank, skel, proj, big = rank.cpu().numpy(), skel.cpu().numpy(), proj.cpu().numpy(), big.cpu().numpy()
+    out = []
+    for b in range(nb):
+        k, n = int(rank[b]), int(ns[b])
+        P = proj[p_off[b]:p_off[b] + k * n].reshape(k, n).astype(dt)
+        if big[b] > 2.0:
+            warnings.warn(f"interpolation matrix entries reach {big[b]:.3g} (> 2); "
+                          "pivoting quality degraded on this block", stacklevel=3)
+        out.append(InterpDecomp(skel=skel[s_off[b]:s_off[b] + k].astype(np.int64), proj=P,
+                                rank=k, achieved_error=float("nan")))
+    return out
+
+
+def id_fixed_precision(A, eps, min_rank=0) -> InterpDecomp:
+    """Column ID to relative precision eps by CPQR (lowrank.py:136-161)."""
+    if not 0 < eps < 1:
+        raise InvalidInput("eps must lie in (0, 1)")
+    return id_fixed_precision_batched([A], eps, [min_rank])[0]
+
+
+def id_rows(A, eps, min_rank=0) -> InterpDecomp:
+    """Row ID: A ~ proj.T @ A[skel, :] (plain transpose, lowrank.py:164-166)."""
+    return id_fixed_precision(np.asarray(A).T, eps, min_rank=min_rank)

@@ -1,0 +1,627 @@
+"""Multilevel recursive skeletonization on the GPU (drop-in for
+skelkit/skel.py).
+
+``compress_source`` keeps the reference's level sweep (skel.py:286-411) as a
+host loop over covers, but every box of a cover is processed by ONE launch of
+``skel_id_level`` (csrc/id_level.cu): a 2-CTA cluster per box assembles
+D = A(rd, cd) and the proxy-compressed targets t_row.T / t_col straight into
+shared memory, runs both CPQR IDs, equalises the ranks through DSMEM and
+writes sorted skeletons plus L / R.  The host only does O(p) integer
+bookkeeping per level (offsets, buckets) and reads back the ranks.
+
+The resulting ``CompressedMatrix`` stays on the device; its per-node numpy
+view (``levels[l].nodes``) is materialised lazily for callers that inspect
+it.
+"""
+
+import warnings
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _native
+from ._device import DeviceGeometry
+from .errors import InvalidInput, RefusedTooLarge
+from .geom import OrthTree, PointSet
+from .kernels import KernelSpec
+
+DEFAULT_N_PROXY = {2: 64, 3: 512}        # skel.py:29
+_RANDOMIZED_CUTOFF = 4096                # skel.py:33
+GLOBAL_MODE_LIMIT = 20000                # skel.py:35
+_RPL_CLASSES = (128, 256, 384, 512, 768)
+
+
+@dataclass
+class ProxyConfig:
+    """Proxy surface: n_proxy points on the circle/sphere of radius
+    3*sqrt(d)*halfwidth*radius_factor (skel.py:53-76)."""
+
+    n_proxy: int | None = None
+    radius_factor: float = 1.0
+    shape: str = "auto"
+
+    def resolve(self, dim):
+        n = self.n_proxy if self.n_proxy is not None else DEFAULT_N_PROXY[dim]
+        floor = 8 if dim == 2 else 32
+        if n < floor:
+            raise InvalidInput(f"n_proxy must be >= {floor} in {dim}D")
+        shape = self.shape
+        if shape == "auto":
+            shape = "circle" if dim == 2 else "sphere"
+        if (shape == "circle") != (dim == 2):
+            raise InvalidInput(f"proxy shape {shape!r} incompatible with {dim}D")
+        return replace(self, n_proxy=n, shape=shape)
+
+
+def proxy_radius(halfwidth, config: ProxyConfig, dim):
+    return config.radius_factor * 3.0 * halfwidth * np.sqrt(dim)
+
+
+def unit_proxy(n, dim):
+    """Unit proxy surface: equispaced circle from angle 0 / Fibonacci sphere
+    (skel.py:87-96)."""
+    if dim == 2:
+        th = 2 * np.pi * np.arange(n) / n
+        return np.column_stack([np.cos(th), np.sin(th)])
+    i = np.arange(n) + 0.5
+    z = 1.0 - 2.0 * i / n
+    rho = np.sqrt(np.clip(1.0 - z * z, 0.0, None))
+    th = np.pi * (3.0 - np.sqrt(5.0)) * i
+    return np.column_stack([rho * np.cos(th), rho * np.sin(th), z])
+
+
+def proxy_points(box, config: ProxyConfig, dim) -> PointSet:
+    cfg = config.resolve(dim)
+    r = proxy_radius(box.halfwidth, cfg, dim)
+    return PointSet(np.asarray(box.center, dtype=np.float64) + r * unit_proxy(cfg.n_proxy, dim))
+
+
+# ---------------------------------------------------------------------------
+# matrix sources with a device descriptor
+
+class _DeviceSourceMixin:
+    """block(rows, cols) in tree positions, evaluated on the GPU."""
+
+    def _desc(self):
+        raise NotImplementedError
+
+    def device_source(self):
+        return self._desc(), self.field
+
+    @property
+    def field(self):
+        return 1 if np.dtype(self.dtype) == np.complex128 else 0
+
+    def block(self, rows, cols):
+        torch = _native.require_cuda()
+        rows = np.asarray(rows, dtype=np.int64)
+        cols = np.asarray(cols, dtype=np.int64)
+        m, n = rows.size, cols.size
+        if m == 0 or n == 0:
+            return np.zeros((m, n), dtype=self.dtype)
+        dev = torch.device("cuda")
+        r = torch.from_numpy(rows.astype(np.int32)).to(dev)
+        c = torch.from_numpy(cols.astype(np.int32)).to(dev)
+        out = torch.empty((m, n), dtype=_native.torch_dtype(self.field), device=dev)
+        _native.check(_native.lib().skel_eval_block(self._desc(), _native.ptr(r), m, _native.ptr(c),
+                                                    n, _native.ptr(out), self.field,
+                                                    _native.stream_ptr()), "skel_eval_block")
+        return out.cpu().numpy()
+
+
+class KernelSource(_DeviceSourceMixin):
+    """Plain kernel matrix in tree order (skel.py:100-124); proxies use the
+    single layer of the same equation.  ``diag`` (an extension used by
+    BASELINE config 4) is added where row == col."""
+
+    def __init__(self, spec: KernelSpec, points: PointSet, perm, diag=0.0):
+        self.spec = spec
+        self.points = points.subset(perm)
+        self.proxy_spec = spec.single_layer()
+        self.n = points.n
+        self.dtype = spec.dtype
+        self.wavenumber = spec.wavenumber
+        self.diag = float(diag)
+        self.geo = DeviceGeometry(points.coords, perm,
+                                  points.normals if spec.layer == "double" else None,
+                                  points.weights, None)
+
+    def _desc(self):
+        return self.geo.source(_native.SRC_KERNEL, self.spec.eq_code, self.spec.layer_code,
+                               self.spec.wavenumber, diag=self.diag,
+                               weighted=self.points.weights is not None)
+
+
+# ---------------------------------------------------------------------------
+# compressed representation
+
+@dataclass
+class CompressedNode:
+    row_skel: np.ndarray
+    col_skel: np.ndarray
+    D: np.ndarray
+    L: np.ndarray
+    R: np.ndarray
+    children: np.ndarray | None
+
+    @property
+    def k_r(self):
+        return self.row_skel.size
+
+    @property
+    def k_c(self):
+        return self.col_skel.size
+
+
+def _off(counts):
+    return np.concatenate([[0], np.cumsum(np.asarray(counts, dtype=np.int64))]).astype(np.int64)
+
+
+class DevLevel:
+    """Device slabs of one compressed level (capacity layouts addressed by
+    per-box element offsets)."""
+
+    def __init__(self, li, nr, nc, kr, kc, d_off, l_off, r_off, D, L, R, rskel, cskel, child_off,
+                 dtype):
+        torch = _native.require_cuda()
+        dev = torch.device("cuda")
+        self.li = li
+        self.p = nr.size
+        self.nr, self.nc = nr.astype(np.int64), nc.astype(np.int64)
+        self.kr, self.kc = kr.astype(np.int64), kc.astype(np.int64)
+        self.d_off, self.l_off, self.r_off = d_off, l_off, r_off
+        self.D, self.L, self.R = D, L, R
+        self.rskel, self.cskel = rskel, cskel          # compacted, int32, device
+        self.child_off = child_off
+        self.dtype = dtype
+        up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        self.t_d_off, self.t_l_off, self.t_r_off = up(d_off), up(l_off), up(r_off)
+        self.t_nr = up(self.nr.astype(np.int32))
+        self.t_kr = up(self.kr.astype(np.int32))
+        self.t_kc = up(self.kc.astype(np.int32))
+        self.t_rdof_off = up(_off(self.nr))
+        self.t_cdof_off = up(_off(self.nc))
+        self.t_kr_off = up(_off(self.kr))
+        self.t_kc_off = up(_off(self.kc))
+        self.t_child_off = None if child_off is None else up(child_off)
+
+
+class CompressedLevel:
+    """Per-level view with the reference's offset tables (skel.py:145-163)."""
+
+    def __init__(self, nodes=None, dev: DevLevel | None = None):
+        self._nodes = nodes
+        self.dev = dev
+        if nodes is not None:
+            self.row_dof_counts = np.array([nd.D.shape[0] for nd in nodes], dtype=np.int64)
+            self.col_dof_counts = np.array([nd.D.shape[1] for nd in nodes], dtype=np.int64)
+            self.kr_counts = np.array([nd.k_r for nd in nodes], dtype=np.int64)
+            self.kc_counts = np.array([nd.k_c for nd in nodes], dtype=np.int64)
+        else:
+            self.row_dof_counts, self.col_dof_counts = dev.nr, dev.nc
+            self.kr_counts, self.kc_counts = dev.kr, dev.kc
+        self.row_dof_off = _off(self.row_dof_counts)
+        self.col_dof_off = _off(self.col_dof_counts)
+        self.kr_off = _off(self.kr_counts)
+        self.kc_off = _off(self.kc_counts)
+
+    @property
+    def nodes(self):
+        if self._nodes is None:
+            d = self.dev
+            D = d.D.cpu().numpy()
+            L = d.L.cpu().numpy()
+            R = d.R.cpu().numpy()
+            rs = d.rskel.cpu().numpy().astype(np.int64)
+            cs = d.cskel.cpu().numpy().astype(np.int64)
+            out = []
+            for a in range(d.p):
+                nr, nc, kr, kc = (int(d.nr[a]), int(d.nc[a]), int(d.kr[a]), int(d.kc[a]))
+                out.append(CompressedNode(
+                    row_skel=rs[self.kr_off[a]:self.kr_off[a + 1]].copy(),
+                    col_skel=cs[self.kc_off[a]:self.kc_off[a + 1]].copy(),
+                    D=D[d.d_off[a]:d.d_off[a] + nr * nc].reshape(nr, nc).copy(),
+                    L=L[d.l_off[a]:d.l_off[a] + nr * kr].reshape(nr, kr).copy(),
+                    R=R[d.r_off[a]:d.r_off[a] + kc * nc].reshape(kc, nc).copy(),
+                    children=None if d.child_off is None else
+                    np.arange(d.child_off[a], d.child_off[a + 1], dtype=np.int64)))
+            self._nodes = out
+        return self._nodes
+
+    @property
+    def K_r(self):
+        return int(self.kr_off[-1])
+
+    @property
+    def K_c(self):
+        return int(self.kc_off[-1])
+
+
+class CompressedMatrix:
+    """Telescoping compressed form A ~ D1 + L1 [ ... S ... ] R1 (skel.py:166-203).
+    ``S`` is materialised on the host on first access; the device copy is
+    ``S_dev``."""
+
+    def __init__(self, levels, S, n, eps, perm, scalar_field, tree=None, S_dev=None):
+        self.levels = levels
+        self._S = S
+        self.S_dev = S_dev
+        self.n = n
+        self.eps = eps
+        self.perm = perm
+        self.scalar_field = scalar_field
+        self.tree = tree
+
+    @property
+    def S(self):
+        if self._S is None:
+            self._S = self.S_dev.cpu().numpy()
+        return self._S
+
+    @S.setter
+    def S(self, v):
+        self._S = v
+        self.S_dev = None
+
+    @property
+    def nlevels(self):
+        return len(self.levels)
+
+    @property
+    def dtype(self):
+        return np.complex128 if self.scalar_field == "complex" else np.float64
+
+    @property
+    def field(self):
+        return 1 if self.scalar_field == "complex" else 0
+
+    def skeleton_counts(self):
+        return [(lv.K_r, lv.K_c) for lv in self.levels]
+
+    def storage_bytes(self):
+        it = np.dtype(self.dtype).itemsize
+        tot = int(np.prod(self.S_shape())) * it + self.perm.nbytes
+        for lv in self.levels:
+            nr, nc, kr, kc = lv.row_dof_counts, lv.col_dof_counts, lv.kr_counts, lv.kc_counts
+            tot += int((nr * nc + nr * kr + kc * nc).sum()) * it + int((kr + kc).sum()) * 8
+        return tot
+
+    def S_shape(self):
+        if self._S is not None:
+            return self._S.shape
+        return tuple(self.S_dev.shape)
+
+    def apply(self, x):
+        return apply(self, x)
+
+    def matvec_dense(self):
+        return apply(self, np.eye(self.n, dtype=self.dtype))
+
+    # -- device view ----------------------------------------------------------
+    def device_levels(self):
+        """DevLevel per level; host-built levels are packed and uploaded once."""
+        out = []
+        for li, lv in enumerate(self.levels):
+            if lv.dev is None:
+                lv.dev = _pack_level(li, lv, self.dtype)
+            out.append(lv.dev)
+        return out
+
+    def device_S(self):
+        if self.S_dev is None:
+            torch = _native.require_cuda()
+            self.S_dev = torch.from_numpy(np.ascontiguousarray(self._S, dtype=self.dtype)).to("cuda")
+        return self.S_dev
+
+
+def _pack_level(li, lv, dtype):
+    torch = _native.require_cuda()
+    dev = torch.device("cuda")
+    nodes = lv.nodes
+    nr, nc = lv.row_dof_counts, lv.col_dof_counts
+    kr, kc = lv.kr_counts, lv.kc_counts
+    d_off, l_off, r_off = _off(nr * nc), _off(nr * kr), _off(kc * nc)
+    cat = lambda arrs: (np.concatenate([np.asarray(a, dtype=dtype).ravel() for a in arrs])  # noqa: E731
+                        if arrs else np.zeros(0, dtype=dtype))
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    D = up(cat([nd.D for nd in nodes]))
+    L = up(cat([nd.L for nd in nodes]))
+    R = up(cat([nd.R for nd in nodes]))
+    rs = up(np.concatenate([nd.row_skel for nd in nodes]).astype(np.int32) if nodes else np.zeros(0, np.int32))
+    cs = up(np.concatenate([nd.col_skel for nd in nodes]).astype(np.int32) if nodes else np.zeros(0, np.int32))
+    child_off = None
+    if li > 0:
+        counts = [0 if nd.children is None else len(nd.children) for nd in nodes]
+        child_off = _off(counts)
+        firsts = [int(nd.children[0]) for nd in nodes if nd.children is not None and len(nd.children)]
+        # children must be contiguous runs in order (as compress produces)
+        flat = np.concatenate([np.asarray(nd.children, dtype=np.int64) for nd in nodes
+                               if nd.children is not None and len(nd.children)]) if firsts else np.zeros(0, np.int64)
+        if flat.size and not np.array_equal(flat, np.arange(flat.size)):
+            raise InvalidInput("children of each level must be consecutive positions of the previous level")
+    return DevLevel(li, nr, nc, kr, kc, d_off, l_off, r_off, D, L, R, rs, cs, child_off, dtype)
+
+
+# ---------------------------------------------------------------------------
+# compression sweep
+
+def compress(spec: KernelSpec, points: PointSet, tree: OrthTree, eps, proxy=None, mode="proxy",
+             equalize_ranks=True, seed=0, allow_large=False) -> CompressedMatrix:
+    """Recursively skeletonize the kernel matrix of ``spec`` (skel.py:267-283)."""
+    source = KernelSource(spec, points, tree.perm)
+    return compress_source(source, tree, eps, proxy=proxy, mode=mode,
+                           equalize_ranks=equalize_ranks, seed=seed, allow_large=allow_large)
+
+
+def _segment_sum(vals, off):
+    cs = np.concatenate([[0], np.cumsum(vals)])
+    return cs[off[1:]] - cs[off[:-1]]
+
+
+def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = None,
+                    mode: str = "proxy", equalize_ranks: bool = True, seed: int = 0,
+                    allow_large: bool = False) -> CompressedMatrix:
+    """GPU compression sweep over a matrix source with a device descriptor
+    (skel.py:286-411)."""
+    if not 0 < eps < 1:
+        raise InvalidInput("eps must lie in (0, 1)")
+    if mode not in ("proxy", "global"):
+        raise InvalidInput(f"unknown mode {mode!r}")
+    n = tree.n_points
+    if mode == "global" and n > GLOBAL_MODE_LIMIT and not allow_large:
+        raise RefusedTooLarge(f"global-mode compression of N={n} is quadratic; "
+                              "pass allow_large=True to force it")
+    if mode == "global":
+        raise InvalidInput("mode='global' is not part of the B200 hot path; use mode='proxy'")
+    if not hasattr(source, "device_source"):
+        raise InvalidInput("matrix source has no device descriptor (use KernelSource, "
+                           "bie.BieSystem sources, or bie.combined_field_system)")
+    torch = _native.require_cuda()
+    dev = torch.device("cuda")
+    cfg = (proxy or ProxyConfig()).resolve(tree.dim)
+    desc, field = source.device_source()
+    dtype = np.complex128 if field else np.float64
+    sfield = "complex" if field else "real"
+    tdt = _native.torch_dtype(field)
+    covers = tree.levels
+    top = next(i for i, c in enumerate(covers) if len(c) == 1)
+    L = _native.lib()
+    st = _native.stream_ptr()
+    p_ = _native.ptr
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+
+    if top == 0:
+        allidx = torch.arange(n, dtype=torch.int32, device=dev)
+        S = torch.empty((n, n), dtype=tdt, device=dev)
+        _native.check(L.skel_eval_block(desc, p_(allidx), n, p_(allidx), n, p_(S), field, st),
+                      "skel_eval_block")
+        return CompressedMatrix([], None, n, eps, tree.perm.copy(), sfield, tree, S_dev=S)
+
+    k_wave = float(getattr(source, "wavenumber", 0.0))
+    dim = tree.dim
+    levels = []
+    prev = None
+    optin = _smem_optin()
+    for li in range(top):
+        ids = covers[li]
+        p = ids.size
+        noff, nidx = tree.cover_neighbors(li)
+        if li == 0:
+            nr = (tree.hi[ids] - tree.lo[ids]).astype(np.int64)
+            nc = nr.copy()
+            rdofs = torch.arange(n, dtype=torch.int32, device=dev)
+            cdofs = rdofs
+            child_off = None
+        else:
+            child_off = tree.cover_children(li)
+            nr = _segment_sum(prev.kr, child_off)
+            nc = _segment_sum(prev.kc, child_off)
+            rdofs, cdofs = prev.rskel, prev.cskel
+        rdof_off, cdof_off = _off(nr), _off(nc)
+        hw = tree.hw[ids]
+        rad = cfg.radius_factor * 3.0 * hw * np.sqrt(dim)
+        neff = np.full(p, cfg.n_proxy, dtype=np.int64)
+        if k_wave > 0:
+            neff += np.ceil(4.0 * k_wave * rad).astype(np.int64)
+        uniq = np.unique(neff)
+        tables = [unit_proxy(int(u), dim) for u in uniq]
+        tstart = _off([t.shape[0] for t in tables])[:-1]
+        pxy_begin = tstart[np.searchsorted(uniq, neff)].astype(np.int32)
+        unit = np.concatenate(tables, axis=0)
+        m0 = _segment_sum(nc[nidx], noff) + neff
+        m1 = _segment_sum(nr[nidx], noff) + neff
+        d_off, l_off, r_off = _off(nr * nc), _off(nr * nr), _off(nc * nc)
+        Dt = torch.empty(max(int(d_off[-1]), 1), dtype=tdt, device=dev)
+        Lt = torch.empty(max(int(l_off[-1]), 1), dtype=tdt, device=dev)
+        Rt = torch.empty(max(int(r_off[-1]), 1), dtype=tdt, device=dev)
+        rskel = torch.empty(max(int(rdof_off[-1]), 1), dtype=torch.int32, device=dev)
+        cskel = torch.empty(max(int(cdof_off[-1]), 1), dtype=torch.int32, device=dev)
+        kr_t = torch.zeros(p, dtype=torch.int32, device=dev)
+        kc_t = torch.zeros(p, dtype=torch.int32, device=dev)
+        flags = torch.zeros(p, dtype=torch.int32, device=dev)
+        keep = dict(
+            rdof_off=up(rdof_off), cdof_off=up(cdof_off), nbr_off=up(noff),
+            nbr=up(nidx.astype(np.int32)), box_c=up(tree.center[ids].ravel()), box_r=up(rad),
+            pxy_begin=up(pxy_begin), pxy_count=up(neff.astype(np.int32)), pxy_unit=up(unit.ravel()),
+            d_off=up(d_off), l_off=up(l_off), r_off=up(r_off))
+        if li > 0:
+            keep["child_off"] = up(child_off)
+            keep["prev_kr"] = up(prev.kr.astype(np.int32))
+            keep["prev_kc"] = up(prev.kc.astype(np.int32))
+        lvd = _native.SkelLevel()
+        lvd.nbox, lvd.level, lvd.equalize, lvd.n_unit = p, li, int(bool(equalize_ranks)), unit.shape[0]
+        lvd.eps = float(eps)
+        lvd.rdof_off, lvd.rdofs = p_(keep["rdof_off"]), p_(rdofs)
+        lvd.cdof_off, lvd.cdofs = p_(keep["cdof_off"]), p_(cdofs)
+        lvd.child_off = p_(keep.get("child_off"))
+        lvd.prev_kr, lvd.prev_kc = p_(keep.get("prev_kr")), p_(keep.get("prev_kc"))
+        lvd.nbr_off, lvd.nbr = p_(keep["nbr_off"]), p_(keep["nbr"])
+        lvd.box_c, lvd.box_r = p_(keep["box_c"]), p_(keep["box_r"])
+        lvd.pxy_begin, lvd.pxy_count, lvd.pxy_unit = (p_(keep["pxy_begin"]), p_(keep["pxy_count"]),
+                                                      p_(keep["pxy_unit"]))
+        lvd.d_off, lvd.l_off, lvd.r_off = p_(keep["d_off"]), p_(keep["l_off"]), p_(keep["r_off"])
+        lvd.D, lvd.L, lvd.R = p_(Dt), p_(Lt), p_(Rt)
+        lvd.rskel, lvd.cskel = p_(rskel), p_(cskel)
+        lvd.kr, lvd.kc, lvd.flags = p_(kr_t), p_(kc_t), p_(flags)
+        # bucket boxes by target height so each launch gets a tight register
+        # tile (rows per lane) and shared-memory size
+        need_m = np.maximum(m0, m1)
+        need_n = np.maximum(nr, nc)
+        cls = np.searchsorted(np.array(_RPL_CLASSES), need_m, side="left")
+        scratch_keep = []
+        for c in np.unique(cls):
+            sel = np.nonzero(cls == c)[0]
+            sel = sel[np.argsort(-(need_m[sel] * need_n[sel]), kind="stable")]
+            max_m, max_n = int(need_m[sel].max()), max(int(need_n[sel].max()), 1)
+            elem = 16 if field else 8
+            fixed = _level_smem_fixed(max_n, field)
+            if fixed + max_m * max_n * elem > optin:
+                sb = 2 * sel.size * max_m * max_n * elem
+                scr = torch.empty(sb // 8 + 1, dtype=torch.float64, device=dev)
+                scratch_keep.append(scr)
+                lvd.scratch, lvd.scratch_bytes = p_(scr), sb
+            else:
+                lvd.scratch, lvd.scratch_bytes = None, 0
+            order = up(sel.astype(np.int32))
+            scratch_keep.append(order)
+            _native.check(L.skel_id_level(desc, lvd, p_(order), sel.size, max_m, max_n, field, st),
+                          f"skel_id_level (level {li})")
+        kr = kr_t.cpu().numpy().astype(np.int64)
+        kc = kc_t.cpu().numpy().astype(np.int64)
+        fl = flags.cpu().numpy()
+        if np.any(fl & 8):
+            raise RuntimeError(f"level {li}: a box exceeds the kernel's neighbour/child limits")
+        for a in np.nonzero(fl & 3)[0]:
+            warnings.warn(f"interpolation matrix entries reach > 2 at level {li}, node {a}; "
+                          "pivoting quality degraded on this block", stacklevel=2)
+        # compact the sorted skeletons: they are the next level's dof lists
+        kro, kco = _off(kr), _off(kc)
+        rsk = torch.empty(max(int(kro[-1]), 1), dtype=torch.int32, device=dev)
+        csk = torch.empty(max(int(kco[-1]), 1), dtype=torch.int32, device=dev)
+        t_kr, t_kc = up(kr.astype(np.int32)), up(kc.astype(np.int32))
+        t_kro, t_kco = up(kro), up(kco)
+        _native.check(L.skel_compact_i32(p, keep["rdof_off"].data_ptr(), p_(t_kr), p_(t_kro),
+                                         p_(rskel), p_(rsk), st), "skel_compact_i32")
+        _native.check(L.skel_compact_i32(p, keep["cdof_off"].data_ptr(), p_(t_kc), p_(t_kco),
+                                         p_(cskel), p_(csk), st), "skel_compact_i32")
+        rsk, csk = rsk[:int(kro[-1])], csk[:int(kco[-1])]
+        dl = DevLevel(li, nr, nc, kr, kc, d_off,
+                      _off(nr * nr), _off(nc * nc), Dt, Lt, Rt, rsk, csk, child_off, dtype)
+        # L is stored nr x kr inside an nr x nr slot, R kc x nc inside nc x nc
+        levels.append(CompressedLevel(dev=dl))
+        prev = dl
+
+    last = prev
+    Kr, Kc = int(last.kr.sum()), int(last.kc.sum())
+    S = torch.zeros((max(Kr, 0), max(Kc, 0)), dtype=tdt, device=dev)
+    if Kr and Kc:
+        rbox = up(np.repeat(np.arange(last.p), last.kr).astype(np.int32))
+        cbox = up(np.repeat(np.arange(last.p), last.kc).astype(np.int32))
+        _native.check(L.skel_assemble_S(desc, p_(last.rskel), p_(rbox), Kr, p_(last.cskel),
+                                        p_(cbox), Kc, p_(S), field, st), "skel_assemble_S")
+    return CompressedMatrix(levels, None, n, eps, tree.perm.copy(), sfield, tree, S_dev=S)
+
+
+_OPTIN = None
+
+
+def _smem_optin():
+    global _OPTIN
+    if _OPTIN is None:
+        import ctypes
+        a, b, c, d = (ctypes.c_int32() for _ in range(4))
+        _native.check(_native.lib().skel_device_query(ctypes.byref(a), ctypes.byref(b),
+                                                      ctypes.byref(c), ctypes.byref(d)),
+                      "skel_device_query")
+        _OPTIN = b.value
+    return _OPTIN
+
+
+def _level_smem_fixed(max_n, field):
+    """Host mirror of level_smem_fixed<T> in csrc/id_level.cu (upper bound)."""
+    al = lambda v: (v + 15) // 16 * 16  # noqa: E731
+    sh = al(80)
+    hdr = al(4 * (257 + 256 + 9 + 9 + 2) + 8 * 32 + 8)
+    return sh + hdr + al(80 * max_n) + al(16 * max_n) + al(8 * max_n)
+
+
+# ---------------------------------------------------------------------------
+# compressed apply (skel.py:206-249)
+
+def _as_device_rhs(x, n, dtype):
+    torch = _native.require_cuda()
+    if hasattr(x, "is_cuda"):
+        X = x.reshape(n, -1).to(_native.torch_dtype(int(np.dtype(dtype) == np.complex128)))
+        return X.contiguous(), True
+    X = np.ascontiguousarray(np.asarray(x).reshape(n, -1), dtype=dtype)
+    return torch.from_numpy(X).to("cuda"), False
+
+
+def apply(cm: CompressedMatrix, x) -> np.ndarray:
+    """y = A x through the compressed form: R up-sweep, S, D + L down-sweep."""
+    torch = _native.require_cuda()
+    xa = x if hasattr(x, "is_cuda") else np.asarray(x)
+    if xa.shape[0] != cm.n:
+        raise InvalidInput(f"length mismatch: matrix is {cm.n}, vector {xa.shape[0]}")
+    single = xa.ndim == 1
+    xdt = np.complex128 if (hasattr(xa, "is_complex") and xa.is_complex()) else getattr(xa, "dtype", np.float64)
+    dtype = np.result_type(cm.dtype, xdt if not hasattr(xa, "is_cuda") else
+                           (np.complex128 if xa.is_complex() else np.float64))
+    if dtype == np.complex128 and cm.dtype == np.float64:
+        re = apply(cm, xa.real)
+        im = apply(cm, xa.imag)
+        return re + 1j * im
+    field = int(dtype == np.complex128)
+    X, on_dev = _as_device_rhs(xa, cm.n, dtype)
+    Rn = X.shape[1]
+    L = _native.lib()
+    st = _native.stream_ptr()
+    p_ = _native.ptr
+    perm = torch.from_numpy(cm.perm).to("cuda")
+    xt = torch.empty_like(X)
+    _native.check(L.skel_permute_rows(p_(perm), cm.n, p_(X), p_(xt), Rn, 0, field, st), "permute")
+    if cm.nlevels == 0:
+        yt = _dense_apply(cm.device_S(), xt, field)
+    else:
+        dls = cm.device_levels()
+        us = [xt]
+        u = xt
+        for dl in dls:
+            nxt = torch.empty((int(dl.kc.sum()), Rn), dtype=X.dtype, device="cuda")
+            _native.check(L.skel_sweep_up_ex(dl.p, p_(dl.t_nr), p_(dl.t_kc), p_(dl.t_cdof_off),
+                                             p_(dl.t_kc_off), p_(dl.t_r_off), p_(dl.R), p_(u),
+                                             p_(nxt), Rn, field, int(max(dl.nc.max(), 1)), st),
+                          "sweep_up")
+            us.append(nxt)
+            u = nxt
+        v = _dense_apply(cm.device_S(), u, field)
+        for li in range(cm.nlevels - 1, -1, -1):
+            dl = dls[li]
+            w = torch.empty((int(dl.nr.sum()), Rn), dtype=X.dtype, device="cuda")
+            _native.check(L.skel_sweep_down_ex(dl.p, p_(dl.t_nr), p_(dl.t_kr), p_(dl.t_rdof_off),
+                                               p_(dl.t_kr_off), p_(dl.t_d_off), p_(dl.D),
+                                               p_(dl.t_l_off), p_(dl.L), p_(us[li]), p_(v), p_(w),
+                                               Rn, field, int(max((dl.nr + dl.kr).max(), 1)), st),
+                          "sweep_down")
+            v = w
+        yt = v
+    out = torch.empty_like(yt)
+    _native.check(L.skel_permute_rows(p_(perm), cm.n, p_(yt), p_(out), Rn, 1, field, st), "permute")
+    if on_dev:
+        return out[:, 0] if single else out
+    res = out.cpu().numpy()
+    return res[:, 0] if single else res
+
+
+def _dense_apply(M, x, field):
+    torch = _native.require_cuda()
+    K, Kc = M.shape
+    Rn = x.shape[1]
+    y = torch.empty((K, Rn), dtype=x.dtype, device="cuda")
+    if K and Kc:
+        _native.check(_native.lib().skel_dense_apply(_native.ptr(M), K, Kc, _native.ptr(x),
+                                                     _native.ptr(y), Rn, field,
+                                                     _native.stream_ptr()), "dense_apply")
+    elif K:
+        y.zero_()
+    return y

@@ -1,0 +1,320 @@
+"""Telescoping factorization and multi-RHS solve on the GPU (drop-in for the
+factor / solve half of skelkit/solver.py).
+
+``factor`` runs one ``skel_factor_level`` launch per level (one CTA per box,
+csrc/factor.cu) and one dense inverse of Shat at the top; ``solve`` runs the
+up-sweep, the top GEMM and the down-sweep (csrc/solve.cu).  Per-box numerical
+outcomes come back as status / rcond arrays and are mapped onto the
+reference's contract: ``SingularBlock(level, node, what)`` for an exact zero
+pivot, ``InvalidInput`` for non-square blocks, and ``warnings`` tuples
+``(level, node, what, rcond)`` for rcond < 1e-14 (solver.py:199-262).
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .errors import InvalidInput, SingularBlock
+from .skel import CompressedMatrix, _dense_apply, _off
+
+_RCOND_WARN = 1e-14
+
+
+@dataclass
+class FactoredNode:
+    Dd: np.ndarray
+    Ld: np.ndarray
+    Rd: np.ndarray
+    Lam: np.ndarray
+    lu_D: tuple | None = None
+    lu_M: tuple | None = None
+
+
+class DevFactorLevel:
+    def __init__(self, n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, child_off):
+        torch = _native.require_cuda()
+        up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda")  # noqa: E731
+        self.p = n.size
+        self.n, self.k = n, k
+        self.dd_off, self.ld_off, self.lam_off = dd_off, ld_off, lam_off
+        self.Dd, self.Ld, self.Rd, self.Lam = Dd, Ld, Rd, Lam
+        self.child_off = child_off
+        self.t_n = up(n.astype(np.int32))
+        self.t_k = up(k.astype(np.int32))
+        self.t_noff = up(_off(n))
+        self.t_koff = up(_off(k))
+        self.t_dd_off = up(dd_off)
+        self.t_ld_off = up(ld_off)
+        self.t_lam_off = up(lam_off)
+        self.max_n = int(max(n.max(initial=0), 1))
+        self.max_nk = int(max((n + k).max(initial=0), 1))
+
+
+class FactoredLevel:
+    """Per-level view (solver.py:153-159); nodes materialised lazily."""
+
+    def __init__(self, dev: DevFactorLevel):
+        self.dev = dev
+        self.row_dof_off = _off(dev.n)
+        self.col_dof_off = _off(dev.n)
+        self.kr_off = _off(dev.k)
+        self.kc_off = _off(dev.k)
+        self._nodes = None
+
+    @property
+    def nodes(self):
+        if self._nodes is None:
+            d = self.dev
+            Dd, Ld, Rd, Lam = (t.cpu().numpy() for t in (d.Dd, d.Ld, d.Rd, d.Lam))
+            out = []
+            for a in range(d.p):
+                n, k = int(d.n[a]), int(d.k[a])
+                out.append(FactoredNode(
+                    Dd=Dd[d.dd_off[a]:d.dd_off[a] + n * n].reshape(n, n).copy(),
+                    Ld=Ld[d.ld_off[a]:d.ld_off[a] + n * k].reshape(n, k).copy(),
+                    Rd=Rd[d.ld_off[a]:d.ld_off[a] + n * k].reshape(k, n).copy(),
+                    Lam=Lam[d.lam_off[a]:d.lam_off[a] + k * k].reshape(k, k).copy()))
+            self._nodes = out
+        return self._nodes
+
+
+class FactoredInverse:
+    """Telescoping inverse held on the device (solver.py:162-176).
+    ``S_hat`` / ``S_inv`` are the top matrix and its inverse (device)."""
+
+    def __init__(self, levels, S_hat, S_inv, n, perm, scalar_field, warnings):
+        self.levels = levels
+        self.S_hat = S_hat
+        self.S_inv = S_inv
+        self.n = n
+        self.perm = perm
+        self.scalar_field = scalar_field
+        self.warnings = warnings
+        self._perm_dev = None
+
+    @property
+    def dtype(self):
+        return np.complex128 if self.scalar_field == "complex" else np.float64
+
+    @property
+    def field(self):
+        return 1 if self.scalar_field == "complex" else 0
+
+    @property
+    def S_lu(self):
+        """Explicit top inverse stands in for the reference's (lu, piv); kept
+        for attribute compatibility."""
+        return None if self.S_inv is None else (self.S_inv, None)
+
+    def perm_dev(self):
+        if self._perm_dev is None:
+            torch = _native.require_cuda()
+            self._perm_dev = torch.from_numpy(np.ascontiguousarray(self.perm)).to("cuda")
+        return self._perm_dev
+
+    def solve(self, b):
+        return solve(self, b)
+
+    def factor_bytes(self):
+        it = np.dtype(self.dtype).itemsize
+        tot = 0
+        for lv in self.levels:
+            n, k = lv.dev.n, lv.dev.k
+            tot += int((n * n + 2 * n * k).sum()) * it
+        if self.S_inv is not None:
+            tot += self.S_inv.numel() * it
+        return tot
+
+
+def _invert_top(Sh, regularize, field):
+    """Shat^-1 on the device (single CTA Gauss-Jordan); status 1 -> singular."""
+    torch = _native.require_cuda()
+    K = Sh.shape[0]
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rc = torch.zeros(1, dtype=torch.float64, device="cuda")
+    scratch = torch.empty((K * K + K) * (2 if field else 1) + 1, dtype=torch.float64, device="cuda")
+    _native.check(_native.lib().skel_dense_inverse(_native.ptr(Sh), None, None, K, float(regularize),
+                                                   _native.ptr(st), _native.ptr(rc), field,
+                                                   _native.ptr(scratch), _native.stream_ptr()),
+                  "skel_dense_inverse")
+    return int(st.item()), float(rc.item())
+
+
+def factor(cm: CompressedMatrix, regularize: float = 0.0) -> FactoredInverse:
+    """Telescoping inverse of a compressed matrix (solver.py:187-276)."""
+    torch = _native.require_cuda()
+    dev = torch.device("cuda")
+    field = cm.field
+    tdt = _native.torch_dtype(field)
+    L = _native.lib()
+    st = _native.stream_ptr()
+    p_ = _native.ptr
+    warns = []
+    if cm.nlevels == 0:
+        S = cm.device_S()
+        if S.shape[0] != S.shape[1]:
+            raise InvalidInput(f"non-square S block ({S.shape[0]}x{S.shape[1]}) at level top, "
+                               "node 0; compress with equalize_ranks=True")
+        if S.numel() == 0:
+            return FactoredInverse([], None, None, cm.n, cm.perm.copy(), cm.scalar_field, warns)
+        Sinv = S.clone()
+        status, _ = _invert_top(Sinv, regularize, field)
+        if status:
+            raise SingularBlock("top", 0, "S")
+        return FactoredInverse([], S, Sinv, cm.n, cm.perm.copy(), cm.scalar_field, warns)
+
+    dls = cm.device_levels()
+    flevels = []
+    prev = None
+    for li, dl in enumerate(dls):
+        p = dl.p
+        sq_bad = dl.nr != dl.nc
+        lam_bad = (~sq_bad) & (dl.nr > 0) & (dl.kr != dl.kc)
+        n = np.where(sq_bad | lam_bad, 0, dl.nr).astype(np.int64)
+        k = np.where(n > 0, dl.kr, 0).astype(np.int64)
+        dd_off, ld_off, lam_off = _off(n * n), _off(n * k), _off(k * k)
+        Dd = torch.empty(max(int(dd_off[-1]), 1), dtype=tdt, device=dev)
+        Ld = torch.empty(max(int(ld_off[-1]), 1), dtype=tdt, device=dev)
+        Rd = torch.empty(max(int(ld_off[-1]), 1), dtype=tdt, device=dev)
+        Lam = torch.empty(max(int(lam_off[-1]), 1), dtype=tdt, device=dev)
+        status = torch.zeros(p, dtype=torch.int32, device=dev)
+        rcd = torch.ones(p, dtype=torch.float64, device=dev)
+        rcm = torch.ones(p, dtype=torch.float64, device=dev)
+        fl = DevFactorLevel(n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, dl.child_off)
+        F = _native.SkelFactorLevel()
+        F.nbox, F.level, F.regularize = p, li, float(regularize)
+        F.n, F.k = p_(fl.t_n), p_(fl.t_k)
+        F.d_off, F.l_off, F.r_off = p_(dl.t_d_off), p_(dl.t_l_off), p_(dl.t_r_off)
+        F.D, F.L, F.R = p_(dl.D), p_(dl.L), p_(dl.R)
+        if li > 0:
+            F.child_off = p_(dl.t_child_off)
+            F.prev_lam_off, F.prev_lam, F.prev_k = p_(prev.t_lam_off), p_(prev.Lam), p_(prev.t_k)
+        F.dd_off, F.ld_off, F.rd_off, F.lam_off = (p_(fl.t_dd_off), p_(fl.t_ld_off),
+                                                   p_(fl.t_ld_off), p_(fl.t_lam_off))
+        F.Dd, F.Ld, F.Rd, F.Lam = p_(Dd), p_(Ld), p_(Rd), p_(Lam)
+        F.status, F.rcond_d, F.rcond_m = p_(status), p_(rcd), p_(rcm)
+        max_n = int(max(n.max(initial=0), 1))
+        max_k = int(k.max(initial=0))
+        elem = 16 if field else 8
+        need = (max_n * max_n + 4 * max_n * max_k + max_k * max_k + max_n) * elem
+        scr = None
+        if need + 1024 > _smem_optin():
+            scr = torch.empty(p * need // 8 + 1, dtype=torch.float64, device=dev)
+            F.scratch, F.scratch_bytes = p_(scr), p * need
+        _native.check(L.skel_factor_level(F, max_n, max_k, field, st), f"skel_factor_level ({li})")
+        sts = status.cpu().numpy()
+        rd_h = rcd.cpu().numpy()
+        rm_h = rcm.cpu().numpy()
+        fails = np.nonzero(sq_bad | lam_bad | (sts != 0))[0]
+        if fails.size:
+            a = int(fails[0])
+            if sq_bad[a]:
+                raise InvalidInput(f"non-square D block ({dl.nr[a]}x{dl.nc[a]}) at level {li + 1}, "
+                                   f"node {a}; compress with equalize_ranks=True")
+            if sts[a] == 1:
+                raise SingularBlock(li + 1, a, "D")
+            if lam_bad[a]:
+                raise InvalidInput(f"non-square Lambda block ({dl.kc[a]}x{dl.kr[a]}) at level "
+                                   f"{li + 1}, node {a}; compress with equalize_ranks=True")
+            raise SingularBlock(li + 1, a, "Lambda")
+        for a in np.nonzero(((n > 0) & (rd_h < _RCOND_WARN)) | ((k > 0) & (rm_h < _RCOND_WARN)))[0]:
+            if n[a] > 0 and rd_h[a] < _RCOND_WARN:
+                warns.append((li + 1, int(a), "D", float(rd_h[a])))
+            if k[a] > 0 and rm_h[a] < _RCOND_WARN:
+                warns.append((li + 1, int(a), "Lambda", float(rm_h[a])))
+        flevels.append(FactoredLevel(fl))
+        prev = fl
+
+    # top: Shat = S with the last level's Lambdas on the diagonal blocks
+    S = cm.device_S()
+    last = dls[-1]
+    if S.shape[0] != S.shape[1]:
+        raise InvalidInput(f"non-square S block ({S.shape[0]}x{S.shape[1]}) at level top, node 0; "
+                           "compress with equalize_ranks=True")
+    Sh = S.clone()
+    kro = _off(prev.k)
+    for a in range(prev.p):
+        ka = int(prev.k[a])
+        if ka:
+            Sh[kro[a]:kro[a] + ka, kro[a]:kro[a] + ka] = \
+                prev.Lam[prev.lam_off[a]:prev.lam_off[a] + ka * ka].view(ka, ka)
+    del last
+    if Sh.numel() == 0:
+        return FactoredInverse(flevels, Sh, None, cm.n, cm.perm.copy(), cm.scalar_field, warns)
+    Sinv = Sh.clone()
+    status, _ = _invert_top(Sinv, regularize, field)
+    if status:
+        raise SingularBlock("top", 0, "S")
+    return FactoredInverse(flevels, Sh, Sinv, cm.n, cm.perm.copy(), cm.scalar_field, warns)
+
+
+def _smem_optin():
+    from .skel import _smem_optin as f
+    return f()
+
+
+def solve(fi: FactoredInverse, b):
+    """x = Dd1 b + Ld1 [ ... Shat^-1 ... ] Rd1 b for one or many RHS
+    (solver.py:279-318).  numpy in -> numpy out; a CUDA tensor in -> CUDA
+    tensor out (no host round trip)."""
+    torch = _native.require_cuda()
+    on_dev = hasattr(b, "is_cuda")
+    ba = b if on_dev else np.asarray(b)
+    if ba.shape[0] != fi.n:
+        raise InvalidInput(f"length mismatch: system is {fi.n}, rhs {ba.shape[0]}")
+    single = ba.ndim == 1
+    bdt = (np.complex128 if ba.is_complex() else np.float64) if on_dev else ba.dtype
+    dtype = np.result_type(fi.dtype, bdt)
+    if dtype == np.complex128 and fi.dtype == np.float64:
+        # real factorization, complex data: two real solves (linear)
+        return solve(fi, ba.real) + 1j * solve(fi, ba.imag)
+    field = int(dtype == np.complex128)
+    if on_dev:
+        B = ba.reshape(fi.n, -1).to(_native.torch_dtype(field)).contiguous()
+    else:
+        B = torch.from_numpy(np.ascontiguousarray(ba.reshape(fi.n, -1), dtype=dtype)).to("cuda")
+    X = solve_device(fi, B)
+    if on_dev:
+        return X[:, 0] if single else X
+    x = X.cpu().numpy()
+    return x[:, 0] if single else x
+
+
+def solve_device(fi: FactoredInverse, B):
+    """Device-resident solve of an (N, R) CUDA tensor (original ordering)."""
+    torch = _native.require_cuda()
+    L = _native.lib()
+    st = _native.stream_ptr()
+    p_ = _native.ptr
+    field = fi.field
+    Rn = B.shape[1]
+    perm = fi.perm_dev()
+    bt = torch.empty_like(B)
+    _native.check(L.skel_permute_rows(p_(perm), fi.n, p_(B), p_(bt), Rn, 0, field, st), "permute")
+    if not fi.levels:
+        xt = _dense_apply(fi.S_inv, bt, field) if fi.S_inv is not None else bt
+    else:
+        us = [bt]
+        u = bt
+        for lv in fi.levels:
+            d = lv.dev
+            nxt = torch.empty((int(d.k.sum()), Rn), dtype=B.dtype, device="cuda")
+            _native.check(L.skel_sweep_up_ex(d.p, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
+                                             p_(d.t_ld_off), p_(d.Rd), p_(u), p_(nxt), Rn, field,
+                                             d.max_n, st), "sweep_up")
+            us.append(nxt)
+            u = nxt
+        v = _dense_apply(fi.S_inv, u, field) if (fi.S_inv is not None and u.shape[0]) else u
+        for li in range(len(fi.levels) - 1, -1, -1):
+            d = fi.levels[li].dev
+            w = torch.empty((int(d.n.sum()), Rn), dtype=B.dtype, device="cuda")
+            _native.check(L.skel_sweep_down_ex(d.p, p_(d.t_n), p_(d.t_k), p_(d.t_noff),
+                                               p_(d.t_koff), p_(d.t_dd_off), p_(d.Dd),
+                                               p_(d.t_ld_off), p_(d.Ld), p_(us[li]), p_(v), p_(w),
+                                               Rn, field, d.max_nk, st), "sweep_down")
+            v = w
+        xt = v
+    X = torch.empty_like(xt)
+    _native.check(L.skel_permute_rows(p_(perm), fi.n, p_(xt), p_(X), Rn, 1, field, st), "permute")
+    return X

@@ -1,0 +1,91 @@
+"""CPU-only checks: the C-ABI library loads and exports every symbol the
+header declares; the native tree / neighbour builder equals the oracle (and
+hence the reference); host-side API validation."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+
+def test_library_exports_header_symbols():
+    from paper_1110_3105_b200 import _native
+    lib = _native.lib()
+    syms = _native.header_symbols()
+    assert len(syms) >= 15
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert b"sm_100a" in lib.skel_version()
+
+
+@pytest.mark.parametrize("n,dim", [(1024, 2), (4096, 2), (65536, 2), (5000, 3), (20000, 3)])
+def test_native_tree_equals_oracle(n, dim):
+    import paper_1110_3105_b200 as sk
+    X = oracle.ellipse(2.0, 1.0, n)["xy"] if dim == 2 else oracle.fib_sphere(n)
+    T = sk.build_tree(sk.PointSet(X), 64)
+    O = oracle.build_tree(X, 64)
+    np.testing.assert_array_equal(T.perm, O.perm)
+    np.testing.assert_array_equal(T.center, O.center)
+    np.testing.assert_array_equal(T.hw, O.hw)
+    assert len(T.levels) == len(O.covers)
+    for li in range(len(T.levels)):
+        np.testing.assert_array_equal(T.levels[li], O.covers[li])
+        off, idx = T.cover_neighbors(li)
+        o2, i2 = oracle.level_neighbors(O, li)
+        np.testing.assert_array_equal(off, o2)
+        np.testing.assert_array_equal(idx, i2)
+        if li:
+            np.testing.assert_array_equal(T.cover_children(li), oracle.cover_children(O, li))
+
+
+def test_native_tree_matches_golden(golden):
+    import paper_1110_3105_b200 as sk
+    g = golden("sphere_2000_1e-6")
+    T = sk.build_tree(sk.PointSet(oracle.fib_sphere(2000)), 64)
+    np.testing.assert_array_equal(T.perm, g["perm"])
+    for li in range(T.depth):
+        off, idx = T.cover_neighbors(li)
+        np.testing.assert_array_equal(off, g[f"N{li}_off"])
+        np.testing.assert_array_equal(idx, g[f"N{li}_idx"])
+    assert sk.level_neighbors(T, 0)[0] == list(g["N0_idx"][g["N0_off"][0]:g["N0_off"][1]])
+
+
+def test_tree_edge_cases():
+    import paper_1110_3105_b200 as sk
+    # identical points do not recurse forever (geom.py _MAX_DEPTH)
+    T = sk.build_tree(sk.PointSet(np.zeros((100, 2))), 8)
+    assert T.n_points == 100
+    # split-plane tie goes to the upper child
+    X = np.array([[0.0, 0.0], [1.0, 1.0], [0.5, 0.5], [0.25, 0.75]])
+    T = sk.build_tree(sk.PointSet(X), 1)
+    O = oracle.build_tree(X, 1)
+    np.testing.assert_array_equal(T.perm, O.perm)
+    # single point
+    T = sk.build_tree(sk.PointSet(np.array([[3.0, 4.0]])), 64)
+    assert T.depth == 1
+
+
+def test_host_validation():
+    import paper_1110_3105_b200 as sk
+    with pytest.raises(sk.InvalidInput):
+        sk.PointSet(np.zeros((3, 4)))
+    with pytest.raises(sk.InvalidInput):
+        sk.PointSet(np.array([[np.nan, 0.0]]))
+    with pytest.raises(sk.InvalidInput):
+        sk.KernelSpec("stokes", 2)
+    with pytest.raises(sk.InvalidInput):
+        sk.KernelSpec("helmholtz", 2)
+    with pytest.raises(sk.InvalidInput):
+        sk.bie.discretize_dirichlet(sk.bie.ellipse(2, 1, 64), sk.KernelSpec("helmholtz", 2, "double", 3.0),
+                                    quad="plain_trapezoid")
+    with pytest.raises(sk.InvalidInput):
+        sk.ProxyConfig(n_proxy=4).resolve(2)
+
+
+def test_proxy_points_match_oracle():
+    import paper_1110_3105_b200 as sk
+    T = sk.build_tree(sk.PointSet(oracle.ellipse(2.0, 1.0, 512)["xy"]), 64)
+    node = T.nodes[3]
+    P = sk.proxy_points(node, sk.ProxyConfig(), 2).coords
+    ref = node.center + oracle.geometry.proxy_radius(node.halfwidth, 2) * oracle.proxy_unit_points(64, 2)
+    np.testing.assert_array_equal(P, ref)
