@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark of the recursive-skeletonization factor / multi-RHS solve path
+on B200 (BASELINE.json config 2 + config 5).
+
+One step = one pass of the hot path over the config-2 workload: build the
+quadtree + neighbour lists, compress (proxy IDs), factor (telescoping
+inverse) of the 2D Laplace double-layer system on the a=2, b=1 ellipse at
+N = 2^20, eps = 1e-12 (identity_coef -1/2), then a 16-RHS
+solve.  ``value`` is the factor time (s) of the step (tree + compress +
+factor, geometry resident in HBM), ``solve`` the 16-RHS N*RHS/s, and
+``solve_1024`` config 5's 1024-RHS throughput on the same factorization.
+
+  python bench.py [--gpus N --steps K --warmup W]      # ours
+  python bench.py --impl reference ...                  # CPU oracle (rank 0)
+
+Prints ONE JSON line on rank 0.  See DESIGN.md ("Measurement") for every key.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "factor time (s) and solve N·RHS/s at N=2^20, 1/2/4/8 GPU; rel err vs oracle"
+CONFIG_NAME = ("config2: 2D Laplace double layer (identity_coef -1/2), ellipse a=2 b=1, "
+               "N=2^20, eps=1e-12, leaf 64, 16 RHS; config5: same factor, 1024 RHS")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=2 ** 20)
+    ap.add_argument("--eps", type=float, default=1e-12)
+    ap.add_argument("--nrhs", type=int, default=16)
+    ap.add_argument("--nrhs-big", type=int, default=1024)
+    ap.add_argument("--sample-n", type=int, default=16384,
+                    help="CPU oracle sample size (scaled linearly to --n)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-residual", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.3)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax = float(parts[2])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (test infrastructure: the cpu_baseline leg / --impl reference)
+
+def oracle_sample(n_s, eps, nrhs):
+    """Time the oracle's factor path (tree + compress + factor) and a
+    nrhs-solve on an n_s-point instance of the same workload."""
+    import numpy as np
+
+    import oracle
+    cur = oracle.ellipse(2.0, 1.0, n_s)
+    t0 = time.perf_counter()
+    T = oracle.build_tree(cur["xy"], 64)
+    src = oracle.BieSource(cur, T.perm)
+    oc = oracle.compress(src, T, eps)
+    of = oracle.factor(oc)
+    t1 = time.perf_counter()
+    B = np.random.default_rng(0).standard_normal((n_s, nrhs))
+    oracle.solve(of, B)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import warnings
+    warnings.simplefilter("ignore")
+    scale = args.n / args.sample_n
+    for _ in range(args.warmup):
+        oracle_sample(args.sample_n, args.eps, args.nrhs)
+    fts, sts = [], []
+    for _ in range(args.steps):
+        ft, stt = oracle_sample(args.sample_n, args.eps, args.nrhs)
+        fts.append(ft)
+        sts.append(stt)
+    ft = statistics.mean(fts) * scale
+    st = statistics.mean(sts)
+    cores = host_cores()
+    sample = (f"oracle/ (numpy+scipy restatement of skelkit, bit-exact vs the reference) on "
+              f"N={args.sample_n}, eps={args.eps:g}: tree+compress+factor, scaled x{scale:g} to "
+              f"N={args.n} (O(N) algorithm); O(p) neighbour lists (the as-shipped O(p^2) scan "
+              f"would add ~5900 s at 2^20, SURVEY F4)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ft, "unit": "s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * (statistics.mean(fts) + st),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (analytic ellipse nodes, seeded N(0,1) RHS)",
+        "config": {"workload": CONFIG_NAME, "n": args.n, "eps": args.eps, "nrhs": args.nrhs,
+                   "sample_n": args.sample_n, "l2": "n/a (CPU)"},
+        "solve": {"nrhs_per_s": args.sample_n * args.nrhs / st, "R": args.nrhs,
+                  "note": f"measured at N={args.sample_n}"},
+        "cpu_baseline": {"value": ft, "unit": "s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": ft, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# ours
+
+def fp64_peak(torch, lib, kind, iters=4096):
+    import ctypes
+    scratch = torch.zeros(4096, dtype=torch.float64, device="cuda")
+    fl = ctypes.c_double()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    best = 0.0
+    for _ in range(3):
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        rc = lib.skel_fp64_probe(kind, iters, ctypes.c_void_p(scratch.data_ptr()), ctypes.byref(fl), st)
+        e.record()
+        torch.cuda.synchronize()
+        if rc != 0:
+            return None
+        best = max(best, fl.value / (s.elapsed_time(e) * 1e-3) / 1e12)
+    return best
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_1110_3105_b200 as sk
+    from paper_1110_3105_b200 import _native, _profile
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    import warnings
+    warnings.simplefilter("ignore")
+    n, eps, R = args.n, args.eps, args.nrhs
+    curve = sk.bie.ellipse(2.0, 1.0, n)
+    system = sk.bie.discretize_dirichlet(curve, sk.KernelSpec("laplace", 2))
+    B_host = np.random.default_rng(0).standard_normal((n, R))
+    # RHS columns sharded across ranks (the factor is replicated per rank)
+    cols = np.array_split(np.arange(R), ws)[rank]
+    B_dev = torch.from_numpy(np.ascontiguousarray(B_host[:, cols])).to("cuda")
+    flush = torch.empty(512 * 2 ** 20 // 8, dtype=torch.float64, device="cuda")   # > 126 MB L2
+
+    def factor_step():
+        tree = sk.build_tree(system.points, 64)
+        src = sk.bie.BieSource(system, tree.perm)
+        cm = sk.compress_source(src, tree, eps)
+        return src, cm, sk.factor(cm)
+
+    for _ in range(args.warmup):
+        src, cm, fi = factor_step()
+        sk.solve_device(fi, B_dev)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    fts, sts = [], []
+    launches0 = _native.launch_count[0]
+    _profile.reset()
+    _profile.enabled = True
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        src, cm, fi = factor_step()
+        e1.record()
+        X = sk.solve_device(fi, B_dev)
+        e2.record()
+        torch.cuda.synchronize()
+        barrier()
+        fts.append(e0.elapsed_time(e1) * 1e-3)
+        sts.append(e1.elapsed_time(e2) * 1e-3)
+    _profile.enabled = False
+    launches = _native.launch_count[0] - launches0
+    clk = clocks.stop()
+    factor_s = max_over_ranks(statistics.mean(fts))
+    solve_s = max_over_ranks(statistics.mean(sts))
+
+    # roofline of the dominant kernel of the factor step, from the live events
+    kinds = {}
+    for kind in ("id_level", "factor_level", "sweep"):
+        cnt, ms, flops, nbytes = _profile.summary(kind)
+        kinds[kind] = (cnt, ms, flops, nbytes)
+    pk_dfma = fp64_peak(torch, _native.lib(), 0)
+    pk_dmma = fp64_peak(torch, _native.lib(), 1)
+    fp64_pk = max(v for v in (pk_dfma, pk_dmma) if v)
+    hbm_pk = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm_pk = float(json.load(f)["hbm_gbs"])
+        hbm_src = "MEASURED_PEAKS.json"
+    except Exception:
+        hbm_pk, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+    cnt, ms, flops, _ = kinds["id_level"]
+    ach = flops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+    roofline = {"kernel": "k_id_level (fused K1 assembly + K2 CPQR ID)", "bound": "fp64",
+                "achieved": ach, "peak": fp64_pk, "unit": "TFLOP/s", "frac": ach / fp64_pk,
+                "traffic": None, "launches": cnt, "avg_launch_ms": ms / max(cnt, 1),
+                "share_of_factor": (ms * 1e-3 / args.steps) / statistics.mean(fts),
+                "peak_source": f"measured live by bench.py: DFMA {pk_dfma:.1f}, DMMA {pk_dmma:.1f} TFLOP/s "
+                               "(MEASURED_PEAKS.json has no FP64 figure)",
+                "work": "SURVEY 8(d): per box 2x[4mnk-2k^2(m+n)+k^2(n-k)] + 10 flop/entry assembly"}
+    fc, fms, fflops, fbytes = kinds["factor_level"]
+    sc, sms, sflops, sbytes = kinds["sweep"]
+    roof_factor = {"kernel": "k_factor_level", "bound": "fp64", "launches": fc,
+                   "achieved": fflops / (fms * 1e-3) / 1e12 if fms else 0.0, "peak": fp64_pk,
+                   "unit": "TFLOP/s"}
+    roof_factor["frac"] = roof_factor["achieved"] / fp64_pk
+    roof_solve = {"kernel": "k_sweep_up/k_sweep_down (R=%d)" % len(cols), "bound": "hbm",
+                  "achieved": sbytes / (sms * 1e-3) / 1e9 if sms else 0.0, "peak": hbm_pk,
+                  "unit": "GB/s", "peak_source": hbm_src, "launches": sc}
+    roof_solve["frac"] = roof_solve["achieved"] / hbm_pk
+
+    # config 5: 1024 RHS on the same factorization, columns sharded across ranks
+    big = None
+    if args.nrhs_big > 0:
+        bc = np.array_split(np.arange(args.nrhs_big), ws)[rank].size
+        g = torch.Generator(device="cuda")
+        g.manual_seed(1234 + rank)
+        Bb = torch.randn((n, bc), dtype=torch.float64, device="cuda", generator=g)
+        sk.solve_device(fi, Bb)
+        torch.cuda.synchronize()
+        ts = []
+        _profile.reset()
+        _profile.enabled = True
+        for _ in range(max(2, min(args.steps, 4))):
+            barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            sk.solve_device(fi, Bb)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        _profile.enabled = False
+        _, bms, bflops, bbytes = _profile.summary("sweep")
+        tb = max_over_ranks(statistics.mean(ts))
+        big = {"R": args.nrhs_big, "nrhs_per_s": n * args.nrhs_big / tb, "ms": tb * 1e3,
+               "roofline": {"kernel": "k_sweep_up/k_sweep_down", "bound": "fp64",
+                            "achieved": bflops / (bms * 1e-3) / 1e12 if bms else 0.0,
+                            "peak": fp64_pk, "unit": "TFLOP/s"}}
+        big["roofline"]["frac"] = big["roofline"]["achieved"] / fp64_pk
+        del Bb
+
+    # end to end through the public API, host buffers in and out
+    e2e_ts = []
+    nrhs_local = len(cols)
+    B_pinned = torch.from_numpy(np.ascontiguousarray(B_host[:, cols])).pin_memory().numpy()
+    for it in range(max(1, args.steps)):
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        sys_e = sk.bie.discretize_dirichlet(sk.bie.Curve2D(curve.t, curve.xy, curve.normals,
+                                                           curve.curvature, curve.weights),
+                                            sk.KernelSpec("laplace", 2))
+        sigma, cm_e, fi_e = sk.bie.solve_dirichlet(sys_e, B_pinned, eps, 64)
+        torch.cuda.synchronize()
+        e2e_ts.append(time.perf_counter() - t0)
+        del cm_e, fi_e
+    e2e_s = max_over_ranks(statistics.mean(e2e_ts))
+    h2d = n * 8 * (2 + 2 + 1 + 1 + 1) + n * nrhs_local * 8
+    d2h = n * nrhs_local * 8
+
+    # correctness evidence at full size: residual against the exact operator
+    resid = None
+    if not args.no_residual and rank == 0:
+        xs = np.asarray(sigma)[:, :1]
+        y = sk.bie.dense_matvec(src, xs)
+        bcol = B_host[:, cols[:1]]
+        resid = float(np.linalg.norm(y - bcol) / np.linalg.norm(bcol))
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        ft, st_ = oracle_sample(args.sample_n, args.eps, R)
+        scale = args.n / args.sample_n
+        cpu = {"value": ft * scale, "unit": "s", "cores": host_cores(), "kind": "port",
+               "sample": f"oracle/ (bit-exact restatement of skelkit) tree+compress+factor at "
+                         f"N={args.sample_n}, eps={args.eps:g}, scaled x{scale:g} to N={args.n}; "
+                         f"16-RHS solve {args.sample_n * R / st_:.3e} N*RHS/s at that N",
+               "solve_nrhs_per_s": args.sample_n * R / st_}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": factor_s, "unit": "s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * (factor_s + solve_s),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic ellipse nodes, seeded N(0,1) RHS)",
+            "config": {"workload": CONFIG_NAME, "n": n, "eps": eps, "nrhs": R,
+                       "parallelism": ("single GPU" if ws == 1 else
+                                       f"factor replicated x{ws}, RHS columns sharded"),
+                       "l2": "512 MB buffer written between timed steps; factor data 1.9 GB > L2",
+                       "levels": cm.nlevels, "S": list(cm.S_shape()),
+                       "factor_bytes_per_point": fi.factor_bytes() / n},
+            "solve": {"R": R, "nrhs_per_s": n * R / solve_s, "ms": solve_s * 1e3},
+            "solve_1024": big,
+            "roofline": roofline,
+            "roofline_factor": roof_factor,
+            "roofline_solve": roof_solve,
+            "residual": resid,
+            "clocks": clk,
+            "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "what": "bie.solve_dirichlet(host geometry, host 16-RHS) -> host solution"},
+            "gpu_launches": launches,
+            "gpu_launches_per_step": launches / max(args.steps, 1),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

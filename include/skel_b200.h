@@ -254,6 +254,11 @@ int skel_tree_neighbors(void* handle, int32_t li, int64_t* off, int64_t* count,
                         int64_t* idx);
 int skel_tree_free(void* handle);
 
+/* FP64 throughput probe: kind 0 = DFMA chains, 1 = DMMA (mma.sync m8n8k4
+ * f64).  *flops receives the launch's flop count; time it with events. */
+int skel_fp64_probe(int32_t kind, int32_t iters, double* scratch, double* flops,
+                    void* stream);
+
 /* Library self-description (for the loader's symbol check). */
 const char* skel_version(void);
 int skel_device_query(int32_t* sm_count, int32_t* smem_optin, int32_t* cc_major,

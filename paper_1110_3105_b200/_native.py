@@ -91,9 +91,45 @@ _SIGS = {
     "skel_tree_neighbors": [c_vp, c_i32, c_vp, _P(c_i64), c_vp],
     "skel_tree_free": [c_vp],
     "skel_device_query": [_P(c_i32), _P(c_i32), _P(c_i32), _P(c_i32)],
+    "skel_fp64_probe": [c_i32, c_i32, c_vp, _P(c_f64), c_vp],
 }
 
 _lib = None
+
+# entry points that launch kernels (the tree builder / queries run on the host)
+_LAUNCHING = {"skel_id_level", "skel_assemble_S", "skel_eval_block", "skel_id_batched",
+              "skel_factor_level", "skel_dense_inverse", "skel_sweep_up_ex",
+              "skel_sweep_down_ex", "skel_dense_apply", "skel_permute_rows",
+              "skel_compact_i32", "skel_dense_matvec", "skel_fp64_probe"}
+launch_count = [0]
+
+
+class _CountingLib:
+    """Wraps the CDLL so every launching entry point is counted (bench.py
+    reports ``gpu_launches`` from this)."""
+
+    def __init__(self, cdll):
+        self._cdll = cdll
+        for name in _SIGS:
+            fn = getattr(cdll, name)
+            if name in _LAUNCHING:
+                setattr(self, name, self._wrap(name, fn))
+            else:
+                setattr(self, name, fn)
+        self.skel_version = cdll.skel_version
+
+    @staticmethod
+    def _wrap(name, fn):
+        def call(*args):
+            n = 1
+            if name == "skel_dense_matvec":
+                n = max(1, (int(args[3]) + 3) // 4)
+            elif name == "skel_id_level":
+                n = 1 if int(args[3]) > 0 else 0
+            launch_count[0] += n
+            return fn(*args)
+        call.__name__ = name
+        return call
 
 
 class NativeError(RuntimeError):
@@ -115,7 +151,7 @@ def lib():
             fn.restype = c_i32
         L.skel_version.restype = ctypes.c_char_p
         L.skel_version.argtypes = []
-        _lib = L
+        _lib = _CountingLib(L)
     return _lib
 
 

@@ -21,3 +21,54 @@ int skel_device_query(int32_t* sm_count, int32_t* smem_optin, int32_t* cc_major,
 }
 
 }  // extern "C"
+
+// ---- FP64 peak probes (bench.py's roofline denominator for FP64 kernels;
+// MEASURED_PEAKS.json carries only HBM and bf16 figures) --------------------
+__global__ void __launch_bounds__(256) k_dfma_probe(double* out, int iters) {
+  double a[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) a[c] = 1e-3 * (threadIdx.x + c);
+  const double b = 0.999999999, d = 1e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) a[c] = fma(a[c], b, d);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += a[c];
+  if (s == 12345.678) out[blockIdx.x] = s;  // keep the chains alive
+}
+
+__global__ void __launch_bounds__(256) k_dmma_probe(double* out, int iters) {
+  double acc[4][2];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) { acc[c][0] = 1e-3 * c; acc[c][1] = 2e-3 * c; }
+  const double av = 1e-3 * (threadIdx.x & 31), bv = 0.5;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(acc[c][0]), "+d"(acc[c][1])
+                   : "d"(av), "d"(bv));
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) s += acc[c][0] + acc[c][1];
+  if (s == 12345.678) out[blockIdx.x] = s;
+}
+
+extern "C" int skel_fp64_probe(int32_t kind, int32_t iters, double* scratch, double* flops,
+                               void* stream) {
+  int sms = skel_sm_count();
+  int blocks = sms * 8, threads = 256;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (kind == 0) {
+    k_dfma_probe<<<blocks, threads, 0, st>>>(scratch, iters);
+    *flops = 2.0 * 8.0 * (double)iters * blocks * threads;
+  } else {
+    k_dmma_probe<<<blocks, threads, 0, st>>>(scratch, iters);
+    *flops = 512.0 * 4.0 * (double)iters * blocks * (threads / 32);
+  }
+  return skel_last_error();
+}

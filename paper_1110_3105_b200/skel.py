@@ -19,7 +19,7 @@ from dataclasses import dataclass, replace
 
 import numpy as np
 
-from . import _native
+from . import _native, _profile
 from ._device import DeviceGeometry
 from .errors import InvalidInput, RefusedTooLarge
 from .geom import OrthTree, PointSet
@@ -353,6 +353,17 @@ def compress(spec: KernelSpec, points: PointSet, tree: OrthTree, eps, proxy=None
                            equalize_ranks=equalize_ranks, seed=seed, allow_large=allow_large)
 
 
+def id_level_flops(m0, m1, nr, nc, kr, kc, c_entry=10.0):
+    """Algorithmic flops of one box of skel_id_level: two CPQR
+    IDs, 4mnk - 2k^2(m+n) + k^2(n-k) each, plus entry assembly at c_entry
+    flops per entry (targets and D)."""
+    def one(m, n, k):
+        m, n, k = (np.asarray(v, dtype=np.float64) for v in (m, n, k))
+        return 4 * m * n * k - 2 * k * k * (m + n) + k * k * (n - k)
+    asm = c_entry * (np.asarray(m0) * nr + np.asarray(m1) * nc + np.asarray(nr) * nc)
+    return one(m0, nr, kr) + one(m1, nc, kc) + asm
+
+
 def _segment_sum(vals, off):
     cs = np.concatenate([[0], np.cumsum(vals)])
     return cs[off[1:]] - cs[off[:-1]]
@@ -469,6 +480,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         need_n = np.maximum(nr, nc)
         cls = np.searchsorted(np.array(_RPL_CLASSES), need_m, side="left")
         scratch_keep = []
+        recs = []
         for c in np.unique(cls):
             sel = np.nonzero(cls == c)[0]
             sel = sel[np.argsort(-(need_m[sel] * need_n[sel]), kind="stable")]
@@ -484,16 +496,26 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
                 lvd.scratch, lvd.scratch_bytes = None, 0
             order = up(sel.astype(np.int32))
             scratch_keep.append(order)
-            _native.check(L.skel_id_level(desc, lvd, p_(order), sel.size, max_m, max_n, field, st),
-                          f"skel_id_level (level {li})")
+            with _profile.timed("id_level", level=li, sel=sel) as rec:
+                _native.check(L.skel_id_level(desc, lvd, p_(order), sel.size, max_m, max_n, field, st),
+                              f"skel_id_level (level {li})")
+            if rec is not None:
+                recs.append(rec)
         kr = kr_t.cpu().numpy().astype(np.int64)
         kc = kc_t.cpu().numpy().astype(np.int64)
+        for rec in recs:
+            b = rec.meta["sel"]
+            rec.flops = float(id_level_flops(m0[b], m1[b], nr[b], nc[b], kr[b], kc[b]).sum())
+        recs.clear()
         fl = flags.cpu().numpy()
         if np.any(fl & 8):
             raise RuntimeError(f"level {li}: a box exceeds the kernel's neighbour/child limits")
-        for a in np.nonzero(fl & 3)[0]:
-            warnings.warn(f"interpolation matrix entries reach > 2 at level {li}, node {a}; "
-                          "pivoting quality degraded on this block", stacklevel=2)
+        bad = np.nonzero(fl & 3)[0]
+        if bad.size:
+            # lowrank.py:128-132 warns once per ID call; aggregated per level here
+            warnings.warn(f"interpolation matrix entries reach > 2 on {bad.size} block(s) at "
+                          f"level {li} (first node {bad[0]}); pivoting quality degraded",
+                          stacklevel=2)
         # compact the sorted skeletons: they are the next level's dof lists
         kro, kco = _off(kr), _off(kc)
         rsk = torch.empty(max(int(kro[-1]), 1), dtype=torch.int32, device=dev)

@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _native
+from . import _native, _profile
 from .errors import InvalidInput, SingularBlock
 from .skel import CompressedMatrix, _dense_apply, _off
 
@@ -202,7 +202,12 @@ def factor(cm: CompressedMatrix, regularize: float = 0.0) -> FactoredInverse:
         if need + 1024 > _smem_optin():
             scr = torch.empty(p * need // 8 + 1, dtype=torch.float64, device=dev)
             F.scratch, F.scratch_bytes = p_(scr), p * need
-        _native.check(L.skel_factor_level(F, max_n, max_k, field, st), f"skel_factor_level ({li})")
+        with _profile.timed("factor_level", level=li) as rec:
+            _native.check(L.skel_factor_level(F, max_n, max_k, field, st), f"skel_factor_level ({li})")
+        if rec is not None:
+            nf, kf = n.astype(np.float64), k.astype(np.float64)
+            rec.flops = float((2 * nf ** 3 + 6 * nf * nf * kf + 6 * kf * kf * nf + 2 * kf ** 3).sum())
+            rec.nbytes = float(((nf * nf + 2 * nf * kf) * 2 + kf * kf).sum()) * (16 if field else 8)
         sts = status.cpu().numpy()
         rd_h = rcd.cpu().numpy()
         rm_h = rcm.cpu().numpy()
@@ -281,6 +286,20 @@ def solve(fi: FactoredInverse, b):
     return x[:, 0] if single else x
 
 
+def _sweep_work(rec, d, Rn, field, up):
+    """Algorithmic flops / bytes of one sweep launch: factor
+    blocks read once, vectors read and written once."""
+    it = 16 if field else 8
+    fl = 4 if field else 1
+    n, k = d.n.astype(np.float64), d.k.astype(np.float64)
+    if up:
+        rec.flops = fl * 2.0 * Rn * float((n * k).sum())
+        rec.nbytes = it * float((n * k).sum() + Rn * (n.sum() + k.sum()))
+    else:
+        rec.flops = fl * 2.0 * Rn * float((n * n + n * k).sum())
+        rec.nbytes = it * float((n * n + n * k).sum() + Rn * (2 * n.sum() + k.sum()))
+
+
 def solve_device(fi: FactoredInverse, B):
     """Device-resident solve of an (N, R) CUDA tensor (original ordering)."""
     torch = _native.require_cuda()
@@ -300,19 +319,25 @@ def solve_device(fi: FactoredInverse, B):
         for lv in fi.levels:
             d = lv.dev
             nxt = torch.empty((int(d.k.sum()), Rn), dtype=B.dtype, device="cuda")
-            _native.check(L.skel_sweep_up_ex(d.p, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
-                                             p_(d.t_ld_off), p_(d.Rd), p_(u), p_(nxt), Rn, field,
-                                             d.max_n, st), "sweep_up")
+            with _profile.timed("sweep", dir="up") as rec:
+                _native.check(L.skel_sweep_up_ex(d.p, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
+                                                 p_(d.t_ld_off), p_(d.Rd), p_(u), p_(nxt), Rn, field,
+                                                 d.max_n, st), "sweep_up")
+            if rec is not None:
+                _sweep_work(rec, d, Rn, field, up=True)
             us.append(nxt)
             u = nxt
         v = _dense_apply(fi.S_inv, u, field) if (fi.S_inv is not None and u.shape[0]) else u
         for li in range(len(fi.levels) - 1, -1, -1):
             d = fi.levels[li].dev
             w = torch.empty((int(d.n.sum()), Rn), dtype=B.dtype, device="cuda")
-            _native.check(L.skel_sweep_down_ex(d.p, p_(d.t_n), p_(d.t_k), p_(d.t_noff),
-                                               p_(d.t_koff), p_(d.t_dd_off), p_(d.Dd),
-                                               p_(d.t_ld_off), p_(d.Ld), p_(us[li]), p_(v), p_(w),
-                                               Rn, field, d.max_nk, st), "sweep_down")
+            with _profile.timed("sweep", dir="down") as rec:
+                _native.check(L.skel_sweep_down_ex(d.p, p_(d.t_n), p_(d.t_k), p_(d.t_noff),
+                                                   p_(d.t_koff), p_(d.t_dd_off), p_(d.Dd),
+                                                   p_(d.t_ld_off), p_(d.Ld), p_(us[li]), p_(v), p_(w),
+                                                   Rn, field, d.max_nk, st), "sweep_down")
+            if rec is not None:
+                _sweep_work(rec, d, Rn, field, up=False)
             v = w
         xt = v
     X = torch.empty_like(xt)
