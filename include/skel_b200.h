@@ -185,6 +185,9 @@ typedef struct {
   double* rcond_m;
   void* scratch;
   int64_t scratch_bytes;
+  /* optional subset: process boxes order[0..nrun) (NULL: all nbox boxes) */
+  const int32_t* order;
+  int32_t nrun;
 } SkelFactorLevel;
 
 /* factor_node over every box of one level (solver.py:224-262). */

@@ -64,6 +64,7 @@ class SkelFactorLevel(ctypes.Structure):
         ("Dd", c_vp), ("Ld", c_vp), ("Rd", c_vp), ("Lam", c_vp),
         ("status", c_vp), ("rcond_d", c_vp), ("rcond_m", c_vp),
         ("scratch", c_vp), ("scratch_bytes", c_i64),
+        ("order", c_vp), ("nrun", c_i32),
     ]
 
 

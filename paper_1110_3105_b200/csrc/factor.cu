@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) k_factor_level(const SkelFactorLevel F, i
   const size_t hdr = 512 + ((sizeof(int) * (size_t)max_n + 15) / 16) * 16;
   T* base = GW ? reinterpret_cast<T*>(F.scratch) + (size_t)blockIdx.x * fac_elems<T>(max_n, max_k)
                : reinterpret_cast<T*>(smem + hdr);
-  const int a = blockIdx.x;
+  const int a = F.order ? F.order[blockIdx.x] : blockIdx.x;
   const int n = F.n[a], k = F.k[a];
   if (n == 0) {
     if (threadIdx.x == 0) { F.status[a] = 0; F.rcond_d[a] = 1.0; F.rcond_m[a] = 1.0; }
@@ -257,20 +257,21 @@ __global__ void __launch_bounds__(256) k_factor_level(const SkelFactorLevel F, i
 
 template <class T>
 static int factor_level_impl(const SkelFactorLevel* F, int max_n, int max_k, cudaStream_t st) {
-  if (F->nbox <= 0) return 0;
+  const int nrun = F->order ? F->nrun : F->nbox;
+  if (nrun <= 0) return 0;
   if (max_n < 1) max_n = 1;
   size_t hdr = 512 + ((sizeof(int) * (size_t)max_n + 15) / 16) * 16;
   size_t need = hdr + fac_elems<T>(max_n, max_k) * sizeof(T);
   if (need <= (size_t)skel_smem_optin()) {
     auto kern = k_factor_level<T, false>;
     SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
-    kern<<<F->nbox, 256, need, st>>>(*F, max_n, max_k);
+    kern<<<nrun, 256, need, st>>>(*F, max_n, max_k);
   } else {
-    if (!F->scratch || (size_t)F->scratch_bytes < (size_t)F->nbox * fac_elems<T>(max_n, max_k) * sizeof(T))
+    if (!F->scratch || (size_t)F->scratch_bytes < (size_t)nrun * fac_elems<T>(max_n, max_k) * sizeof(T))
       return -2;
     auto kern = k_factor_level<T, true>;
     SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hdr));
-    kern<<<F->nbox, 256, hdr, st>>>(*F, max_n, max_k);
+    kern<<<nrun, 256, hdr, st>>>(*F, max_n, max_k);
   }
   return skel_last_error();
 }

@@ -1,21 +1,170 @@
 // tree.cpp -- native host builder of the adaptive orthtree, its covers and the
 // same-cover neighbour lists (K7).
 //
-// Restates geom.py:118-184 (centre splits, ties to the upper child, pruning,
-// DFS node numbering and permutation, covers with early leaves repeated) and
-// replaces level_neighbors (geom.py:205-219), which is O(p^2) in the
-// reference, by an O(p) grid-hash candidate search followed by the identical
-// predicate _boxes_touch (geom.py:187-189), so the lists are equal.
+// Restates geom.py:118-184: root = padded bounding cube, centre splits with
+// ties to the upper child, empty children pruned, subdivision stops at
+// <= max_leaf points (or depth 60), DFS preorder node numbering and point
+// permutation, covers with early leaves repeated at finer levels.
+//
+// Build: in-place stable counting sort of each node's point range into its
+// 2^d children (coordinates are permuted alongside the indices so every pass
+// streams), top levels serial, the subtrees below a frontier depth built in
+// parallel on host threads and spliced back in preorder.
+//
+// Neighbours replace the reference's O(p^2) level_neighbors (geom.py:205-219)
+// by a top-down O(p) search: two boxes of a cover can only touch if their
+// cover-parents are equal or touch, so the candidates of a box are the
+// children of its parent's neighbours; the reference predicate _boxes_touch
+// (geom.py:187-189) then decides, and lists come out sorted -- identical to
+// the reference's lists.
 #include <algorithm>
+#include <array>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <thread>
 #include <utility>
 #include <vector>
 
 #include "../../include/skel_b200.h"
 
 namespace {
+
+constexpr double kRootPad = 1e-12;
+constexpr int kMaxDepth = 60;
+
+struct NodeRec {
+  double c[3];
+  double hw;
+  int64_t lo, hi, depth, parent;  // parent: local index within the owning list
+  int64_t nchild;
+};
+
+struct Builder {
+  int d;
+  int64_t max_leaf;
+  std::vector<int64_t>* perm;  // tree position -> original index
+  double* px[3];               // coordinates in tree order (permuted alongside)
+  std::vector<int64_t>* tmpi;
+  std::vector<double>* tmpx[3];
+  std::vector<uint8_t>* code;
+
+  int nthreads = 1;
+
+  // parallel stable counting sort of a large range (chunked per thread)
+  void split_par(int64_t lo, int64_t hi, const double* cen, int64_t cnt[8]) {
+    const int nk = 1 << d;
+    const int T = nthreads;
+    const int64_t len = hi - lo, chunk = (len + T - 1) / T;
+    std::vector<std::array<int64_t, 8>> cc(T);
+    uint8_t* cd = code->data();
+    auto count = [&](int t) {
+      std::array<int64_t, 8>& c = cc[t];
+      c.fill(0);
+      const int64_t a0 = lo + t * chunk, a1 = std::min(hi, a0 + chunk);
+      for (int64_t i = a0; i < a1; ++i) {
+        int k = 0;
+        for (int a = 0; a < d; ++a) k |= (px[a][i] >= cen[a] ? 1 : 0) << a;
+        cd[i] = (uint8_t)k;
+        c[k]++;
+      }
+    };
+    {
+      std::vector<std::thread> th;
+      for (int t = 0; t < T; ++t) th.emplace_back(count, t);
+      for (auto& x : th) x.join();
+    }
+    std::vector<std::array<int64_t, 8>> st(T);
+    int64_t s = lo;
+    for (int k = 0; k < nk; ++k) {
+      cnt[k] = 0;
+      for (int t = 0; t < T; ++t) {
+        st[t][k] = s;
+        s += cc[t][k];
+        cnt[k] += cc[t][k];
+      }
+    }
+    int64_t* P = perm->data();
+    int64_t* TI = tmpi->data();
+    auto scatter = [&](int t) {
+      std::array<int64_t, 8> pos = st[t];
+      const int64_t a0 = lo + t * chunk, a1 = std::min(hi, a0 + chunk);
+      for (int64_t i = a0; i < a1; ++i) {
+        int64_t dst = pos[cd[i]]++;
+        TI[dst] = P[i];
+        for (int a = 0; a < d; ++a) (*tmpx[a])[dst] = px[a][i];
+      }
+    };
+    {
+      std::vector<std::thread> th;
+      for (int t = 0; t < T; ++t) th.emplace_back(scatter, t);
+      for (auto& x : th) x.join();
+    }
+    auto copyback = [&](int t) {
+      const int64_t a0 = lo + t * chunk, a1 = std::min(hi, a0 + chunk);
+      if (a1 <= a0) return;
+      std::memcpy(P + a0, TI + a0, (a1 - a0) * sizeof(int64_t));
+      for (int a = 0; a < d; ++a) std::memcpy(px[a] + a0, tmpx[a]->data() + a0, (a1 - a0) * sizeof(double));
+    };
+    {
+      std::vector<std::thread> th;
+      for (int t = 0; t < T; ++t) th.emplace_back(copyback, t);
+      for (auto& x : th) x.join();
+    }
+  }
+
+  // split [lo, hi) of node `cen/hw` into children ranges; returns counts
+  void split(int64_t lo, int64_t hi, const double* cen, int64_t cnt[8]) {
+    if (nthreads > 1 && hi - lo >= (int64_t)1 << 17) {
+      split_par(lo, hi, cen, cnt);
+      return;
+    }
+    const int nk = 1 << d;
+    for (int c = 0; c < nk; ++c) cnt[c] = 0;
+    uint8_t* cd = code->data();
+    for (int64_t t = lo; t < hi; ++t) {
+      int k = 0;
+      for (int a = 0; a < d; ++a) k |= (px[a][t] >= cen[a] ? 1 : 0) << a;
+      cd[t] = (uint8_t)k;
+      cnt[k]++;
+    }
+    int64_t start[8];
+    int64_t s = lo;
+    for (int c = 0; c < nk; ++c) { start[c] = s; s += cnt[c]; }
+    int64_t* P = perm->data();
+    int64_t* TI = tmpi->data();
+    for (int64_t t = lo; t < hi; ++t) {
+      int64_t dst = start[cd[t]]++;
+      TI[dst] = P[t];
+      for (int a = 0; a < d; ++a) (*tmpx[a])[dst] = px[a][t];
+    }
+    std::memcpy(P + lo, TI + lo, (hi - lo) * sizeof(int64_t));
+    for (int a = 0; a < d; ++a) std::memcpy(px[a] + lo, tmpx[a]->data() + lo, (hi - lo) * sizeof(double));
+  }
+
+  // serial preorder build of a subtree into `out` (parent indices local)
+  void build_sub(std::vector<NodeRec>& out, int64_t lo, int64_t hi, const double* cen, double hw,
+                 int64_t depth, int64_t parent) {
+    const int64_t me = (int64_t)out.size();
+    NodeRec r;
+    for (int a = 0; a < 3; ++a) r.c[a] = a < d ? cen[a] : 0.0;
+    r.hw = hw; r.lo = lo; r.hi = hi; r.depth = depth; r.parent = parent; r.nchild = 0;
+    out.push_back(r);
+    if (hi - lo <= max_leaf || depth >= kMaxDepth) return;
+    int64_t cnt[8];
+    split(lo, hi, cen, cnt);
+    int64_t s = lo;
+    for (int c = 0; c < (1 << d); ++c) {
+      if (cnt[c] == 0) continue;
+      double cc[3];
+      for (int a = 0; a < d; ++a) cc[a] = cen[a] + (((c >> a) & 1) ? 0.5 : -0.5) * hw;
+      out[me].nchild += 1;
+      build_sub(out, s, s + cnt[c], cc, 0.5 * hw, depth + 1, me);
+      s += cnt[c];
+    }
+  }
+};
 
 struct Tree {
   int dim = 2;
@@ -24,37 +173,29 @@ struct Tree {
   std::vector<double> hw;
   std::vector<int64_t> lo, hi, depth, parent, nchild;
   std::vector<int64_t> perm;
-  std::vector<std::vector<int64_t>> covers;  // finest first
-  std::vector<std::vector<int64_t>> nbr_off, nbr_idx;  // per cover, lazily
-  std::vector<char> nbr_done;
+  std::vector<std::vector<int64_t>> covers;             // finest first
+  std::vector<std::vector<int64_t>> nbr_off, nbr_idx;   // per cover
+  bool nbr_done = false;
 };
 
-constexpr double kRootPad = 1e-12;
-constexpr int kMaxDepth = 60;
-
-struct Frame {
-  std::vector<int64_t> idx;
-  double c[3];
-  double hw;
-  int64_t depth;
-  int64_t parent;
+// Item of the serial top part: a node, or a subtree task spliced in later.
+struct TopItem {
+  bool task;
+  NodeRec rec;        // node record (task: root geometry)
+  int64_t parent_item;
 };
 
 void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
   T.dim = d;
   T.n = n;
-  double lo_c[3], hi_c[3], c0[3];
-  for (int a = 0; a < d; ++a) {
-    lo_c[a] = INFINITY;
-    hi_c[a] = -INFINITY;
-  }
+  double lo_c[3] = {INFINITY, INFINITY, INFINITY}, hi_c[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int64_t i = 0; i < n; ++i)
     for (int a = 0; a < d; ++a) {
       double v = X[i * d + a];
       lo_c[a] = std::min(lo_c[a], v);
       hi_c[a] = std::max(hi_c[a], v);
     }
-  double ext = 0.0, cabs = 0.0;
+  double c0[3] = {0, 0, 0}, ext = 0.0, cabs = 0.0;
   for (int a = 0; a < d; ++a) {
     c0[a] = 0.5 * (lo_c[a] + hi_c[a]);
     ext = std::max(ext, hi_c[a] - lo_c[a]);
@@ -64,149 +205,184 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
   double scale = std::max(std::max(hw0, cabs), 1.0);
   hw0 = hw0 * (1.0 + kRootPad) + kRootPad * scale;
 
-  T.perm.assign(n, 0);
-  int64_t cursor = 0;
-  std::vector<Frame> stack;
-  Frame root;
-  root.idx.resize(n);
-  for (int64_t i = 0; i < n; ++i) root.idx[i] = i;
-  for (int a = 0; a < d; ++a) root.c[a] = c0[a];
-  root.hw = hw0;
-  root.depth = 0;
-  root.parent = -1;
-  stack.push_back(std::move(root));
-  const int nkids = 1 << d;
-  while (!stack.empty()) {
-    Frame f = std::move(stack.back());
-    stack.pop_back();
-    const int64_t me = (int64_t)T.hw.size();
-    for (int a = 0; a < d; ++a) T.center.push_back(f.c[a]);
-    T.hw.push_back(f.hw);
-    T.lo.push_back(cursor);
-    T.hi.push_back(cursor + (int64_t)f.idx.size());
-    T.depth.push_back(f.depth);
-    T.parent.push_back(f.parent);
-    T.nchild.push_back(0);
-    if (f.parent >= 0) T.nchild[f.parent] += 1;
-    const int64_t sz = (int64_t)f.idx.size();
-    if (sz <= max_leaf || f.depth >= kMaxDepth) {
-      for (int64_t t = 0; t < sz; ++t) T.perm[cursor + t] = f.idx[t];
-      cursor += sz;
-      continue;
-    }
-    std::vector<std::vector<int64_t>> parts(nkids);
-    for (int64_t t = 0; t < sz; ++t) {
-      const int64_t i = f.idx[t];
-      int code = 0;
-      for (int a = 0; a < d; ++a) code |= (X[i * d + a] >= f.c[a] ? 1 : 0) << a;
-      parts[code].push_back(i);
-    }
-    std::vector<Frame> kids;
-    for (int c = 0; c < nkids; ++c) {
-      if (parts[c].empty()) continue;
-      Frame k;
-      k.idx = std::move(parts[c]);
-      for (int a = 0; a < d; ++a) k.c[a] = f.c[a] + (((c >> a) & 1) ? 0.5 : -0.5) * f.hw;
-      k.hw = 0.5 * f.hw;
-      k.depth = f.depth + 1;
-      k.parent = me;
-      kids.push_back(std::move(k));
-    }
-    for (auto it = kids.rbegin(); it != kids.rend(); ++it) stack.push_back(std::move(*it));
+  std::vector<int64_t> perm(n), tmpi(n);
+  std::vector<double> pxv[3], tmpx[3];
+  for (int a = 0; a < d; ++a) {
+    pxv[a].resize(n);
+    tmpx[a].resize(n);
+    for (int64_t i = 0; i < n; ++i) pxv[a][i] = X[i * d + a];
   }
-  const int64_t nn = (int64_t)T.hw.size();
+  for (int64_t i = 0; i < n; ++i) perm[i] = i;
+  std::vector<uint8_t> code(n);
+  Builder B;
+  B.d = d;
+  B.max_leaf = max_leaf;
+  B.perm = &perm;
+  B.tmpi = &tmpi;
+  B.code = &code;
+  for (int a = 0; a < 3; ++a) {
+    B.px[a] = a < d ? pxv[a].data() : nullptr;
+    B.tmpx[a] = &tmpx[a];
+  }
+
+  // serial top part down to a frontier with enough subtrees for the threads
+  unsigned hwc = std::thread::hardware_concurrency();
+  const int nthreads = (int)std::max(1u, std::min(hwc == 0 ? 1u : hwc, 32u));
+  B.nthreads = nthreads;
+  const int64_t frontier_size = std::max<int64_t>(4 * max_leaf, n / (8 * nthreads));
+  std::vector<TopItem> items;
+  struct Fr { int64_t lo, hi; double c[3]; double hw; int64_t depth, parent_item; };
+  std::vector<Fr> stack;
+  stack.push_back({0, n, {c0[0], c0[1], c0[2]}, hw0, 0, -1});
+  while (!stack.empty()) {
+    Fr f = stack.back();
+    stack.pop_back();
+    TopItem it;
+    for (int a = 0; a < 3; ++a) it.rec.c[a] = f.c[a];
+    it.rec.hw = f.hw; it.rec.lo = f.lo; it.rec.hi = f.hi; it.rec.depth = f.depth;
+    it.rec.parent = -1; it.rec.nchild = 0;
+    it.parent_item = f.parent_item;
+    const int64_t sz = f.hi - f.lo;
+    const bool leaf = sz <= max_leaf || f.depth >= kMaxDepth;
+    it.task = !leaf && sz <= frontier_size;
+    const int64_t me = (int64_t)items.size();
+    if (f.parent_item >= 0) items[f.parent_item].rec.nchild += 1;
+    items.push_back(it);
+    if (leaf || it.task) continue;
+    int64_t cnt[8];
+    B.split(f.lo, f.hi, f.c, cnt);
+    std::vector<Fr> kids;
+    int64_t s = f.lo;
+    for (int c = 0; c < (1 << d); ++c) {
+      if (cnt[c] == 0) continue;
+      Fr k;
+      for (int a = 0; a < 3; ++a) k.c[a] = a < d ? f.c[a] + (((c >> a) & 1) ? 0.5 : -0.5) * f.hw : 0.0;
+      k.lo = s; k.hi = s + cnt[c]; k.hw = 0.5 * f.hw; k.depth = f.depth + 1; k.parent_item = me;
+      kids.push_back(k);
+      s += cnt[c];
+    }
+    for (auto it2 = kids.rbegin(); it2 != kids.rend(); ++it2) stack.push_back(*it2);
+  }
+  // parallel subtrees (ranges are disjoint, so the in-place sorts do not race)
+  std::vector<int64_t> task_ids;
+  for (int64_t i = 0; i < (int64_t)items.size(); ++i)
+    if (items[i].task) task_ids.push_back(i);
+  std::vector<std::vector<NodeRec>> sub(task_ids.size());
+  {
+    std::vector<std::thread> pool;
+    std::atomic_int next(0);
+    auto worker = [&]() {
+      for (;;) {
+        int t = next.fetch_add(1);
+        if (t >= (int)task_ids.size()) break;
+        const NodeRec& r = items[task_ids[t]].rec;
+        B.build_sub(sub[t], r.lo, r.hi, r.c, r.hw, r.depth, -1);
+      }
+    };
+    int nt = std::min<int>(nthreads, (int)task_ids.size());
+    for (int i = 0; i < nt; ++i) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+  }
+  // splice in preorder
+  std::vector<int64_t> item_gid(items.size());
+  int64_t gid = 0;
+  size_t tk = 0;
+  for (size_t i = 0; i < items.size(); ++i) {
+    item_gid[i] = gid;
+    gid += items[i].task ? (int64_t)sub[tk++].size() : 1;
+  }
+  const int64_t nn = gid;
+  T.center.resize(nn * d);
+  T.hw.resize(nn);
+  T.lo.resize(nn);
+  T.hi.resize(nn);
+  T.depth.resize(nn);
+  T.parent.resize(nn);
+  T.nchild.resize(nn);
+  auto put = [&](int64_t g, const NodeRec& r, int64_t par) {
+    for (int a = 0; a < d; ++a) T.center[g * d + a] = r.c[a];
+    T.hw[g] = r.hw; T.lo[g] = r.lo; T.hi[g] = r.hi; T.depth[g] = r.depth;
+    T.parent[g] = par; T.nchild[g] = r.nchild;
+  };
+  tk = 0;
+  for (size_t i = 0; i < items.size(); ++i) {
+    const int64_t par = items[i].parent_item >= 0 ? item_gid[items[i].parent_item] : -1;
+    if (!items[i].task) {
+      put(item_gid[i], items[i].rec, par);
+    } else {
+      const std::vector<NodeRec>& s = sub[tk++];
+      const int64_t base = item_gid[i];
+      for (size_t j = 0; j < s.size(); ++j)
+        put(base + (int64_t)j, s[j], j == 0 ? par : base + s[j].parent);
+    }
+  }
+  T.perm = std::move(perm);
+  // covers in id order == sorted by range start (preorder, disjoint ranges)
   int64_t maxd = 0;
   for (int64_t i = 0; i < nn; ++i) maxd = std::max(maxd, T.depth[i]);
+  T.covers.assign(maxd + 1, {});
   for (int64_t f = maxd; f >= 0; --f) {
-    std::vector<int64_t> cov;
+    std::vector<int64_t>& cov = T.covers[maxd - f];
     for (int64_t i = 0; i < nn; ++i)
       if (T.depth[i] == f || (T.nchild[i] == 0 && T.depth[i] < f)) cov.push_back(i);
-    std::stable_sort(cov.begin(), cov.end(),
-                     [&](int64_t x, int64_t y) { return T.lo[x] < T.lo[y]; });
-    T.covers.push_back(std::move(cov));
   }
-  T.nbr_off.resize(T.covers.size());
-  T.nbr_idx.resize(T.covers.size());
-  T.nbr_done.assign(T.covers.size(), 0);
 }
 
-void neighbors(Tree& T, int li) {
-  if (T.nbr_done[li]) return;
-  const std::vector<int64_t>& ids = T.covers[li];
-  const int64_t p = (int64_t)ids.size();
+inline bool touch(const Tree& T, int64_t na, int64_t nb, double tol) {
   const int d = T.dim;
-  std::vector<int64_t>& off = T.nbr_off[li];
-  std::vector<int64_t>& idx = T.nbr_idx[li];
-  off.assign(p + 1, 0);
-  idx.clear();
-  T.nbr_done[li] = 1;
-  if (p < 2) return;
+  for (int a = 0; a < d; ++a) {
+    double gap = std::fabs(T.center[na * d + a] - T.center[nb * d + a]) - (T.hw[na] + T.hw[nb]);
+    if (!(gap <= tol)) return false;
+  }
+  return true;
+}
+
+void all_neighbors(Tree& T) {
+  if (T.nbr_done) return;
+  const int nc = (int)T.covers.size();
+  T.nbr_off.assign(nc, {});
+  T.nbr_idx.assign(nc, {});
   const double tol = 1e-9 * T.hw[0];
-  double hmin = INFINITY;
-  for (int64_t a = 0; a < p; ++a) hmin = std::min(hmin, T.hw[ids[a]]);
-  const double cell = 2.0 * hmin;
-  double origin[3];
-  for (int a = 0; a < d; ++a) origin[a] = T.center[a] - T.hw[0] - 2.0 * cell;
-  std::vector<int64_t> clo(p * d), chi(p * d);
-  int64_t gdim = 1;
-  for (int64_t b = 0; b < p; ++b) {
-    const int64_t nd = ids[b];
-    for (int a = 0; a < d; ++a) {
-      const double c = T.center[nd * d + a], h = T.hw[nd];
-      clo[b * d + a] = (int64_t)std::floor((c - h - tol - origin[a]) / cell);
-      chi[b * d + a] = (int64_t)std::floor((c + h + tol - origin[a]) / cell);
-      gdim = std::max(gdim, chi[b * d + a] + 2);
+  // top cover(s) with a single node: no neighbours
+  for (int li = nc - 1; li >= 0; --li) {
+    const std::vector<int64_t>& ids = T.covers[li];
+    const int64_t p = (int64_t)ids.size();
+    std::vector<int64_t>& off = T.nbr_off[li];
+    std::vector<int64_t>& idx = T.nbr_idx[li];
+    off.assign(p + 1, 0);
+    idx.clear();
+    if (li == nc - 1 || p < 2) continue;
+    // cover parent of every node: the node of cover li+1 containing it
+    const std::vector<int64_t>& up = T.covers[li + 1];
+    const int64_t q = (int64_t)up.size();
+    std::vector<int64_t> cstart(q + 1);  // children runs of cover li+1 in cover li
+    int64_t j = 0;
+    for (int64_t u = 0; u < q; ++u) {
+      cstart[u] = j;
+      while (j < p && T.lo[ids[j]] < T.hi[up[u]]) ++j;
+    }
+    cstart[q] = p;
+    std::vector<int64_t> par(p);
+    for (int64_t u = 0; u < q; ++u)
+      for (int64_t t = cstart[u]; t < cstart[u + 1]; ++t) par[t] = u;
+    const std::vector<int64_t>& uoff = T.nbr_off[li + 1];
+    const std::vector<int64_t>& uidx = T.nbr_idx[li + 1];
+    std::vector<int64_t> cand;
+    for (int64_t a = 0; a < p; ++a) {
+      cand.clear();
+      const int64_t u = par[a];
+      auto take = [&](int64_t w) {
+        for (int64_t t = cstart[w]; t < cstart[w + 1]; ++t)
+          if (t != a && touch(T, ids[a], ids[t], tol)) cand.push_back(t);
+      };
+      take(u);
+      for (int64_t s = uoff[u]; s < uoff[u + 1]; ++s) take(uidx[s]);
+      std::sort(cand.begin(), cand.end());
+      idx.insert(idx.end(), cand.begin(), cand.end());
+      off[a + 1] = (int64_t)idx.size();
     }
   }
-  // (cell key, box) registrations
-  std::vector<std::pair<int64_t, int64_t>> reg;
-  for (int64_t b = 0; b < p; ++b) {
-    int64_t span[3] = {1, 1, 1}, tot = 1;
-    for (int a = 0; a < d; ++a) {
-      span[a] = chi[b * d + a] - clo[b * d + a] + 1;
-      tot *= span[a];
-    }
-    for (int64_t t = 0; t < tot; ++t) {
-      int64_t rem = t, key = 0;
-      for (int a = 0; a < d; ++a) {
-        key = key * gdim + clo[b * d + a] + rem % span[a];
-        rem /= span[a];
-      }
-      reg.emplace_back(key, b);
-    }
-  }
-  std::sort(reg.begin(), reg.end());
-  std::vector<std::pair<int64_t, int64_t>> pairs;
-  size_t s = 0;
-  while (s < reg.size()) {
-    size_t e = s;
-    while (e < reg.size() && reg[e].first == reg[s].first) ++e;
-    for (size_t u = s; u < e; ++u)
-      for (size_t v = u + 1; v < e; ++v) pairs.emplace_back(reg[u].second, reg[v].second);
-    s = e;
-  }
-  std::sort(pairs.begin(), pairs.end());
-  pairs.erase(std::unique(pairs.begin(), pairs.end()), pairs.end());
-  std::vector<std::pair<int64_t, int64_t>> adj;
-  for (auto& pr : pairs) {
-    const int64_t na = ids[pr.first], nb = ids[pr.second];
-    bool touch = true;
-    for (int a = 0; a < d && touch; ++a) {
-      double gap = std::fabs(T.center[na * d + a] - T.center[nb * d + a]) - (T.hw[na] + T.hw[nb]);
-      touch = gap <= tol;
-    }
-    if (touch) {
-      adj.emplace_back(pr.first, pr.second);
-      adj.emplace_back(pr.second, pr.first);
-    }
-  }
-  std::sort(adj.begin(), adj.end());
-  idx.resize(adj.size());
-  for (size_t t = 0; t < adj.size(); ++t) {
-    off[adj[t].first + 1] += 1;
-    idx[t] = adj[t].second;
-  }
-  for (int64_t b = 0; b < p; ++b) off[b + 1] += off[b];
+  T.nbr_done = true;
 }
 
 }  // namespace
@@ -256,7 +432,7 @@ int skel_tree_cover(void* handle, int32_t li, int64_t* count, int64_t* ids) {
 int skel_tree_neighbors(void* handle, int32_t li, int64_t* off, int64_t* count, int64_t* idx) {
   Tree* T = (Tree*)handle;
   if (!T || li < 0 || li >= (int32_t)T->covers.size()) return -1;
-  neighbors(*T, li);
+  all_neighbors(*T);
   *count = (int64_t)T->nbr_idx[li].size();
   if (off) std::memcpy(off, T->nbr_off[li].data(), T->nbr_off[li].size() * sizeof(int64_t));
   if (idx) std::memcpy(idx, T->nbr_idx[li].data(), T->nbr_idx[li].size() * sizeof(int64_t));

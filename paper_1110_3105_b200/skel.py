@@ -24,11 +24,13 @@ from ._device import DeviceGeometry
 from .errors import InvalidInput, RefusedTooLarge
 from .geom import OrthTree, PointSet
 from .kernels import KernelSpec
+from ._staging import Packer, fork, join
 
 DEFAULT_N_PROXY = {2: 64, 3: 512}        # skel.py:29
 _RANDOMIZED_CUTOFF = 4096                # skel.py:33
 GLOBAL_MODE_LIMIT = 20000                # skel.py:35
-_RPL_CLASSES = (128, 256, 384, 512, 768)
+# target-size classes (bytes of the m x n target) -> one launch each
+_W_CLASSES = (24 << 10, 48 << 10, 80 << 10, 112 << 10, 160 << 10, 216 << 10)
 
 
 @dataclass
@@ -159,12 +161,12 @@ def _off(counts):
 
 class DevLevel:
     """Device slabs of one compressed level (capacity layouts addressed by
-    per-box element offsets)."""
+    per-box element offsets).  ``t`` holds the device index arrays (one
+    packed upload per level)."""
 
     def __init__(self, li, nr, nc, kr, kc, d_off, l_off, r_off, D, L, R, rskel, cskel, child_off,
-                 dtype):
-        torch = _native.require_cuda()
-        dev = torch.device("cuda")
+                 dtype, t=None):
+        from ._staging import Packer
         self.li = li
         self.p = nr.size
         self.nr, self.nc = nr.astype(np.int64), nc.astype(np.int64)
@@ -174,16 +176,22 @@ class DevLevel:
         self.rskel, self.cskel = rskel, cskel          # compacted, int32, device
         self.child_off = child_off
         self.dtype = dtype
-        up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
-        self.t_d_off, self.t_l_off, self.t_r_off = up(d_off), up(l_off), up(r_off)
-        self.t_nr = up(self.nr.astype(np.int32))
-        self.t_kr = up(self.kr.astype(np.int32))
-        self.t_kc = up(self.kc.astype(np.int32))
-        self.t_rdof_off = up(_off(self.nr))
-        self.t_cdof_off = up(_off(self.nc))
-        self.t_kr_off = up(_off(self.kr))
-        self.t_kc_off = up(_off(self.kc))
-        self.t_child_off = None if child_off is None else up(child_off)
+        if t is None:
+            pk = Packer()
+            pk.add("d_off", d_off).add("l_off", l_off).add("r_off", r_off)
+            pk.add("nr", self.nr.astype(np.int32)).add("kr", self.kr.astype(np.int32))
+            pk.add("kc", self.kc.astype(np.int32))
+            pk.add("rdof_off", _off(self.nr)).add("cdof_off", _off(self.nc))
+            pk.add("kr_off", _off(self.kr)).add("kc_off", _off(self.kc))
+            if child_off is not None:
+                pk.add("child_off", child_off)
+            t = pk.upload()
+        self.t = t
+        self.t_d_off, self.t_l_off, self.t_r_off = t["d_off"], t["l_off"], t["r_off"]
+        self.t_nr, self.t_kr, self.t_kc = t["nr"], t["kr"], t["kc"]
+        self.t_rdof_off, self.t_cdof_off = t["rdof_off"], t["cdof_off"]
+        self.t_kr_off, self.t_kc_off = t["kr_off"], t["kc_off"]
+        self.t_child_off = t.get("child_off")
 
 
 class CompressedLevel:
@@ -413,6 +421,8 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
     levels = []
     prev = None
     optin = _smem_optin()
+    elem = 16 if field else 8
+    allpos = torch.arange(n, dtype=torch.int32, device=dev)
     for li in range(top):
         ids = covers[li]
         p = ids.size
@@ -420,8 +430,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         if li == 0:
             nr = (tree.hi[ids] - tree.lo[ids]).astype(np.int64)
             nc = nr.copy()
-            rdofs = torch.arange(n, dtype=torch.int32, device=dev)
-            cdofs = rdofs
+            rdofs = cdofs = allpos
             child_off = None
         else:
             child_off = tree.cover_children(li)
@@ -429,8 +438,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             nc = _segment_sum(prev.kc, child_off)
             rdofs, cdofs = prev.rskel, prev.cskel
         rdof_off, cdof_off = _off(nr), _off(nc)
-        hw = tree.hw[ids]
-        rad = cfg.radius_factor * 3.0 * hw * np.sqrt(dim)
+        rad = cfg.radius_factor * 3.0 * tree.hw[ids] * np.sqrt(dim)
         neff = np.full(p, cfg.n_proxy, dtype=np.int64)
         if k_wave > 0:
             neff += np.ceil(4.0 * k_wave * rad).astype(np.int64)
@@ -442,50 +450,56 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         m0 = _segment_sum(nc[nidx], noff) + neff
         m1 = _segment_sum(nr[nidx], noff) + neff
         d_off, l_off, r_off = _off(nr * nc), _off(nr * nr), _off(nc * nc)
+        # size buckets: each launch gets a tight shared-memory footprint (so
+        # small boxes run several CTAs per SM) and a register tile matched to
+        # its tallest target; buckets run concurrently on side streams
+        need_m = np.maximum(m0, m1)
+        need_n = np.maximum(np.maximum(nr, nc), 1)
+        wb = need_m * need_n * elem
+        cls = np.searchsorted(np.asarray(_W_CLASSES), wb, side="left")
+        buckets = []
+        for c in np.unique(cls):
+            sel = np.nonzero(cls == c)[0]
+            sel = sel[np.argsort(-wb[sel], kind="stable")].astype(np.int32)
+            buckets.append(sel)
+        pk = Packer()
+        pk.add("rdof_off", rdof_off).add("cdof_off", cdof_off).add("nbr_off", noff)
+        pk.add("nbr", nidx.astype(np.int32)).add("box_c", np.ascontiguousarray(tree.center[ids]).ravel())
+        pk.add("box_r", rad).add("pxy_begin", pxy_begin).add("pxy_count", neff.astype(np.int32))
+        pk.add("pxy_unit", unit.ravel()).add("d_off", d_off).add("l_off", l_off).add("r_off", r_off)
+        pk.add("nr", nr.astype(np.int32))
+        if li > 0:
+            pk.add("child_off", child_off)
+        for bi, sel in enumerate(buckets):
+            pk.add(f"order{bi}", sel)
+        t = pk.upload()
         Dt = torch.empty(max(int(d_off[-1]), 1), dtype=tdt, device=dev)
         Lt = torch.empty(max(int(l_off[-1]), 1), dtype=tdt, device=dev)
         Rt = torch.empty(max(int(r_off[-1]), 1), dtype=tdt, device=dev)
         rskel = torch.empty(max(int(rdof_off[-1]), 1), dtype=torch.int32, device=dev)
         cskel = torch.empty(max(int(cdof_off[-1]), 1), dtype=torch.int32, device=dev)
-        kr_t = torch.zeros(p, dtype=torch.int32, device=dev)
-        kc_t = torch.zeros(p, dtype=torch.int32, device=dev)
-        flags = torch.zeros(p, dtype=torch.int32, device=dev)
-        keep = dict(
-            rdof_off=up(rdof_off), cdof_off=up(cdof_off), nbr_off=up(noff),
-            nbr=up(nidx.astype(np.int32)), box_c=up(tree.center[ids].ravel()), box_r=up(rad),
-            pxy_begin=up(pxy_begin), pxy_count=up(neff.astype(np.int32)), pxy_unit=up(unit.ravel()),
-            d_off=up(d_off), l_off=up(l_off), r_off=up(r_off))
-        if li > 0:
-            keep["child_off"] = up(child_off)
-            keep["prev_kr"] = up(prev.kr.astype(np.int32))
-            keep["prev_kc"] = up(prev.kc.astype(np.int32))
+        kk = torch.zeros(3 * p, dtype=torch.int32, device=dev)     # kr | kc | flags
         lvd = _native.SkelLevel()
         lvd.nbox, lvd.level, lvd.equalize, lvd.n_unit = p, li, int(bool(equalize_ranks)), unit.shape[0]
         lvd.eps = float(eps)
-        lvd.rdof_off, lvd.rdofs = p_(keep["rdof_off"]), p_(rdofs)
-        lvd.cdof_off, lvd.cdofs = p_(keep["cdof_off"]), p_(cdofs)
-        lvd.child_off = p_(keep.get("child_off"))
-        lvd.prev_kr, lvd.prev_kc = p_(keep.get("prev_kr")), p_(keep.get("prev_kc"))
-        lvd.nbr_off, lvd.nbr = p_(keep["nbr_off"]), p_(keep["nbr"])
-        lvd.box_c, lvd.box_r = p_(keep["box_c"]), p_(keep["box_r"])
-        lvd.pxy_begin, lvd.pxy_count, lvd.pxy_unit = (p_(keep["pxy_begin"]), p_(keep["pxy_count"]),
-                                                      p_(keep["pxy_unit"]))
-        lvd.d_off, lvd.l_off, lvd.r_off = p_(keep["d_off"]), p_(keep["l_off"]), p_(keep["r_off"])
+        lvd.rdof_off, lvd.rdofs = p_(t["rdof_off"]), p_(rdofs)
+        lvd.cdof_off, lvd.cdofs = p_(t["cdof_off"]), p_(cdofs)
+        if li > 0:
+            lvd.child_off = p_(t["child_off"])
+            lvd.prev_kr, lvd.prev_kc = p_(prev.t_kr), p_(prev.t_kc)
+        lvd.nbr_off, lvd.nbr = p_(t["nbr_off"]), p_(t["nbr"])
+        lvd.box_c, lvd.box_r = p_(t["box_c"]), p_(t["box_r"])
+        lvd.pxy_begin, lvd.pxy_count, lvd.pxy_unit = (p_(t["pxy_begin"]), p_(t["pxy_count"]),
+                                                      p_(t["pxy_unit"]))
+        lvd.d_off, lvd.l_off, lvd.r_off = p_(t["d_off"]), p_(t["l_off"]), p_(t["r_off"])
         lvd.D, lvd.L, lvd.R = p_(Dt), p_(Lt), p_(Rt)
         lvd.rskel, lvd.cskel = p_(rskel), p_(cskel)
-        lvd.kr, lvd.kc, lvd.flags = p_(kr_t), p_(kc_t), p_(flags)
-        # bucket boxes by target height so each launch gets a tight register
-        # tile (rows per lane) and shared-memory size
-        need_m = np.maximum(m0, m1)
-        need_n = np.maximum(nr, nc)
-        cls = np.searchsorted(np.array(_RPL_CLASSES), need_m, side="left")
+        lvd.kr, lvd.kc, lvd.flags = p_(kk[:p]), p_(kk[p:2 * p]), p_(kk[2 * p:])
         scratch_keep = []
         recs = []
-        for c in np.unique(cls):
-            sel = np.nonzero(cls == c)[0]
-            sel = sel[np.argsort(-(need_m[sel] * need_n[sel]), kind="stable")]
-            max_m, max_n = int(need_m[sel].max()), max(int(need_n[sel].max()), 1)
-            elem = 16 if field else 8
+        streams = fork(len(buckets)) if len(buckets) > 1 else None
+        for bi, sel in enumerate(buckets):
+            max_m, max_n = int(need_m[sel].max()), int(need_n[sel].max())
             fixed = _level_smem_fixed(max_n, field)
             if fixed + max_m * max_n * elem > optin:
                 sb = 2 * sel.size * max_m * max_n * elem
@@ -494,20 +508,23 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
                 lvd.scratch, lvd.scratch_bytes = p_(scr), sb
             else:
                 lvd.scratch, lvd.scratch_bytes = None, 0
-            order = up(sel.astype(np.int32))
-            scratch_keep.append(order)
-            with _profile.timed("id_level", level=li, sel=sel) as rec:
-                _native.check(L.skel_id_level(desc, lvd, p_(order), sel.size, max_m, max_n, field, st),
-                              f"skel_id_level (level {li})")
+            ctx = torch.cuda.stream(streams[bi]) if streams else _nullctx()
+            with ctx:
+                with _profile.timed("id_level", level=li, sel=sel) as rec:
+                    _native.check(L.skel_id_level(desc, lvd, p_(t[f"order{bi}"]), sel.size, max_m,
+                                                  max_n, field, _native.stream_ptr()),
+                                  f"skel_id_level (level {li})")
             if rec is not None:
                 recs.append(rec)
-        kr = kr_t.cpu().numpy().astype(np.int64)
-        kc = kc_t.cpu().numpy().astype(np.int64)
+        if streams:
+            join(streams)
+        kk_h = kk.cpu().numpy()
+        kr = kk_h[:p].astype(np.int64)
+        kc = kk_h[p:2 * p].astype(np.int64)
+        fl = kk_h[2 * p:]
         for rec in recs:
             b = rec.meta["sel"]
             rec.flops = float(id_level_flops(m0[b], m1[b], nr[b], nc[b], kr[b], kc[b]).sum())
-        recs.clear()
-        fl = flags.cpu().numpy()
         if np.any(fl & 8):
             raise RuntimeError(f"level {li}: a box exceeds the kernel's neighbour/child limits")
         bad = np.nonzero(fl & 3)[0]
@@ -516,20 +533,27 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             warnings.warn(f"interpolation matrix entries reach > 2 on {bad.size} block(s) at "
                           f"level {li} (first node {bad[0]}); pivoting quality degraded",
                           stacklevel=2)
-        # compact the sorted skeletons: they are the next level's dof lists
+        # the sorted skeletons, compacted, are the next level's dof lists
         kro, kco = _off(kr), _off(kc)
+        pk2 = Packer()
+        pk2.add("d_off", d_off).add("l_off", l_off).add("r_off", r_off)
+        pk2.add("kr", kr.astype(np.int32)).add("kc", kc.astype(np.int32))
+        pk2.add("kr_off", kro).add("kc_off", kco)
+        t2 = pk2.upload()
+        t2.update({k: t[k] for k in ("rdof_off", "cdof_off", "nr")})
+        if li > 0:
+            t2["child_off"] = t["child_off"]
+        t2["_buffer0"] = t["_buffer"]
         rsk = torch.empty(max(int(kro[-1]), 1), dtype=torch.int32, device=dev)
         csk = torch.empty(max(int(kco[-1]), 1), dtype=torch.int32, device=dev)
-        t_kr, t_kc = up(kr.astype(np.int32)), up(kc.astype(np.int32))
-        t_kro, t_kco = up(kro), up(kco)
-        _native.check(L.skel_compact_i32(p, keep["rdof_off"].data_ptr(), p_(t_kr), p_(t_kro),
+        _native.check(L.skel_compact_i32(p, p_(t["rdof_off"]), p_(t2["kr"]), p_(t2["kr_off"]),
                                          p_(rskel), p_(rsk), st), "skel_compact_i32")
-        _native.check(L.skel_compact_i32(p, keep["cdof_off"].data_ptr(), p_(t_kc), p_(t_kco),
+        _native.check(L.skel_compact_i32(p, p_(t["cdof_off"]), p_(t2["kc"]), p_(t2["kc_off"]),
                                          p_(cskel), p_(csk), st), "skel_compact_i32")
         rsk, csk = rsk[:int(kro[-1])], csk[:int(kco[-1])]
-        dl = DevLevel(li, nr, nc, kr, kc, d_off,
-                      _off(nr * nr), _off(nc * nc), Dt, Lt, Rt, rsk, csk, child_off, dtype)
         # L is stored nr x kr inside an nr x nr slot, R kc x nc inside nc x nc
+        dl = DevLevel(li, nr, nc, kr, kc, d_off, l_off, r_off, Dt, Lt, Rt, rsk, csk, child_off,
+                      dtype, t=t2)
         levels.append(CompressedLevel(dev=dl))
         prev = dl
 
@@ -545,6 +569,14 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
 
 
 _OPTIN = None
+
+
+class _nullctx:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
 
 
 def _smem_optin():

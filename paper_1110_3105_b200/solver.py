@@ -16,9 +16,12 @@ import numpy as np
 
 from . import _native, _profile
 from .errors import InvalidInput, SingularBlock
-from .skel import CompressedMatrix, _dense_apply, _off
+from ._staging import Packer, fork, join
+from .skel import CompressedMatrix, _dense_apply, _nullctx, _off
 
 _RCOND_WARN = 1e-14
+# per-box shared-memory need classes (bytes) -> one launch each
+_FAC_CLASSES = (24 << 10, 48 << 10, 80 << 10, 112 << 10, 160 << 10, 224 << 10)
 
 
 @dataclass
@@ -32,21 +35,16 @@ class FactoredNode:
 
 
 class DevFactorLevel:
-    def __init__(self, n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, child_off):
-        torch = _native.require_cuda()
-        up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda")  # noqa: E731
+    def __init__(self, n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, child_off, t):
         self.p = n.size
         self.n, self.k = n, k
         self.dd_off, self.ld_off, self.lam_off = dd_off, ld_off, lam_off
         self.Dd, self.Ld, self.Rd, self.Lam = Dd, Ld, Rd, Lam
         self.child_off = child_off
-        self.t_n = up(n.astype(np.int32))
-        self.t_k = up(k.astype(np.int32))
-        self.t_noff = up(_off(n))
-        self.t_koff = up(_off(k))
-        self.t_dd_off = up(dd_off)
-        self.t_ld_off = up(ld_off)
-        self.t_lam_off = up(lam_off)
+        self.t_n, self.t_k = t["n"], t["k"]
+        self.t_noff, self.t_koff = t["noff"], t["koff"]
+        self.t_dd_off, self.t_ld_off, self.t_lam_off = t["dd_off"], t["ld_off"], t["lam_off"]
+        self._buf = t["_buffer"]
         self.max_n = int(max(n.max(initial=0), 1))
         self.max_nk = int(max((n + k).max(initial=0), 1))
 
@@ -165,23 +163,50 @@ def factor(cm: CompressedMatrix, regularize: float = 0.0) -> FactoredInverse:
         return FactoredInverse([], S, Sinv, cm.n, cm.perm.copy(), cm.scalar_field, warns)
 
     dls = cm.device_levels()
-    flevels = []
-    prev = None
+    elem = 16 if field else 8
+    optin = _smem_optin()
+    # host bookkeeping for every level first, then ONE packed upload
+    plan = []
+    pk = Packer()
     for li, dl in enumerate(dls):
-        p = dl.p
         sq_bad = dl.nr != dl.nc
         lam_bad = (~sq_bad) & (dl.nr > 0) & (dl.kr != dl.kc)
         n = np.where(sq_bad | lam_bad, 0, dl.nr).astype(np.int64)
         k = np.where(n > 0, dl.kr, 0).astype(np.int64)
         dd_off, ld_off, lam_off = _off(n * n), _off(n * k), _off(k * k)
+        need = (n * n + 4 * n * k + k * k + n) * elem
+        cls = np.searchsorted(np.asarray(_FAC_CLASSES), need, side="left")
+        buckets = []
+        for c in np.unique(cls[n > 0]):
+            sel = np.nonzero((cls == c) & (n > 0))[0]
+            buckets.append(sel[np.argsort(-need[sel], kind="stable")].astype(np.int32))
+        pre = f"L{li}_"
+        pk.add(pre + "n", n.astype(np.int32)).add(pre + "k", k.astype(np.int32))
+        pk.add(pre + "noff", _off(n)).add(pre + "koff", _off(k))
+        pk.add(pre + "dd_off", dd_off).add(pre + "ld_off", ld_off).add(pre + "lam_off", lam_off)
+        for bi, sel in enumerate(buckets):
+            pk.add(pre + f"order{bi}", sel)
+        plan.append((sq_bad, lam_bad, n, k, dd_off, ld_off, lam_off, buckets))
+    t = pk.upload()
+    P = sum(dl.p for dl in dls)
+    stat = torch.zeros(P, dtype=torch.int32, device=dev)
+    rcd = torch.ones(P, dtype=torch.float64, device=dev)
+    rcm = torch.ones(P, dtype=torch.float64, device=dev)
+    flevels = []
+    prev = None
+    base = 0
+    keep = []
+    for li, dl in enumerate(dls):
+        sq_bad, lam_bad, n, k, dd_off, ld_off, lam_off, buckets = plan[li]
+        p = dl.p
+        pre = f"L{li}_"
+        tl = {key: t[pre + key] for key in ("n", "k", "noff", "koff", "dd_off", "ld_off", "lam_off")}
+        tl["_buffer"] = t["_buffer"]
         Dd = torch.empty(max(int(dd_off[-1]), 1), dtype=tdt, device=dev)
         Ld = torch.empty(max(int(ld_off[-1]), 1), dtype=tdt, device=dev)
         Rd = torch.empty(max(int(ld_off[-1]), 1), dtype=tdt, device=dev)
         Lam = torch.empty(max(int(lam_off[-1]), 1), dtype=tdt, device=dev)
-        status = torch.zeros(p, dtype=torch.int32, device=dev)
-        rcd = torch.ones(p, dtype=torch.float64, device=dev)
-        rcm = torch.ones(p, dtype=torch.float64, device=dev)
-        fl = DevFactorLevel(n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, dl.child_off)
+        fl = DevFactorLevel(n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, dl.child_off, tl)
         F = _native.SkelFactorLevel()
         F.nbox, F.level, F.regularize = p, li, float(regularize)
         F.n, F.k = p_(fl.t_n), p_(fl.t_k)
@@ -193,24 +218,45 @@ def factor(cm: CompressedMatrix, regularize: float = 0.0) -> FactoredInverse:
         F.dd_off, F.ld_off, F.rd_off, F.lam_off = (p_(fl.t_dd_off), p_(fl.t_ld_off),
                                                    p_(fl.t_ld_off), p_(fl.t_lam_off))
         F.Dd, F.Ld, F.Rd, F.Lam = p_(Dd), p_(Ld), p_(Rd), p_(Lam)
-        F.status, F.rcond_d, F.rcond_m = p_(status), p_(rcd), p_(rcm)
-        max_n = int(max(n.max(initial=0), 1))
-        max_k = int(k.max(initial=0))
-        elem = 16 if field else 8
-        need = (max_n * max_n + 4 * max_n * max_k + max_k * max_k + max_n) * elem
-        scr = None
-        if need + 1024 > _smem_optin():
-            scr = torch.empty(p * need // 8 + 1, dtype=torch.float64, device=dev)
-            F.scratch, F.scratch_bytes = p_(scr), p * need
-        with _profile.timed("factor_level", level=li) as rec:
-            _native.check(L.skel_factor_level(F, max_n, max_k, field, st), f"skel_factor_level ({li})")
-        if rec is not None:
-            nf, kf = n.astype(np.float64), k.astype(np.float64)
-            rec.flops = float((2 * nf ** 3 + 6 * nf * nf * kf + 6 * kf * kf * nf + 2 * kf ** 3).sum())
-            rec.nbytes = float(((nf * nf + 2 * nf * kf) * 2 + kf * kf).sum()) * (16 if field else 8)
-        sts = status.cpu().numpy()
-        rd_h = rcd.cpu().numpy()
-        rm_h = rcm.cpu().numpy()
+        F.status, F.rcond_d, F.rcond_m = p_(stat[base:]), p_(rcd[base:]), p_(rcm[base:])
+        streams = fork(len(buckets)) if len(buckets) > 1 else None
+        nf, kf = n.astype(np.float64), k.astype(np.float64)
+        for bi, sel in enumerate(buckets):
+            max_n = int(n[sel].max())
+            max_k = int(k[sel].max())
+            need = (max_n * max_n + 4 * max_n * max_k + max_k * max_k + max_n) * elem
+            F.order, F.nrun = p_(t[pre + f"order{bi}"]), sel.size
+            F.scratch, F.scratch_bytes = None, 0
+            if need + 1024 + 4 * max_n > optin:
+                scr = torch.empty(sel.size * need // 8 + 1, dtype=torch.float64, device=dev)
+                keep.append(scr)
+                F.scratch, F.scratch_bytes = p_(scr), sel.size * need
+            ctx = torch.cuda.stream(streams[bi]) if streams else _nullctx()
+            with ctx:
+                with _profile.timed("factor_level", level=li) as rec:
+                    _native.check(L.skel_factor_level(F, max_n, max_k, field, _native.stream_ptr()),
+                                  f"skel_factor_level ({li})")
+            if rec is not None:
+                b_ = sel
+                rec.flops = float((2 * nf[b_] ** 3 + 6 * nf[b_] ** 2 * kf[b_] + 6 * kf[b_] ** 2 * nf[b_]
+                                   + 2 * kf[b_] ** 3).sum())
+                rec.nbytes = float(((nf[b_] ** 2 + 2 * nf[b_] * kf[b_]) * 2 + kf[b_] ** 2).sum()) * elem
+        if streams:
+            join(streams)
+        flevels.append(FactoredLevel(fl))
+        prev = fl
+        base += p
+    # one read-back of every level's status / rcond, checked in the
+    # reference's (level, node) order (solver.py:222-264)
+    sts_all = stat.cpu().numpy()
+    rd_all = rcd.cpu().numpy()
+    rm_all = rcm.cpu().numpy()
+    base = 0
+    for li, dl in enumerate(dls):
+        sq_bad, lam_bad, n, k = plan[li][:4]
+        p = dl.p
+        sts, rd_h, rm_h = sts_all[base:base + p], rd_all[base:base + p], rm_all[base:base + p]
+        base += p
         fails = np.nonzero(sq_bad | lam_bad | (sts != 0))[0]
         if fails.size:
             a = int(fails[0])
@@ -228,8 +274,6 @@ def factor(cm: CompressedMatrix, regularize: float = 0.0) -> FactoredInverse:
                 warns.append((li + 1, int(a), "D", float(rd_h[a])))
             if k[a] > 0 and rm_h[a] < _RCOND_WARN:
                 warns.append((li + 1, int(a), "Lambda", float(rm_h[a])))
-        flevels.append(FactoredLevel(fl))
-        prev = fl
 
     # top: Shat = S with the last level's Lambdas on the diagonal blocks
     S = cm.device_S()
