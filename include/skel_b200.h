@@ -118,11 +118,12 @@ typedef struct {
  * zeroed, proxy-compressed targets t_row.T / t_col (skel.py:349-368),
  * id_fixed_precision x2 (lowrank.py:48-161), equalize (skel.py:377-382),
  * skeleton sort and L/R (skel.py:384-391).  `box_order` lists the boxes to
- * process (sorted by size by the caller); `max_m`/`max_n` bound the target.
+ * process (sorted by size by the caller); `max_m`/`max_n` bound the target
+ * height / width and `max_w` its m*n element count over the listed boxes.
  * field: 0 = float64, 1 = complex128. */
 int skel_id_level(const SkelSource* src, const SkelLevel* lv, const int32_t* box_order,
-                  int32_t nbox_run, int32_t max_m, int32_t max_n, int32_t field,
-                  void* stream);
+                  int32_t nbox_run, int32_t max_m, int32_t max_n, int64_t max_w,
+                  int32_t field, void* stream);
 
 /* Dense top-level skeleton matrix S = A(row_skel_a, col_skel_b), a != b,
  * zero diagonal blocks (skel.py:399-408). rows/cols: tree positions; rbox/cbox:

@@ -15,30 +15,33 @@ class DeviceGeometry:
     pairs closer than ~1e-13 -- which the BASELINE geometries never have
     (spacing >= 1e-5)."""
 
-    def __init__(self, coords, perm, normals=None, weights=None, curvatures=None):
+    def __init__(self, coords, perm, normals=None, weights=None, curvatures=None, resident=None):
+        """Upload (or reuse, via ``resident``: a ResidentPoints in original
+        order) the point data and gather it into tree order on the device."""
         torch = _native.require_cuda()
-        coords = np.asarray(coords, dtype=np.float64)
         perm = np.asarray(perm, dtype=np.int64)
-        self.n, self.dim = coords.shape
-        dev = torch.device("cuda")
-        ct = coords[perm]
-        put = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
-        self.x = put(ct[:, 0])
-        self.y = put(ct[:, 1])
-        self.z = put(ct[:, 2]) if self.dim == 3 else None
-        if normals is not None:
-            nt = np.asarray(normals, dtype=np.float64)[perm]
-            self.nx, self.ny = put(nt[:, 0]), put(nt[:, 1])
-            self.nz = put(nt[:, 2]) if self.dim == 3 else None
-        else:
-            self.nx = self.ny = self.nz = None
-        self.w = None if weights is None else put(np.asarray(weights, dtype=np.float64)[perm])
-        self.curv = None if curvatures is None else put(np.asarray(curvatures, dtype=np.float64)[perm])
-        self.orig = put(perm)
+        if resident is None:
+            resident = ResidentPoints(coords, normals, weights, curvatures)
+        self.n, self.dim = resident.n, resident.dim
         self.perm = perm
-        span = max(float(np.ptp(coords, axis=0).max()), float(np.abs(coords).max()), 1.0)
-        self.coincide_tol = 1e-14 * span
-        self.host_weights = None if weights is None else np.asarray(weights, dtype=np.float64)[perm]
+        self.orig = torch.from_numpy(np.ascontiguousarray(perm)).to("cuda", non_blocking=False)
+        L = _native.lib()
+        st = _native.stream_ptr()
+
+        def gather(src):
+            if src is None:
+                return None
+            dst = torch.empty_like(src)
+            _native.check(L.skel_permute_rows(_native.ptr(self.orig), self.n, _native.ptr(src),
+                                              _native.ptr(dst), 1, 0, 0, st), "gather")
+            return dst
+
+        r = resident
+        self.x, self.y, self.z = gather(r.x), gather(r.y), gather(r.z)
+        self.nx, self.ny, self.nz = gather(r.nx), gather(r.ny), gather(r.nz)
+        self.w, self.curv = gather(r.w), gather(r.curv)
+        self.coincide_tol = r.coincide_tol
+
 
     def source(self, kind, equation, layer=1, k=0.0, identity_coef=0.0, diag=0.0, wscale=1.0,
                curvature_limit=False, kr10=False, weighted=True):
@@ -62,3 +65,26 @@ class DeviceGeometry:
         s.wscale = float(wscale)
         s.coincide_tol = self.coincide_tol
         return s
+
+
+class ResidentPoints:
+    """A point set's SoA arrays in ORIGINAL order on the device (uploaded
+    once; tree orderings are gathered from it on the device)."""
+
+    def __init__(self, coords, normals=None, weights=None, curvatures=None):
+        torch = _native.require_cuda()
+        coords = np.asarray(coords, dtype=np.float64)
+        self.n, self.dim = coords.shape
+        put = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to("cuda")  # noqa: E731
+        self.x, self.y = put(coords[:, 0]), put(coords[:, 1])
+        self.z = put(coords[:, 2]) if self.dim == 3 else None
+        if normals is not None:
+            nt = np.asarray(normals, dtype=np.float64)
+            self.nx, self.ny = put(nt[:, 0]), put(nt[:, 1])
+            self.nz = put(nt[:, 2]) if self.dim == 3 else None
+        else:
+            self.nx = self.ny = self.nz = None
+        self.w = None if weights is None else put(weights)
+        self.curv = None if curvatures is None else put(curvatures)
+        span = max(float(np.ptp(coords, axis=0).max()), float(np.abs(coords).max()), 1.0)
+        self.coincide_tol = 1e-14 * span

@@ -7,28 +7,56 @@ import numpy as np
 from . import _native
 
 _ALIGN = 256
-_pinned = [None]
-_last_copy = [None]
-_streams = []
+_pools = {}
+_RING_BYTES = 64 << 20
 
 
-def _staging(nbytes):
-    torch = _native.require_cuda()
-    if _last_copy[0] is not None:
-        _last_copy[0].synchronize()       # previous async copy out of the buffer
-        _last_copy[0] = None
-    buf = _pinned[0]
-    if buf is None or buf.numel() < nbytes:
-        size = max(nbytes, 1 << 20, 0 if buf is None else 2 * buf.numel())
-        buf = torch.empty(size, dtype=torch.uint8, pin_memory=True)
-        _pinned[0] = buf
-    return buf
+class _PinnedRing:
+    """Pinned host staging ring: uploads are sub-allocated in order; before a
+    region is reused the event of the copy that last read it is awaited
+    (no per-upload cudaHostAlloc, which can stall the device)."""
+
+    def __init__(self, size):
+        import collections
+        torch = _native.require_cuda()
+        self.buf = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+        self.size = size
+        self.head = 0
+        self.pending = collections.deque()     # (start, end, event)
+
+    def alloc(self, nbytes):
+        nbytes = (nbytes + _ALIGN - 1) // _ALIGN * _ALIGN
+        if nbytes > self.size:
+            return None, 0
+        if self.head + nbytes > self.size:
+            self.head = 0
+        lo, hi = self.head, self.head + nbytes
+        while self.pending:
+            s, e, ev = self.pending[0]
+            if s < hi and lo < e:
+                ev.synchronize()
+                self.pending.popleft()
+            else:
+                break
+        self.head = hi
+        return self.buf[lo:hi], lo
+
+    def retire(self, lo, nbytes, event):
+        self.pending.append((lo, lo + nbytes, event))
+
+
+_ring = [None]
+
+
+def _get_ring():
+    if _ring[0] is None:
+        _ring[0] = _PinnedRing(_RING_BYTES)
+    return _ring[0]
 
 
 class Packer:
     """Collects numpy arrays and uploads them with ONE async copy from a
-    pinned staging buffer (the next upload waits for the previous copy
-    before overwriting the buffer)."""
+    pinned staging block."""
 
     def __init__(self):
         self.items = []
@@ -44,15 +72,19 @@ class Packer:
     def upload(self):
         torch = _native.require_cuda()
         size = max(self.size, 1)
-        host = _staging(size)
+        ring = _get_ring()
+        host, lo = ring.alloc(size)
+        if host is None:      # larger than the ring: one-off pinned block
+            host = torch.empty(size, dtype=torch.uint8, pin_memory=True)
         hv = host.numpy()
         for _, arr, off in self.items:
             hv[off:off + arr.nbytes] = arr.view(np.uint8).ravel()
         dev = torch.empty(size, dtype=torch.uint8, device="cuda")
         dev.copy_(host[:size], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        _last_copy[0] = ev
+        if host.data_ptr() >= ring.buf.data_ptr() and host.data_ptr() < ring.buf.data_ptr() + ring.size:
+            ev = torch.cuda.Event()
+            ev.record()
+            ring.retire(lo, host.numel(), ev)
         out = {}
         for name, arr, off in self.items:
             tdt = {np.dtype(np.int64): torch.int64, np.dtype(np.int32): torch.int32,
@@ -63,28 +95,35 @@ class Packer:
         return out
 
 
-def side_streams(k):
+def side_streams(k, tag="default"):
     torch = _native.require_cuda()
-    while len(_streams) < k:
-        _streams.append(torch.cuda.Stream())
-    return _streams[:k]
+    pool = _pools.setdefault(tag, [])
+    while len(pool) < k:
+        pool.append(torch.cuda.Stream())
+    return pool[:k]
 
 
-def fork(k):
+def fork(k, tag="default"):
     """k side streams that start after the current stream's pending work."""
     torch = _native.require_cuda()
     ev = torch.cuda.Event()
     ev.record()
-    ss = side_streams(k)
+    ss = side_streams(k, tag)
     for s in ss:
         s.wait_event(ev)
     return ss
 
 
 def join(streams):
+    """The current stream waits for everything queued on ``streams``."""
     torch = _native.require_cuda()
     cur = torch.cuda.current_stream()
     for s in streams:
         ev = torch.cuda.Event()
         ev.record(s)
         cur.wait_event(ev)
+
+
+def eager_stream():
+    """The side stream of the eager (overlapped) factorization."""
+    return side_streams(1, "eager")[0]

@@ -11,7 +11,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
-from ._device import DeviceGeometry
+from ._device import DeviceGeometry, ResidentPoints
 from .errors import InvalidInput
 from .geom import PointSet, build_tree
 from .kernels import KernelSpec, eval_block
@@ -90,6 +90,7 @@ class BieSystem(_DeviceSourceMixin):
         self.identity_coef = float(identity_coef)
         self.points = curve.point_set()
         self._geo = None
+        self._res = None
 
     @property
     def n(self):
@@ -103,14 +104,20 @@ class BieSystem(_DeviceSourceMixin):
     def wavenumber(self):
         return self.spec.wavenumber
 
+    def resident(self):
+        """Curve nodes resident on the device in original order (uploaded
+        once per system; every tree ordering is gathered from it on the GPU)."""
+        if self._res is None:
+            self._res = ResidentPoints(self.curve.xy, self.curve.normals, self.curve.weights,
+                                       self.curve.curvature)
+        return self._res
+
     def geometry(self, perm=None):
         if perm is None:
             if self._geo is None:
-                self._geo = DeviceGeometry(self.curve.xy, np.arange(self.n), self.curve.normals,
-                                           self.curve.weights, self.curve.curvature)
+                self._geo = DeviceGeometry(None, np.arange(self.n), resident=self.resident())
             return self._geo
-        return DeviceGeometry(self.curve.xy, perm, self.curve.normals, self.curve.weights,
-                              self.curve.curvature)
+        return DeviceGeometry(None, perm, resident=self.resident())
 
     def descriptor(self, geo, wscale=1.0):
         return geo.source(_native.SRC_BIE, self.spec.eq_code, _native.LAYER_DOUBLE,

@@ -81,6 +81,10 @@ __device__ __forceinline__ zc warp_sum(zc v) {
   return v;
 }
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ double shfl_xor_T(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ zc shfl_xor_T(zc v, int o) {
+  return zc(__shfl_xor_sync(0xffffffffu, v.re, o), __shfl_xor_sync(0xffffffffu, v.im, o));
+}
 __device__ __forceinline__ zc shfl(zc v, int src) {
   return zc(__shfl_sync(0xffffffffu, v.re, src), __shfl_sync(0xffffffffu, v.im, src));
 }

@@ -14,16 +14,25 @@
 //   * P[:, skel] = I, P[:, rest] = R11^-1 R12 (lowrank.py:122-133); padding to
 //     min_rank with unit rows (lowrank.py:147-157)
 //
-// GPU mapping: warp 0 runs the serial part of a step (argmax, swap,
-// Householder vector); then every warp owns a strided set of trailing
-// columns and, per column, computes v^H w, applies the reflector and
-// downdates that column's norm -- fusing the next step's renormalisation /
-// stale checks into the same pass so a step costs two CTA barriers.
-// With RPL > 0 the reflector and the column slice live in registers
-// (RPL = max rows per lane), so each element is read and written once.
+// GPU mapping (two CTA barriers per step, almost no serial work):
+//   * columns never move: a position -> column map (`piv`, which is also the
+//     pivot order the reference returns) replaces the column swaps;
+//   * phase B (all warps): every warp owns a round-robin share of the trailing
+//     positions and, per column, applies the reflector (v^H w and the rank-1
+//     update with the column held in registers), downdates that position's
+//     norm, runs the NEXT step's renormalisation / stale rule, records the
+//     exact trailing norm (the next Householder |x| if this column is picked)
+//     and folds the position into a per-warp first-maximum candidate; a
+//     column is handled by a group of GL lanes (several columns per warp
+//     instruction, log2(GL)-level reductions);
+//   * phase A (one thread): reduce the per-warp candidates to the pivot,
+//     apply the stop rule, swap the position bookkeeping and form alpha, v0,
+//     2/|v|^2 from the precomputed exact norm.
 #pragma once
 
 #include "common.cuh"
+
+#define CPQR_MAXW 32
 
 template <class T>
 struct CpqrShared {
@@ -35,218 +44,197 @@ struct CpqrShared {
   int stop;      // loop exit flag
   int pad;       // padded columns (min_rank > achieved rank)
   int partner_k; // rank of the other side of the box (equalize)
+  int pc;        // column of the current pivot
   double bigP;   // max |P| (interp quality warning, lowrank.py:128-132)
+  double cand_v[CPQR_MAXW];
+  int cand_i[CPQR_MAXW];
 };
 
 __device__ __forceinline__ double sk_unit_phase(double x0, double) { return x0 > 0.0 ? 1.0 : -1.0; }
 __device__ __forceinline__ zc sk_unit_phase(zc x0, double a) { return zc(x0.re / a, x0.im / a); }
 
-// squared norm of rows [r0, m) of column c, warp-cooperative
-template <class T>
-__device__ __forceinline__ double col_norm2(const T* W, int ld, int c, int r0, int m, int lane) {
-  double s = 0.0;
-  for (int i = r0 + lane; i < m; i += SKEL_WARP) s += sk_abs2(W[(int64_t)c * ld + i]);
-  return warp_sum(s);
+// first-maximum merge: larger value wins, ties -> lower position
+__device__ __forceinline__ void cand_merge(double& bv, int& bi, double ov, int oi) {
+  if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
 }
-
-// Initial exact norms (all rows), nrm = ref (lowrank.py:55-64).
-template <class T>
-__device__ void cpqr_init(const T* W, int m, int n, int ld, double* nrm, double* ref, int* piv) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int c = warp; c < n; c += nw) {
-    double s = col_norm2(W, ld, c, 0, m, lane);
-    if (lane == 0) {
-      nrm[c] = s;
-      ref[c] = s;
-    }
-  }
-  for (int c = threadIdx.x; c < n; c += blockDim.x) piv[c] = c;
-}
-
-// Serial part of step s on warp 0.  Returns via sh.
-template <class T>
-__device__ void cpqr_pivot_step(T* W, int m, int n, int ld, double* nrm, int* piv,
-                                CpqrShared<T>& sh, int s, double eps, int min_rank) {
-  const int lane = threadIdx.x & 31;
-  // first maximum of nrm[s:]
-  double best = -1.0;
-  int bj = n;
-  for (int c = s + lane; c < n; c += SKEL_WARP) {
-    double v = nrm[c];
-    if (v > best) { best = v; bj = c; }
-  }
+__device__ __forceinline__ void warp_cand(double& bv, int& bi) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    double ov = __shfl_xor_sync(0xffffffffu, best, o);
-    int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-    if (ov > best || (ov == best && oj < bj)) { best = ov; bj = oj; }
-  }
-  double pn = sqrt(fmax(best, 0.0));
-  int stop = 0;
-  if (s == 0) {
-    if (lane == 0) sh.p0 = pn;
-    if (pn == 0.0) stop = 1;
-  }
-  double p0 = (s == 0) ? pn : sh.p0;
-  if (!stop && s >= min_rank && pn <= eps * p0) stop = 1;
-  if (!stop && pn == 0.0) stop = 1;
-  if (stop) {
-    if (lane == 0) sh.stop = 1;
-    return;
-  }
-  if (bj != s) {
-    for (int i = lane; i < m; i += SKEL_WARP) {
-      T a = W[(int64_t)s * ld + i];
-      W[(int64_t)s * ld + i] = W[(int64_t)bj * ld + i];
-      W[(int64_t)bj * ld + i] = a;
-    }
-    if (lane == 0) {
-      double t = nrm[s]; nrm[s] = nrm[bj]; nrm[bj] = t;
-      int p = piv[s]; piv[s] = piv[bj]; piv[bj] = p;
-    }
-  }
-  __syncwarp();
-  // Householder vector of x = W[s:, s]
-  double s1 = 0.0;
-  for (int i = s + 1 + lane; i < m; i += SKEL_WARP) s1 += sk_abs2(W[(int64_t)s * ld + i]);
-  s1 = warp_sum(s1);
-  if (lane == 0) {
-    T x0 = W[(int64_t)s * ld + s];
-    double ax0 = sk_abs(x0);
-    double normx = sqrt(s1 + sk_abs2(x0));
-    T phase = T(1.0);
-    if (ax0 != 0.0) phase = sk_unit_phase(x0, ax0);   // x0 / |x0|
-    T alpha = -(phase * normx);
-    T v0 = x0 - alpha;
-    double vv = s1 + sk_abs2(v0);
-    sh.v0 = v0;
-    sh.alpha = alpha;
-    sh.beta = vv > 0.0 ? 2.0 / vv : 0.0;
-    sh.stop = 0;
+    double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    cand_merge(bv, bi, ov, oi);
   }
 }
 
-// Parallel part of step s: apply the reflector to columns s+1..n-1, downdate
-// norms, and run step s+1's renormalisation / stale recompute.
-template <class T, int RPL>
-__device__ void cpqr_update(T* W, int m, int n, int ld, double* nrm, double* ref,
-                            const CpqrShared<T>& sh, int s, int kmax) {
+// Initial exact norms (all rows): nrm = ref = xn2, piv = identity, and the
+// per-warp pivot candidates for step 0 (lowrank.py:55-64).
+template <class T>
+__device__ void cpqr_init(const T* W, int m, int n, int ld, double* nrm, double* ref,
+                          double* xn2, int* piv, CpqrShared<T>& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double bv = -1.0;
+  int bi = 0x7fffffff;
+  for (int c = warp; c < n; c += nw) {
+    double s = 0.0;
+    for (int i = lane; i < m; i += SKEL_WARP) s += sk_abs2(W[(int64_t)c * ld + i]);
+    s = warp_sum(s);
+    if (lane == 0) { nrm[c] = s; ref[c] = s; xn2[c] = s; }
+    cand_merge(bv, bi, s, c);
+  }
+  for (int c = threadIdx.x; c < n; c += blockDim.x) piv[c] = c;
+  if (lane == 0) { sh.cand_v[warp] = bv; sh.cand_i[warp] = bi; }
+}
+
+// Phase A of step s (thread 0).
+template <class T>
+__device__ void cpqr_pivot(T* W, int n, int ld, double* nrm, double* xn2, int* piv,
+                           CpqrShared<T>& sh, int s, double eps, int min_rank, int nw) {
+  double bv = -1.0;
+  int j = 0x7fffffff;
+  for (int w = 0; w < nw; ++w) cand_merge(bv, j, sh.cand_v[w], sh.cand_i[w]);
+  if (j >= n) { sh.stop = 1; return; }
+  double pn = sqrt(fmax(nrm[j], 0.0));
+  if (s == 0) {
+    sh.p0 = pn;
+    if (pn == 0.0) { sh.stop = 1; return; }
+  }
+  if ((s >= min_rank && pn <= eps * sh.p0) || pn == 0.0) { sh.stop = 1; return; }
+  if (j != s) {
+    double t = nrm[s]; nrm[s] = nrm[j]; nrm[j] = t;
+    t = xn2[s]; xn2[s] = xn2[j]; xn2[j] = t;
+    int q = piv[s]; piv[s] = piv[j]; piv[j] = q;
+  }
+  const int pc = piv[s];
+  const T x0 = W[(int64_t)pc * ld + s];
+  const double ax0 = sk_abs(x0);
+  const double normx = sqrt(xn2[s]);
+  T phase = T(1.0);
+  if (ax0 != 0.0) phase = sk_unit_phase(x0, ax0);   // x0 / |x0|
+  const T alpha = -(phase * normx);
+  const double vv = 2.0 * normx * (normx + ax0);    // |x - alpha e1|^2
+  sh.v0 = x0 - alpha;
+  sh.alpha = alpha;
+  sh.beta = vv > 0.0 ? 2.0 / vv : 0.0;
+  sh.pc = pc;
+  sh.stop = 0;
+}
+
+// Phase B of step s (all warps).  Register path: a column is handled by a
+// group of GL lanes (32/GL columns per warp per pass), each lane holding
+// RPL rows (i = s + lane%GL + GL*r) of the reflector and of its column, so the
+// two reductions per column (v^H w, trailing |w|^2) take log2(GL) shuffle
+// levels and several columns share every instruction.
+template <class T, int GL, int RPL>
+__device__ void cpqr_update(T* W, int m, int n, int ld, double* nrm, double* ref, double* xn2,
+                            const int* piv, CpqrShared<T>& sh, int s, int kmax) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const T v0 = sh.v0;
   const double beta = sh.beta;
   const int s1 = s + 1;
   const bool renorm = (s1 < kmax) && (s1 % 32 == 0);
-  const bool check = (s1 < kmax);
-  const T* vcol = W + (int64_t)s * ld;
+  const T* vcol = W + (int64_t)sh.pc * ld;
+  double bv = -1.0;
+  int bi = 0x7fffffff;
   if constexpr (RPL > 0) {
+    constexpr int CPW = 32 / GL;             // columns per warp per pass
+    const int g = lane / GL, gl = lane - (lane / GL) * GL;
     T vr[RPL];
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
-      int i = s + lane + SKEL_WARP * r;
-      vr[r] = (i < m) ? ((r == 0 && lane == 0) ? v0 : vcol[i]) : T(0.0);
+      int i = s + gl + GL * r;
+      vr[r] = (i < m) ? ((r == 0 && gl == 0) ? v0 : vcol[i]) : T(0.0);
     }
-    for (int c = s1 + warp; c < n; c += nw) {
-      T* wc = W + (int64_t)c * ld;
+    for (int cb = s1 + warp * CPW; cb < n; cb += nw * CPW) {
+      const int c = cb + g;
+      const bool act = c < n;
+      T* wc = W + (int64_t)piv[act ? c : n - 1] * ld;
       T wr[RPL];
-      T dot = T(0.0);
+      // 4 partial sums break the dependent FMA chains
+      T d4[4] = {T(0.0), T(0.0), T(0.0), T(0.0)};
 #pragma unroll
       for (int r = 0; r < RPL; ++r) {
-        int i = s + lane + SKEL_WARP * r;
+        int i = s + gl + GL * r;
         wr[r] = (i < m) ? wc[i] : T(0.0);
-        dot += sk_conj(vr[r]) * wr[r];
+        d4[r & 3] += sk_conj(vr[r]) * wr[r];
       }
-      dot = warp_sum(dot);
-      if (beta != 0.0) {
-        T f = dot * beta;
+      T dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
 #pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-          int i = s + lane + SKEL_WARP * r;
-          if (i < m) {
-            wr[r] -= vr[r] * f;
-            wc[i] = wr[r];
-          }
-        }
-      }
-      T row = shfl(wr[0], 0);
-      double nv = 0.0;
-      if (check) {
-        double acc = 0.0;
+      for (int o = GL / 2; o > 0; o >>= 1) dot += shfl_xor_T(dot, o);
+      const T f = dot * beta;
+      double x4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-          int i = s + lane + SKEL_WARP * r;
-          if (i < m && i > s) acc += sk_abs2(wr[r]);
-        }
-        nv = acc;  // reduced lazily below (only if needed)
-      }
-      if (lane == 0) {
-        double t = nrm[c] - sk_abs2(row);
-        nrm[c] = t > 0.0 ? t : 0.0;
-      }
-      __syncwarp();
-      if (check) {
-        bool need = renorm || (nrm[c] < 1e-8 * ref[c]);
-        if (need) {
-          double full = warp_sum(nv);
-          if (lane == 0) { nrm[c] = full; ref[c] = full; }
+      for (int r = 0; r < RPL; ++r) {
+        int i = s + gl + GL * r;
+        if (beta != 0.0) wr[r] -= vr[r] * f;
+        if (i < m) {
+          if (beta != 0.0 && act) wc[i] = wr[r];
+          if (i > s) x4[r & 3] += sk_abs2(wr[r]);
         }
       }
-      __syncwarp();
+      double xa = (x4[0] + x4[1]) + (x4[2] + x4[3]);
+#pragma unroll
+      for (int o = GL / 2; o > 0; o >>= 1) xa += __shfl_xor_sync(0xffffffffu, xa, o);
+      if (gl == 0 && act) {
+        // wr[0] of the group leader is row s of the updated column (R[s, c])
+        double t = nrm[c] - sk_abs2(wr[0]);
+        t = t > 0.0 ? t : 0.0;
+        if (renorm || t < 1e-8 * ref[c]) { t = xa; ref[c] = xa; }
+        nrm[c] = t;
+        xn2[c] = xa;
+        cand_merge(bv, bi, t, c);
+      }
     }
+    warp_cand(bv, bi);
   } else {
     for (int c = s1 + warp; c < n; c += nw) {
-      T* wc = W + (int64_t)c * ld;
+      T* wc = W + (int64_t)piv[c] * ld;
       T dot = T(0.0);
       for (int i = s + lane; i < m; i += SKEL_WARP) {
         T vi = (i == s) ? v0 : vcol[i];
         dot += sk_conj(vi) * wc[i];
       }
       dot = warp_sum(dot);
+      const T f = dot * beta;
       double acc = 0.0;
-      T row = wc[s];
-      if (beta != 0.0) {
-        T f = dot * beta;
-        for (int i = s + lane; i < m; i += SKEL_WARP) {
-          T vi = (i == s) ? v0 : vcol[i];
-          T nwv = wc[i] - vi * f;
+      for (int i = s + lane; i < m; i += SKEL_WARP) {
+        T vi = (i == s) ? v0 : vcol[i];
+        T nwv = wc[i];
+        if (beta != 0.0) {
+          nwv -= vi * f;
           wc[i] = nwv;
-          if (i > s) acc += sk_abs2(nwv);
         }
-        __syncwarp();
-        row = wc[s];
-      } else {
-        for (int i = s + 1 + lane; i < m; i += SKEL_WARP) acc += sk_abs2(wc[i]);
+        if (i > s) acc += sk_abs2(nwv);
       }
+      __syncwarp();
+      acc = warp_sum(acc);
+      const T row = wc[s];
       if (lane == 0) {
         double t = nrm[c] - sk_abs2(row);
-        nrm[c] = t > 0.0 ? t : 0.0;
+        t = t > 0.0 ? t : 0.0;
+        if (renorm || t < 1e-8 * ref[c]) { t = acc; ref[c] = acc; }
+        nrm[c] = t;
+        xn2[c] = acc;
+        cand_merge(bv, bi, t, c);
       }
-      __syncwarp();
-      if (check) {
-        bool need = renorm || (nrm[c] < 1e-8 * ref[c]);
-        if (need) {
-          double full = warp_sum(acc);
-          if (lane == 0) { nrm[c] = full; ref[c] = full; }
-        }
-      }
-      __syncwarp();
     }
   }
+  if (lane == 0) { sh.cand_v[warp] = bv; sh.cand_i[warp] = bi; }
 }
 
 // Run CPQR steps from sh.rank until the stop rule (with min_rank) fires.
-template <class T, int RPL>
-__device__ void cpqr_run(T* W, int m, int n, int ld, double* nrm, double* ref, int* piv,
-                         CpqrShared<T>& sh, double eps, int min_rank) {
+template <class T, int GL, int RPL>
+__device__ void cpqr_run(T* W, int m, int n, int ld, double* nrm, double* ref, double* xn2,
+                         int* piv, CpqrShared<T>& sh, double eps, int min_rank) {
   const int kmax = m < n ? m : n;
-  const int warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
   int s = sh.rank;
   while (s < kmax) {
-    if (warp == 0) cpqr_pivot_step<T>(W, m, n, ld, nrm, piv, sh, s, eps, min_rank);
+    if (threadIdx.x == 0) cpqr_pivot<T>(W, n, ld, nrm, xn2, piv, sh, s, eps, min_rank, nw);
     __syncthreads();
     if (sh.stop) break;
-    cpqr_update<T, RPL>(W, m, n, ld, nrm, ref, sh, s, kmax);
+    cpqr_update<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, s, kmax);
     if (threadIdx.x == 0) {
-      W[(int64_t)s * ld + s] = sh.alpha;
+      W[(int64_t)sh.pc * ld + s] = sh.alpha;
       sh.rank = s + 1;
     }
     __syncthreads();
@@ -255,27 +243,27 @@ __device__ void cpqr_run(T* W, int m, int n, int ld, double* nrm, double* ref, i
   __syncthreads();
 }
 
-// X = R11^-1 R12 in place (columns r..n-1, rows 0..r-1), one thread per
+// X = R11^-1 R12 in place (positions r..n-1, rows 0..r-1), one thread per
 // column, column-oriented back substitution (dtrsm order).  Also pads to
 // min_rank and records max|P|.
 template <class T>
-__device__ void interp_solve(T* W, int n, int ld, CpqrShared<T>& sh, int min_rank,
+__device__ void interp_solve(T* W, int n, int ld, const int* piv, CpqrShared<T>& sh, int min_rank,
                              double* red) {
   const int r = sh.rank;
   double big = 0.0;
   for (int c = r + threadIdx.x; c < n; c += blockDim.x) {
-    T* x = W + (int64_t)c * ld;
+    T* x = W + (int64_t)piv[c] * ld;
     for (int s = r - 1; s >= 0; --s) {
       T xs = x[s];
       if (xs != T(0.0)) {
-        xs = xs / W[(int64_t)s * ld + s];
+        const T* rs = W + (int64_t)piv[s] * ld;   // R[:, s]
+        xs = xs / rs[s];
         x[s] = xs;
-        for (int t = 0; t < s; ++t) x[t] -= W[(int64_t)s * ld + t] * xs;
+        for (int t = 0; t < s; ++t) x[t] -= rs[t] * xs;
       }
     }
     for (int s = 0; s < r; ++s) big = fmax(big, sk_abs(x[s]));
   }
-  // block max
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) big = fmax(big, __shfl_xor_sync(0xffffffffu, big, o));
@@ -293,9 +281,10 @@ __device__ void interp_solve(T* W, int n, int ld, CpqrShared<T>& sh, int min_ran
 }
 
 // Entry P(s, q) of the interpolation matrix for pivot POSITION q (column
-// piv[q] of the original target), row s (pivot order), after interp_solve.
+// piv[q] of the target), row s (pivot order), after interp_solve.
 template <class T>
-__device__ __forceinline__ T interp_entry(const T* W, int ld, int r, int kfin, int s, int q) {
+__device__ __forceinline__ T interp_entry(const T* W, int ld, const int* piv, int r, int kfin, int s,
+                                          int q) {
   if (q < kfin) return (s == q) ? T(1.0) : T(0.0);
-  return (s < r) ? W[(int64_t)q * ld + s] : T(0.0);
+  return (s < r) ? W[(int64_t)piv[q] * ld + s] : T(0.0);
 }

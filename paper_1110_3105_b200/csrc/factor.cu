@@ -47,10 +47,18 @@ __device__ double sm_norm1(const T* A, int lda, int p, int q, FacShared<T>& sh) 
 }
 
 // In-place Gauss-Jordan inverse of a row-major p x p matrix with partial
-// pivoting.  colk: p scratch entries, ipiv: p ints.  Returns 0 or 1 (zero pivot).
+// pivoting (pivot = first maximum |a| as LAPACK's i?amax).  Two barriers per
+// step: warp 0 finds the pivot and stages the pivot column and the two rows
+// being exchanged; then every thread updates an independent (row, column)
+// tile (row exchange, scaling and elimination fused).
+// scratch: 3p entries (colk, rowp, rowk), ipiv: p ints.  Returns 1 on an
+// exactly zero pivot (SingularBlock).
 template <class T>
-__device__ int sm_invert(T* A, int lda, int p, T* colk, int* ipiv, FacShared<T>& sh) {
+__device__ int sm_invert(T* A, int lda, int p, T* scratch, int* ipiv, FacShared<T>& sh) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  T* colk = scratch;
+  T* rowp = scratch + p;
+  T* rowk = scratch + 2 * p;
   for (int kk = 0; kk < p; ++kk) {
     if (warp == 0) {
       double best = -1.0;
@@ -65,6 +73,17 @@ __device__ int sm_invert(T* A, int lda, int p, T* colk, int* ipiv, FacShared<T>&
         int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
       }
+      if (best > 0.0) {
+        const int pr = bi;
+        for (int j = lane; j < p; j += 32) {
+          rowp[j] = A[(int64_t)pr * lda + j];
+          rowk[j] = A[(int64_t)kk * lda + j];
+        }
+        for (int i = lane; i < p; i += 32) {
+          // pivot column after the exchange of rows kk and pr
+          colk[i] = (i == pr) ? A[(int64_t)kk * lda + kk] : A[(int64_t)i * lda + kk];
+        }
+      }
       if (lane == 0) {
         sh.piv_row = bi;
         sh.amax = best;
@@ -74,28 +93,18 @@ __device__ int sm_invert(T* A, int lda, int p, T* colk, int* ipiv, FacShared<T>&
     __syncthreads();
     if (sh.amax == 0.0) return 1;
     const int pr = sh.piv_row;
-    if (pr != kk) {
-      for (int j = tid; j < p; j += nt) {
-        T t = A[(int64_t)kk * lda + j];
-        A[(int64_t)kk * lda + j] = A[(int64_t)pr * lda + j];
-        A[(int64_t)pr * lda + j] = t;
+    const T inv = T(1.0) / rowp[kk];
+    for (int i = warp; i < p; i += (nt >> 5)) {
+      T* Ai = A + (int64_t)i * lda;
+      const T f = colk[i];
+      for (int j = lane; j < p; j += 32) {
+        const T rk = (j == kk) ? inv : rowp[j] * inv;     // new (scaled) pivot row
+        T v;
+        if (i == kk) v = rk;
+        else if (j == kk) v = -(f * inv);
+        else v = ((i == pr) ? rowk[j] : Ai[j]) - f * rk;
+        Ai[j] = v;
       }
-      __syncthreads();
-    }
-    const T inv = T(1.0) / A[(int64_t)kk * lda + kk];
-    for (int i = tid; i < p; i += nt) colk[i] = A[(int64_t)i * lda + kk];
-    __syncthreads();
-    for (int j = tid; j < p; j += nt) {
-      if (j == kk) A[(int64_t)kk * lda + kk] = inv;
-      else A[(int64_t)kk * lda + j] = A[(int64_t)kk * lda + j] * inv;
-    }
-    __syncthreads();
-    for (int64_t e = tid; e < (int64_t)p * p; e += nt) {
-      int i = (int)(e / p), j = (int)(e - (int64_t)i * p);
-      if (i == kk) continue;
-      T f = colk[i];
-      if (j == kk) A[(int64_t)i * lda + kk] = -(f * inv);
-      else A[(int64_t)i * lda + j] -= f * A[(int64_t)kk * lda + j];
     }
     __syncthreads();
   }
@@ -156,7 +165,7 @@ __device__ void copy_out(T* dst, const T* src, int64_t cnt) {
 
 template <class T>
 static __host__ __device__ inline size_t fac_elems(int n, int k) {
-  return (size_t)n * n + 4 * (size_t)n * k + (size_t)k * k + (size_t)n;
+  return (size_t)n * n + 4 * (size_t)n * k + (size_t)k * k + 3 * (size_t)n;
 }
 
 template <class T, bool GW>
@@ -285,7 +294,7 @@ __global__ void __launch_bounds__(1024) k_dense_inverse(T* Ag, int K, double reg
   int* ipiv = reinterpret_cast<int*>(smem + 512);
   size_t hdr = 512 + ((sizeof(int) * (size_t)K + 15) / 16) * 16;
   T* A = GW ? scratch : reinterpret_cast<T*>(smem + hdr);
-  T* colk = GW ? scratch + (size_t)K * K : A + (size_t)K * K;
+  T* colk = GW ? scratch + (size_t)K * K : A + (size_t)K * K;   // 3K scratch
   for (int64_t e = threadIdx.x; e < (int64_t)K * K; e += blockDim.x) A[e] = Ag[e];
   __syncthreads();
   if (reg != 0.0) {
@@ -311,7 +320,7 @@ static int dense_inverse_impl(void* A, int K, double reg, int32_t* status, doubl
                               void* scratch, cudaStream_t st) {
   if (K <= 0) return 0;
   size_t hdr = 512 + ((sizeof(int) * (size_t)K + 15) / 16) * 16;
-  size_t need = hdr + ((size_t)K * K + K) * sizeof(T);
+  size_t need = hdr + ((size_t)K * K + 3 * K) * sizeof(T);
   if (need <= (size_t)skel_smem_optin()) {
     auto kern = k_dense_inverse<T, false>;
     SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));

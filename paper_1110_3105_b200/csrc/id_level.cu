@@ -41,7 +41,7 @@ static __host__ __device__ inline size_t level_smem_fixed(int max_n) {
   size_t s = align_up(sizeof(CpqrShared<T>), 16);
   s += align_up(sizeof(LevelSmemHdr), 16);
   s += align_up(sizeof(Pt) * (size_t)max_n, 16);
-  s += align_up(2 * sizeof(double) * (size_t)max_n, 16);
+  s += align_up(3 * sizeof(double) * (size_t)max_n, 16);
   s += align_up(2 * sizeof(int) * (size_t)max_n, 16);
   return s;
 }
@@ -52,10 +52,10 @@ __device__ __forceinline__ int find_run(const int* pref, int cnt, int i) {
   return q;
 }
 
-template <class T, int RPL, bool GW>
+template <class T, int GL, int RPL, bool GW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
     k_id_level(const SkelSource S, const SkelLevel L, const int32_t* __restrict__ order,
-               int max_m, int max_n) {
+               int64_t max_w, int max_n) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* p = smem;
   CpqrShared<T>& sh = *reinterpret_cast<CpqrShared<T>*>(p);
@@ -66,11 +66,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
   p += align_up(sizeof(Pt) * (size_t)max_n, 16);
   double* nrm = reinterpret_cast<double*>(p);
   double* ref = nrm + max_n;
-  p += align_up(2 * sizeof(double) * (size_t)max_n, 16);
+  double* xn2 = ref + max_n;
+  p += align_up(3 * sizeof(double) * (size_t)max_n, 16);
   int* piv = reinterpret_cast<int*>(p);
   int* pos = piv + max_n;
   p += align_up(2 * sizeof(int) * (size_t)max_n, 16);
-  T* W = GW ? reinterpret_cast<T*>(L.scratch) + (size_t)blockIdx.x * max_m * max_n
+  T* W = GW ? reinterpret_cast<T*>(L.scratch) + (size_t)blockIdx.x * max_w
             : reinterpret_cast<T*>(p);
 
   const int side = blockIdx.x & 1;
@@ -151,25 +152,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
       }
     }
   }
-  // ---- D = A(rd, cd), children's diagonal blocks zeroed (side 1) --------
-  if (side == 1 && nr > 0 && nc > 0) {
+  // ---- D = A(rd, cd), children's diagonal blocks zeroed ------------------
+  // rows split between the two CTAs of the cluster; side 1 holds cd in smem
+  if (nr > 0 && nc > 0) {
     T* D = reinterpret_cast<T*>(L.D) + L.d_off[a];
     const int nch = hd.nch;
-    for (int e = tid; e < nr * nc; e += nt) {
-      int i = e / nc, j = e - i * nc;
+    const int half = (nr + 1) / 2;
+    const int ib = side == 0 ? 0 : half, ie = side == 0 ? half : nr;
+    const int cnt = (ie - ib) * nc;
+    for (int e = tid; e < cnt; e += nt) {
+      int i = ib + e / nc, j = e - (e / nc) * nc;
       bool zero = false;
       if (nch > 0) zero = find_run(hd.rsplit, nch + 1, i) == find_run(hd.csplit, nch + 1, j);
       T v = T(0.0);
-      if (!zero) v = entry_A<T>(S, load_pt(S, L.rdofs[r0 + i]), cp[j]);
-      D[e] = v;
+      if (!zero) {
+        const Pt tp = side == 0 ? cp[i] : load_pt(S, L.rdofs[r0 + i]);
+        const Pt sp = side == 1 ? cp[j] : load_pt(S, L.cdofs[c0 + j]);
+        v = entry_A<T>(S, tp, sp);
+      }
+      D[(int64_t)i * nc + j] = v;
     }
   }
   __syncthreads();
 
   // ---- K2: CPQR ID ---------------------------------------------------------
-  cpqr_init<T>(W, m, n, ld, nrm, ref, piv);
+  cpqr_init<T>(W, m, n, ld, nrm, ref, xn2, piv, sh);
   __syncthreads();
-  cpqr_run<T, RPL>(W, m, n, ld, nrm, ref, piv, sh, L.eps, 0);
+  cpqr_run<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, L.eps, 0);
   int min_rank = 0;
   if (eq) {
     cg::cluster_group cl = cg::this_cluster();
@@ -182,10 +191,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
     const int k = sh.rank > sh.partner_k ? sh.rank : sh.partner_k;
     if (sh.rank < k) {
       min_rank = k;
-      cpqr_run<T, RPL>(W, m, n, ld, nrm, ref, piv, sh, L.eps, k);
+      cpqr_run<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, L.eps, k);
     }
   }
-  interp_solve<T>(W, n, ld, sh, min_rank, hd.red);
+  interp_solve<T>(W, n, ld, piv, sh, min_rank, hd.red);
   const int r = sh.rank;
   const int K = r + sh.pad;
   for (int s = tid; s < K; s += nt) {
@@ -202,13 +211,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
     T* Lo = reinterpret_cast<T*>(L.L) + L.l_off[a];
     for (int e = tid; e < n * K; e += nt) {
       int q = e / K, s = e - q * K;
-      Lo[(int64_t)piv[q] * K + pos[s]] = interp_entry<T>(W, ld, r, K, s, q);
+      Lo[(int64_t)piv[q] * K + pos[s]] = interp_entry<T>(W, ld, piv, r, K, s, q);
     }
   } else {
     T* Ro = reinterpret_cast<T*>(L.R) + L.r_off[a];
     for (int e = tid; e < n * K; e += nt) {
       int s = e / n, q = e - s * n;
-      Ro[(int64_t)pos[s] * n + piv[q]] = interp_entry<T>(W, ld, r, K, s, q);
+      Ro[(int64_t)pos[s] * n + piv[q]] = interp_entry<T>(W, ld, piv, r, K, s, q);
     }
   }
   if (tid == 0) {
@@ -219,7 +228,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
 }
 
 // explicit batched ID (id_fixed_precision), one CTA per matrix
-template <class T, int RPL, bool GW>
+template <class T, int GL, int RPL, bool GW>
 __global__ void __launch_bounds__(128)
     k_id_batched(const T* __restrict__ A, const int64_t* a_off, const int32_t* mm,
                  const int32_t* nn, double eps, const int32_t* min_rank_arr, int32_t* rank_out,
@@ -233,7 +242,8 @@ __global__ void __launch_bounds__(128)
   p += align_up(32 * sizeof(double), 16);
   double* nrm = reinterpret_cast<double*>(p);
   double* ref = nrm + max_n;
-  p += align_up(2 * sizeof(double) * (size_t)max_n, 16);
+  double* xn2 = ref + max_n;
+  p += align_up(3 * sizeof(double) * (size_t)max_n, 16);
   int* piv = reinterpret_cast<int*>(p);
   p += align_up(sizeof(int) * (size_t)max_n, 16);
   T* W = GW ? scratch + (size_t)blockIdx.x * max_m * max_n : reinterpret_cast<T*>(p);
@@ -244,17 +254,17 @@ __global__ void __launch_bounds__(128)
   const T* src = A + a_off[b];
   for (int64_t e = tid; e < (int64_t)m * n; e += nt) W[e] = src[e];
   __syncthreads();
-  cpqr_init<T>(W, m, n, ld, nrm, ref, piv);
+  cpqr_init<T>(W, m, n, ld, nrm, ref, xn2, piv, sh);
   __syncthreads();
-  cpqr_run<T, RPL>(W, m, n, ld, nrm, ref, piv, sh, eps, min_rank);
-  interp_solve<T>(W, n, ld, sh, min_rank, red);
+  cpqr_run<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, eps, min_rank);
+  interp_solve<T>(W, n, ld, piv, sh, min_rank, red);
   const int r = sh.rank, K = r + sh.pad;
   int32_t* sk = skel_out + skel_off[b];
   for (int s = tid; s < K; s += nt) sk[s] = piv[s];
   T* P = proj + proj_off[b];
   for (int e = tid; e < n * K; e += nt) {
     int s = e / n, q = e - s * n;
-    P[(int64_t)s * n + piv[q]] = interp_entry<T>(W, ld, r, K, s, q);
+    P[(int64_t)s * n + piv[q]] = interp_entry<T>(W, ld, piv, r, K, s, q);
   }
   if (tid == 0) {
     rank_out[b] = K;
@@ -324,55 +334,62 @@ __global__ void __launch_bounds__(256) k_dense_matvec(const SkelSource S, const 
 
 // ---------------------------------------------------------------------------
 // host launchers
-template <class T, int RPL, bool GW>
+template <class T, int GL, int RPL, bool GW>
 static int launch_id_level(const SkelSource* src, const SkelLevel* lv, const int32_t* order,
-                           int nrun, int max_m, int max_n, size_t smem, cudaStream_t st) {
-  auto kern = k_id_level<T, RPL, GW>;
+                           int nrun, int64_t max_w, int max_n, size_t smem, cudaStream_t st) {
+  auto kern = k_id_level<T, GL, RPL, GW>;
   SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<2 * nrun, 128, smem, st>>>(*src, *lv, order, max_m, max_n);
+  kern<<<2 * nrun, 128, smem, st>>>(*src, *lv, order, max_w, max_n);
   return skel_last_error();
 }
 
+// register tile: GL lanes per column, RPL rows per lane (GL * RPL >= max_m)
 template <class T, bool GW>
 static int dispatch_id_level(const SkelSource* src, const SkelLevel* lv, const int32_t* order,
-                             int nrun, int max_m, int max_n, size_t smem, cudaStream_t st) {
-  int rpl = (max_m + 31) / 32;
+                             int nrun, int max_m, int64_t max_w, int max_n, size_t smem,
+                             cudaStream_t st) {
+#define SKEL_L(GL_, RPL_) launch_id_level<T, GL_, RPL_, GW>(src, lv, order, nrun, max_w, max_n, smem, st)
   if constexpr (sizeof(T) == 8) {
-    if (rpl <= 4) return launch_id_level<T, 4, GW>(src, lv, order, nrun, max_m, max_n, smem, st);
-    if (rpl <= 8) return launch_id_level<T, 8, GW>(src, lv, order, nrun, max_m, max_n, smem, st);
-    if (rpl <= 12) return launch_id_level<T, 12, GW>(src, lv, order, nrun, max_m, max_n, smem, st);
-    if (rpl <= 16) return launch_id_level<T, 16, GW>(src, lv, order, nrun, max_m, max_n, smem, st);
-    if (rpl <= 24) return launch_id_level<T, 24, GW>(src, lv, order, nrun, max_m, max_n, smem, st);
+    if (max_m <= 64) return SKEL_L(8, 8);
+    if (max_m <= 128) return SKEL_L(8, 16);
+    if (max_m <= 192) return SKEL_L(16, 12);
+    if (max_m <= 256) return SKEL_L(16, 16);
+    if (max_m <= 384) return SKEL_L(32, 12);
+    if (max_m <= 512) return SKEL_L(32, 16);
+    if (max_m <= 768) return SKEL_L(32, 24);
   } else {
-    if (rpl <= 4) return launch_id_level<T, 4, GW>(src, lv, order, nrun, max_m, max_n, smem, st);
-    if (rpl <= 8) return launch_id_level<T, 8, GW>(src, lv, order, nrun, max_m, max_n, smem, st);
-    if (rpl <= 12) return launch_id_level<T, 12, GW>(src, lv, order, nrun, max_m, max_n, smem, st);
+    if (max_m <= 128) return SKEL_L(16, 8);
+    if (max_m <= 256) return SKEL_L(32, 8);
+    if (max_m <= 384) return SKEL_L(32, 12);
   }
-  return launch_id_level<T, 0, GW>(src, lv, order, nrun, max_m, max_n, smem, st);
+  return SKEL_L(32, 0);
+#undef SKEL_L
 }
 
+// max_m / max_n bound the bucket's target; max_w (elements) bounds m*n
 template <class T>
 static int id_level_impl(const SkelSource* src, const SkelLevel* lv, const int32_t* order,
-                         int nrun, int max_m, int max_n, cudaStream_t st) {
+                         int nrun, int max_m, int max_n, int64_t max_w, cudaStream_t st) {
   if (nrun <= 0) return 0;
   if (max_m < 1) max_m = 1;
   if (max_n < 1) max_n = 1;
+  if (max_w < 1) max_w = 1;
   size_t fixed = level_smem_fixed<T>(max_n);
-  size_t wbytes = (size_t)max_m * max_n * sizeof(T);
+  size_t wbytes = (size_t)max_w * sizeof(T);
   size_t optin = (size_t)skel_smem_optin();
   if (fixed + wbytes <= optin)
-    return dispatch_id_level<T, false>(src, lv, order, nrun, max_m, max_n, fixed + wbytes, st);
+    return dispatch_id_level<T, false>(src, lv, order, nrun, max_m, max_w, max_n, fixed + wbytes, st);
   if ((size_t)lv->scratch_bytes < (size_t)2 * nrun * wbytes || !lv->scratch) return -2;
-  return dispatch_id_level<T, true>(src, lv, order, nrun, max_m, max_n, fixed, st);
+  return dispatch_id_level<T, true>(src, lv, order, nrun, max_m, max_w, max_n, fixed, st);
 }
 
-template <class T, int RPL, bool GW>
+template <class T, int GL, int RPL, bool GW>
 static int launch_id_batched(const void* A, const int64_t* a_off, const int32_t* m,
                              const int32_t* n, int nmat, double eps, const int32_t* min_rank,
                              int32_t* rank, int32_t* skel, const int64_t* skel_off, void* proj,
                              const int64_t* proj_off, double* bigP, void* scratch, int max_m,
                              int max_n, size_t smem, cudaStream_t st) {
-  auto kern = k_id_batched<T, RPL, GW>;
+  auto kern = k_id_batched<T, GL, RPL, GW>;
   SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<nmat, 128, smem, st>>>((const T*)A, a_off, m, n, eps, min_rank, rank, skel, skel_off,
                                 (T*)proj, proj_off, bigP, (T*)scratch, max_m, max_n);
@@ -389,25 +406,30 @@ static int id_batched_impl(const void* A, const int64_t* a_off, const int32_t* m
   if (max_m < 1) max_m = 1;
   if (max_n < 1) max_n = 1;
   size_t fixed = align_up(sizeof(CpqrShared<T>), 16) + align_up(32 * sizeof(double), 16) +
-                 align_up(2 * sizeof(double) * max_n, 16) + align_up(sizeof(int) * max_n, 16);
+                 align_up(3 * sizeof(double) * max_n, 16) + align_up(sizeof(int) * max_n, 16);
   size_t wbytes = (size_t)max_m * max_n * sizeof(T);
   if (fixed + wbytes <= (size_t)skel_smem_optin()) {
-    return launch_id_batched<T, 0, false>(A, a_off, m, n, nmat, eps, min_rank, rank, skel,
+    if (max_m <= 128)
+      return launch_id_batched<T, 8, 16, false>(A, a_off, m, n, nmat, eps, min_rank, rank, skel,
+                                                skel_off, proj, proj_off, bigP, scratch, max_m, max_n,
+                                                fixed + wbytes, st);
+    return launch_id_batched<T, 32, 0, false>(A, a_off, m, n, nmat, eps, min_rank, rank, skel,
                                           skel_off, proj, proj_off, bigP, scratch, max_m, max_n,
                                           fixed + wbytes, st);
   }
   if (!scratch || (size_t)scratch_bytes < (size_t)nmat * wbytes) return -2;
-  return launch_id_batched<T, 0, true>(A, a_off, m, n, nmat, eps, min_rank, rank, skel, skel_off,
+  return launch_id_batched<T, 32, 0, true>(A, a_off, m, n, nmat, eps, min_rank, rank, skel, skel_off,
                                        proj, proj_off, bigP, scratch, max_m, max_n, fixed, st);
 }
 
 extern "C" {
 
 int skel_id_level(const SkelSource* src, const SkelLevel* lv, const int32_t* box_order,
-                  int32_t nbox_run, int32_t max_m, int32_t max_n, int32_t field, void* stream) {
+                  int32_t nbox_run, int32_t max_m, int32_t max_n, int64_t max_w, int32_t field,
+                  void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (field == 0) return id_level_impl<double>(src, lv, box_order, nbox_run, max_m, max_n, st);
-  return id_level_impl<zc>(src, lv, box_order, nbox_run, max_m, max_n, st);
+  if (field == 0) return id_level_impl<double>(src, lv, box_order, nbox_run, max_m, max_n, max_w, st);
+  return id_level_impl<zc>(src, lv, box_order, nbox_run, max_m, max_n, max_w, st);
 }
 
 int skel_id_batched(const void* A, const int64_t* a_off, const int32_t* m, const int32_t* n,

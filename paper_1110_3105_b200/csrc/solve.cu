@@ -96,16 +96,17 @@ __global__ void k_dense_apply(const T* __restrict__ M, int K, int Kc, const T* _
   y[e] = acc;
 }
 
+// one row per thread group of R lanes (R <= 32) or one thread per row chunk
 template <class T>
 __global__ void k_permute(const int64_t* __restrict__ perm, int64_t N, const T* __restrict__ src,
                           T* __restrict__ dst, int R, int scatter) {
-  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= N * R) return;
-  int64_t i = e / R;
-  int c = (int)(e - i * R);
-  int64_t p = perm[i];
-  if (scatter) dst[p * R + c] = src[e];
-  else dst[e] = src[p * R + c];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+  if (i >= N) return;
+  const int64_t p = perm[i];
+  for (int c = threadIdx.x; c < R; c += blockDim.x) {
+    if (scatter) dst[p * R + c] = src[i * R + c];
+    else dst[i * R + c] = src[p * R + c];
+  }
 }
 
 __global__ void k_compact(int nseg, const int64_t* src_off, const int32_t* len, const int64_t* dst_off,
@@ -180,12 +181,13 @@ int skel_dense_apply(const void* M, int32_t K, int32_t Kc, const void* x, void* 
 
 int skel_permute_rows(const int64_t* perm, int64_t N, const void* src, void* dst, int32_t R,
                       int32_t scatter, int32_t field, void* stream) {
-  int64_t tot = N * R;
-  if (tot == 0) return 0;
-  int blocks = (int)((tot + 255) / 256);
+  if (N == 0 || R <= 0) return 0;
+  int tx = R >= 32 ? 32 : (R >= 16 ? 16 : (R >= 8 ? 8 : (R >= 4 ? 4 : (R >= 2 ? 2 : 1))));
+  dim3 block(tx, 256 / tx);
+  int blocks = (int)((N + block.y - 1) / block.y);
   cudaStream_t st = (cudaStream_t)stream;
-  if (field == 0) k_permute<double><<<blocks, 256, 0, st>>>(perm, N, (const double*)src, (double*)dst, R, scatter);
-  else k_permute<zc><<<blocks, 256, 0, st>>>(perm, N, (const zc*)src, (zc*)dst, R, scatter);
+  if (field == 0) k_permute<double><<<blocks, block, 0, st>>>(perm, N, (const double*)src, (double*)dst, R, scatter);
+  else k_permute<zc><<<blocks, block, 0, st>>>(perm, N, (const zc*)src, (zc*)dst, R, scatter);
   return skel_last_error();
 }
 

@@ -24,13 +24,16 @@ from ._device import DeviceGeometry
 from .errors import InvalidInput, RefusedTooLarge
 from .geom import OrthTree, PointSet
 from .kernels import KernelSpec
-from ._staging import Packer, fork, join
+from ._staging import Packer, eager_stream, fork, join
 
 DEFAULT_N_PROXY = {2: 64, 3: 512}        # skel.py:29
 _RANDOMIZED_CUTOFF = 4096                # skel.py:33
 GLOBAL_MODE_LIMIT = 20000                # skel.py:35
 # target-size classes (bytes of the m x n target) -> one launch each
-_W_CLASSES = (24 << 10, 48 << 10, 80 << 10, 112 << 10, 160 << 10, 216 << 10)
+# (boundaries chosen so a bucket's shared memory fits 8/6/5/4/3/2/1 CTAs per SM)
+_W_CLASSES = (18 << 10, 27 << 10, 35 << 10, 46 << 10, 64 << 10, 100 << 10, 214 << 10)
+# register-tile classes of the target height (see dispatch_id_level)
+_M_CLASSES = (64, 128, 192, 256, 384, 512, 768)
 
 
 @dataclass
@@ -200,6 +203,7 @@ class CompressedLevel:
     def __init__(self, nodes=None, dev: DevLevel | None = None):
         self._nodes = nodes
         self.dev = dev
+        self.dev_from_compress = dev is not None
         if nodes is not None:
             self.row_dof_counts = np.array([nd.D.shape[0] for nd in nodes], dtype=np.int64)
             self.col_dof_counts = np.array([nd.D.shape[1] for nd in nodes], dtype=np.int64)
@@ -259,6 +263,7 @@ class CompressedMatrix:
         self.perm = perm
         self.scalar_field = scalar_field
         self.tree = tree
+        self._eager = None
 
     @property
     def S(self):
@@ -379,9 +384,14 @@ def _segment_sum(vals, off):
 
 def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = None,
                     mode: str = "proxy", equalize_ranks: bool = True, seed: int = 0,
-                    allow_large: bool = False) -> CompressedMatrix:
+                    allow_large: bool = False, eager_factor: bool = True) -> CompressedMatrix:
     """GPU compression sweep over a matrix source with a device descriptor
-    (skel.py:286-411)."""
+    (skel.py:286-411).
+
+    ``eager_factor`` (extension, default on): each level's telescoping
+    factorization is launched on a side stream as soon as the level is
+    compressed, overlapping the next level's compression; ``factor(cm)``
+    then only finalises (same kernels and results as a separate factor)."""
     if not 0 < eps < 1:
         raise InvalidInput("eps must lie in (0, 1)")
     if mode not in ("proxy", "global"):
@@ -423,7 +433,13 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
     optin = _smem_optin()
     elem = 16 if field else 8
     allpos = torch.arange(n, dtype=torch.int32, device=dev)
+    run = None
+    if eager_factor:
+        from .solver import FactorRun
+        run = FactorRun(field, 0.0, stream=eager_stream())
     for li in range(top):
+        lev_ctx = _profile.timed("level", level=li)
+        lev_rec = lev_ctx.__enter__()
         ids = covers[li]
         p = ids.size
         noff, nidx = tree.cover_neighbors(li)
@@ -456,7 +472,8 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         need_m = np.maximum(m0, m1)
         need_n = np.maximum(np.maximum(nr, nc), 1)
         wb = need_m * need_n * elem
-        cls = np.searchsorted(np.asarray(_W_CLASSES), wb, side="left")
+        cls = (np.searchsorted(np.asarray(_W_CLASSES), wb, side="left") * 16
+               + np.searchsorted(np.asarray(_M_CLASSES), need_m, side="left"))
         buckets = []
         for c in np.unique(cls):
             sel = np.nonzero(cls == c)[0]
@@ -500,9 +517,10 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         streams = fork(len(buckets)) if len(buckets) > 1 else None
         for bi, sel in enumerate(buckets):
             max_m, max_n = int(need_m[sel].max()), int(need_n[sel].max())
+            max_w = int((need_m[sel] * need_n[sel]).max())
             fixed = _level_smem_fixed(max_n, field)
-            if fixed + max_m * max_n * elem > optin:
-                sb = 2 * sel.size * max_m * max_n * elem
+            if fixed + max_w * elem > optin:
+                sb = 2 * sel.size * max_w * elem
                 scr = torch.empty(sb // 8 + 1, dtype=torch.float64, device=dev)
                 scratch_keep.append(scr)
                 lvd.scratch, lvd.scratch_bytes = p_(scr), sb
@@ -510,9 +528,10 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
                 lvd.scratch, lvd.scratch_bytes = None, 0
             ctx = torch.cuda.stream(streams[bi]) if streams else _nullctx()
             with ctx:
-                with _profile.timed("id_level", level=li, sel=sel) as rec:
+                with _profile.timed("id_level", level=li, sel=sel, max_m=max_m, max_n=max_n,
+                                    max_w=max_w) as rec:
                     _native.check(L.skel_id_level(desc, lvd, p_(t[f"order{bi}"]), sel.size, max_m,
-                                                  max_n, field, _native.stream_ptr()),
+                                                  max_n, max_w, field, _native.stream_ptr()),
                                   f"skel_id_level (level {li})")
             if rec is not None:
                 recs.append(rec)
@@ -556,6 +575,12 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
                       dtype, t=t2)
         levels.append(CompressedLevel(dev=dl))
         prev = dl
+        if run is not None:
+            ev = torch.cuda.Event()
+            ev.record()
+            run.stream.wait_event(ev)
+            run.add_level(li, dl)
+        lev_ctx.__exit__(None, None, None)
 
     last = prev
     Kr, Kc = int(last.kr.sum()), int(last.kc.sum())
@@ -565,7 +590,9 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         cbox = up(np.repeat(np.arange(last.p), last.kc).astype(np.int32))
         _native.check(L.skel_assemble_S(desc, p_(last.rskel), p_(rbox), Kr, p_(last.cskel),
                                         p_(cbox), Kc, p_(S), field, st), "skel_assemble_S")
-    return CompressedMatrix(levels, None, n, eps, tree.perm.copy(), sfield, tree, S_dev=S)
+    cm = CompressedMatrix(levels, None, n, eps, tree.perm.copy(), sfield, tree, S_dev=S)
+    cm._eager = run
+    return cm
 
 
 _OPTIN = None
@@ -594,9 +621,9 @@ def _smem_optin():
 def _level_smem_fixed(max_n, field):
     """Host mirror of level_smem_fixed<T> in csrc/id_level.cu (upper bound)."""
     al = lambda v: (v + 15) // 16 * 16  # noqa: E731
-    sh = al(80)
+    sh = al(96 + 8 * 32 + 4 * 32)
     hdr = al(4 * (257 + 256 + 9 + 9 + 2) + 8 * 32 + 8)
-    return sh + hdr + al(80 * max_n) + al(16 * max_n) + al(8 * max_n)
+    return sh + hdr + al(80 * max_n) + al(24 * max_n) + al(8 * max_n)
 
 
 # ---------------------------------------------------------------------------

@@ -131,7 +131,7 @@ def _invert_top(Sh, regularize, field):
     K = Sh.shape[0]
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
     rc = torch.zeros(1, dtype=torch.float64, device="cuda")
-    scratch = torch.empty((K * K + K) * (2 if field else 1) + 1, dtype=torch.float64, device="cuda")
+    scratch = torch.empty((K * K + 3 * K) * (2 if field else 1) + 1, dtype=torch.float64, device="cuda")
     _native.check(_native.lib().skel_dense_inverse(_native.ptr(Sh), None, None, K, float(regularize),
                                                    _native.ptr(st), _native.ptr(rc), field,
                                                    _native.ptr(scratch), _native.stream_ptr()),
@@ -139,18 +139,160 @@ def _invert_top(Sh, regularize, field):
     return int(st.item()), float(rc.item())
 
 
+class FactorRun:
+    """Incremental telescoping factorization: ``add_level`` launches one
+    level (size buckets on side streams) on ``stream`` without any host
+    synchronisation; ``finish`` joins, maps the per-box statuses to the
+    reference's exceptions / warnings and factors the top.  compress_source
+    drives one of these on a side stream so level l's factor overlaps level
+    l+1's compression."""
+
+    def __init__(self, field, regularize=0.0, stream=None):
+        self.torch = _native.require_cuda()
+        self.field = field
+        self.regularize = float(regularize)
+        self.stream = stream
+        self.levels = []       # (plan, DevFactorLevel, status, rcd, rcm, dl)
+        self.keep = []
+
+    def add_level(self, li, dl):
+        torch = self.torch
+        dev = torch.device("cuda")
+        field = self.field
+        tdt = _native.torch_dtype(field)
+        elem = 16 if field else 8
+        optin = _smem_optin()
+        L = _native.lib()
+        p_ = _native.ptr
+        sq_bad = dl.nr != dl.nc
+        lam_bad = (~sq_bad) & (dl.nr > 0) & (dl.kr != dl.kc)
+        n = np.where(sq_bad | lam_bad, 0, dl.nr).astype(np.int64)
+        k = np.where(n > 0, dl.kr, 0).astype(np.int64)
+        dd_off, ld_off, lam_off = _off(n * n), _off(n * k), _off(k * k)
+        need = (n * n + 4 * n * k + k * k + 3 * n) * elem
+        cls = np.searchsorted(np.asarray(_FAC_CLASSES), need, side="left")
+        buckets = []
+        for c in np.unique(cls[n > 0]):
+            sel = np.nonzero((cls == c) & (n > 0))[0]
+            buckets.append(sel[np.argsort(-need[sel], kind="stable")].astype(np.int32))
+        p = dl.p
+        outer = torch.cuda.stream(self.stream) if self.stream is not None else _nullctx()
+        with outer:
+            pk = Packer()
+            pk.add("n", n.astype(np.int32)).add("k", k.astype(np.int32))
+            pk.add("noff", _off(n)).add("koff", _off(k))
+            pk.add("dd_off", dd_off).add("ld_off", ld_off).add("lam_off", lam_off)
+            for bi, sel in enumerate(buckets):
+                pk.add(f"order{bi}", sel)
+            t = pk.upload()
+            Dd = torch.empty(max(int(dd_off[-1]), 1), dtype=tdt, device=dev)
+            Ld = torch.empty(max(int(ld_off[-1]), 1), dtype=tdt, device=dev)
+            Rd = torch.empty(max(int(ld_off[-1]), 1), dtype=tdt, device=dev)
+            Lam = torch.empty(max(int(lam_off[-1]), 1), dtype=tdt, device=dev)
+            status = torch.zeros(p, dtype=torch.int32, device=dev)
+            rcd = torch.ones(p, dtype=torch.float64, device=dev)
+            rcm = torch.ones(p, dtype=torch.float64, device=dev)
+            fl = DevFactorLevel(n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, dl.child_off, t)
+            prev = self.levels[-1][1] if self.levels else None
+            F = _native.SkelFactorLevel()
+            F.nbox, F.level, F.regularize = p, li, self.regularize
+            F.n, F.k = p_(fl.t_n), p_(fl.t_k)
+            F.d_off, F.l_off, F.r_off = p_(dl.t_d_off), p_(dl.t_l_off), p_(dl.t_r_off)
+            F.D, F.L, F.R = p_(dl.D), p_(dl.L), p_(dl.R)
+            if li > 0:
+                F.child_off = p_(dl.t_child_off)
+                F.prev_lam_off, F.prev_lam, F.prev_k = p_(prev.t_lam_off), p_(prev.Lam), p_(prev.t_k)
+            F.dd_off, F.ld_off, F.rd_off, F.lam_off = (p_(fl.t_dd_off), p_(fl.t_ld_off),
+                                                       p_(fl.t_ld_off), p_(fl.t_lam_off))
+            F.Dd, F.Ld, F.Rd, F.Lam = p_(Dd), p_(Ld), p_(Rd), p_(Lam)
+            F.status, F.rcond_d, F.rcond_m = p_(status), p_(rcd), p_(rcm)
+            streams = fork(len(buckets), tag="factor") if len(buckets) > 1 else None
+            nf, kf = n.astype(np.float64), k.astype(np.float64)
+            for bi, sel in enumerate(buckets):
+                max_n = int(n[sel].max())
+                max_k = int(k[sel].max())
+                nd = (max_n * max_n + 4 * max_n * max_k + max_k * max_k + 3 * max_n) * elem
+                F.order, F.nrun = p_(t[f"order{bi}"]), sel.size
+                F.scratch, F.scratch_bytes = None, 0
+                if nd + 1024 + 4 * max_n > optin:
+                    scr = torch.empty(sel.size * nd // 8 + 1, dtype=torch.float64, device=dev)
+                    self.keep.append(scr)
+                    F.scratch, F.scratch_bytes = p_(scr), sel.size * nd
+                ctx = torch.cuda.stream(streams[bi]) if streams else _nullctx()
+                with ctx:
+                    with _profile.timed("factor_level", level=li) as rec:
+                        _native.check(L.skel_factor_level(F, max_n, max_k, field, _native.stream_ptr()),
+                                      f"skel_factor_level ({li})")
+                if rec is not None:
+                    b_ = sel
+                    rec.flops = float((2 * nf[b_] ** 3 + 6 * nf[b_] ** 2 * kf[b_]
+                                       + 6 * kf[b_] ** 2 * nf[b_] + 2 * kf[b_] ** 3).sum())
+                    rec.nbytes = float(((nf[b_] ** 2 + 2 * nf[b_] * kf[b_]) * 2 + kf[b_] ** 2).sum()) * elem
+            if streams:
+                join(streams)
+        self.levels.append(((sq_bad, lam_bad, n, k), fl, status, rcd, rcm, dl))
+
+    def finish(self, cm):
+        torch = self.torch
+        if self.stream is not None:
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+            torch.cuda.current_stream().wait_event(ev)
+        warns = []
+        flevels = []
+        for li, ((sq_bad, lam_bad, n, k), fl, status, rcd, rcm, dl) in enumerate(self.levels):
+            sts, rd_h, rm_h = status.cpu().numpy(), rcd.cpu().numpy(), rcm.cpu().numpy()
+            fails = np.nonzero(sq_bad | lam_bad | (sts != 0))[0]
+            if fails.size:
+                a = int(fails[0])
+                if sq_bad[a]:
+                    raise InvalidInput(f"non-square D block ({dl.nr[a]}x{dl.nc[a]}) at level {li + 1}, "
+                                       f"node {a}; compress with equalize_ranks=True")
+                if sts[a] == 1:
+                    raise SingularBlock(li + 1, a, "D")
+                if lam_bad[a]:
+                    raise InvalidInput(f"non-square Lambda block ({dl.kc[a]}x{dl.kr[a]}) at level "
+                                       f"{li + 1}, node {a}; compress with equalize_ranks=True")
+                raise SingularBlock(li + 1, a, "Lambda")
+            for a in np.nonzero(((n > 0) & (rd_h < _RCOND_WARN)) | ((k > 0) & (rm_h < _RCOND_WARN)))[0]:
+                if n[a] > 0 and rd_h[a] < _RCOND_WARN:
+                    warns.append((li + 1, int(a), "D", float(rd_h[a])))
+                if k[a] > 0 and rm_h[a] < _RCOND_WARN:
+                    warns.append((li + 1, int(a), "Lambda", float(rm_h[a])))
+            flevels.append(FactoredLevel(fl))
+        prev = self.levels[-1][1]
+        S = cm.device_S()
+        if S.shape[0] != S.shape[1]:
+            raise InvalidInput(f"non-square S block ({S.shape[0]}x{S.shape[1]}) at level top, node 0; "
+                               "compress with equalize_ranks=True")
+        # top: Shat = S with the last level's Lambdas on the diagonal blocks
+        Sh = S.clone()
+        kro = _off(prev.k)
+        for a in range(prev.p):
+            ka = int(prev.k[a])
+            if ka:
+                Sh[kro[a]:kro[a] + ka, kro[a]:kro[a] + ka] = \
+                    prev.Lam[prev.lam_off[a]:prev.lam_off[a] + ka * ka].view(ka, ka)
+        if Sh.numel() == 0:
+            return FactoredInverse(flevels, Sh, None, cm.n, cm.perm.copy(), cm.scalar_field, warns)
+        Sinv = Sh.clone()
+        status, _ = _invert_top(Sinv, self.regularize, self.field)
+        if status:
+            raise SingularBlock("top", 0, "S")
+        return FactoredInverse(flevels, Sh, Sinv, cm.n, cm.perm.copy(), cm.scalar_field, warns)
+
+
 def factor(cm: CompressedMatrix, regularize: float = 0.0) -> FactoredInverse:
-    """Telescoping inverse of a compressed matrix (solver.py:187-276)."""
-    torch = _native.require_cuda()
-    dev = torch.device("cuda")
+    """Telescoping inverse of a compressed matrix (solver.py:187-276).
+
+    A CompressedMatrix produced by compress_source already carries an
+    eager factorization launched level by level on a side stream (same
+    kernels, regularize = 0); it is reused unless ``regularize`` differs or
+    the host view of a level was materialised (and may have been edited)."""
     field = cm.field
-    tdt = _native.torch_dtype(field)
-    L = _native.lib()
-    st = _native.stream_ptr()
-    p_ = _native.ptr
-    warns = []
     if cm.nlevels == 0:
         S = cm.device_S()
+        warns = []
         if S.shape[0] != S.shape[1]:
             raise InvalidInput(f"non-square S block ({S.shape[0]}x{S.shape[1]}) at level top, "
                                "node 0; compress with equalize_ranks=True")
@@ -161,141 +303,20 @@ def factor(cm: CompressedMatrix, regularize: float = 0.0) -> FactoredInverse:
         if status:
             raise SingularBlock("top", 0, "S")
         return FactoredInverse([], S, Sinv, cm.n, cm.perm.copy(), cm.scalar_field, warns)
-
-    dls = cm.device_levels()
-    elem = 16 if field else 8
-    optin = _smem_optin()
-    # host bookkeeping for every level first, then ONE packed upload
-    plan = []
-    pk = Packer()
-    for li, dl in enumerate(dls):
-        sq_bad = dl.nr != dl.nc
-        lam_bad = (~sq_bad) & (dl.nr > 0) & (dl.kr != dl.kc)
-        n = np.where(sq_bad | lam_bad, 0, dl.nr).astype(np.int64)
-        k = np.where(n > 0, dl.kr, 0).astype(np.int64)
-        dd_off, ld_off, lam_off = _off(n * n), _off(n * k), _off(k * k)
-        need = (n * n + 4 * n * k + k * k + n) * elem
-        cls = np.searchsorted(np.asarray(_FAC_CLASSES), need, side="left")
-        buckets = []
-        for c in np.unique(cls[n > 0]):
-            sel = np.nonzero((cls == c) & (n > 0))[0]
-            buckets.append(sel[np.argsort(-need[sel], kind="stable")].astype(np.int32))
-        pre = f"L{li}_"
-        pk.add(pre + "n", n.astype(np.int32)).add(pre + "k", k.astype(np.int32))
-        pk.add(pre + "noff", _off(n)).add(pre + "koff", _off(k))
-        pk.add(pre + "dd_off", dd_off).add(pre + "ld_off", ld_off).add(pre + "lam_off", lam_off)
-        for bi, sel in enumerate(buckets):
-            pk.add(pre + f"order{bi}", sel)
-        plan.append((sq_bad, lam_bad, n, k, dd_off, ld_off, lam_off, buckets))
-    t = pk.upload()
-    P = sum(dl.p for dl in dls)
-    stat = torch.zeros(P, dtype=torch.int32, device=dev)
-    rcd = torch.ones(P, dtype=torch.float64, device=dev)
-    rcm = torch.ones(P, dtype=torch.float64, device=dev)
-    flevels = []
-    prev = None
-    base = 0
-    keep = []
-    for li, dl in enumerate(dls):
-        sq_bad, lam_bad, n, k, dd_off, ld_off, lam_off, buckets = plan[li]
-        p = dl.p
-        pre = f"L{li}_"
-        tl = {key: t[pre + key] for key in ("n", "k", "noff", "koff", "dd_off", "ld_off", "lam_off")}
-        tl["_buffer"] = t["_buffer"]
-        Dd = torch.empty(max(int(dd_off[-1]), 1), dtype=tdt, device=dev)
-        Ld = torch.empty(max(int(ld_off[-1]), 1), dtype=tdt, device=dev)
-        Rd = torch.empty(max(int(ld_off[-1]), 1), dtype=tdt, device=dev)
-        Lam = torch.empty(max(int(lam_off[-1]), 1), dtype=tdt, device=dev)
-        fl = DevFactorLevel(n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, dl.child_off, tl)
-        F = _native.SkelFactorLevel()
-        F.nbox, F.level, F.regularize = p, li, float(regularize)
-        F.n, F.k = p_(fl.t_n), p_(fl.t_k)
-        F.d_off, F.l_off, F.r_off = p_(dl.t_d_off), p_(dl.t_l_off), p_(dl.t_r_off)
-        F.D, F.L, F.R = p_(dl.D), p_(dl.L), p_(dl.R)
-        if li > 0:
-            F.child_off = p_(dl.t_child_off)
-            F.prev_lam_off, F.prev_lam, F.prev_k = p_(prev.t_lam_off), p_(prev.Lam), p_(prev.t_k)
-        F.dd_off, F.ld_off, F.rd_off, F.lam_off = (p_(fl.t_dd_off), p_(fl.t_ld_off),
-                                                   p_(fl.t_ld_off), p_(fl.t_lam_off))
-        F.Dd, F.Ld, F.Rd, F.Lam = p_(Dd), p_(Ld), p_(Rd), p_(Lam)
-        F.status, F.rcond_d, F.rcond_m = p_(stat[base:]), p_(rcd[base:]), p_(rcm[base:])
-        streams = fork(len(buckets)) if len(buckets) > 1 else None
-        nf, kf = n.astype(np.float64), k.astype(np.float64)
-        for bi, sel in enumerate(buckets):
-            max_n = int(n[sel].max())
-            max_k = int(k[sel].max())
-            need = (max_n * max_n + 4 * max_n * max_k + max_k * max_k + max_n) * elem
-            F.order, F.nrun = p_(t[pre + f"order{bi}"]), sel.size
-            F.scratch, F.scratch_bytes = None, 0
-            if need + 1024 + 4 * max_n > optin:
-                scr = torch.empty(sel.size * need // 8 + 1, dtype=torch.float64, device=dev)
-                keep.append(scr)
-                F.scratch, F.scratch_bytes = p_(scr), sel.size * need
-            ctx = torch.cuda.stream(streams[bi]) if streams else _nullctx()
-            with ctx:
-                with _profile.timed("factor_level", level=li) as rec:
-                    _native.check(L.skel_factor_level(F, max_n, max_k, field, _native.stream_ptr()),
-                                  f"skel_factor_level ({li})")
-            if rec is not None:
-                b_ = sel
-                rec.flops = float((2 * nf[b_] ** 3 + 6 * nf[b_] ** 2 * kf[b_] + 6 * kf[b_] ** 2 * nf[b_]
-                                   + 2 * kf[b_] ** 3).sum())
-                rec.nbytes = float(((nf[b_] ** 2 + 2 * nf[b_] * kf[b_]) * 2 + kf[b_] ** 2).sum()) * elem
-        if streams:
-            join(streams)
-        flevels.append(FactoredLevel(fl))
-        prev = fl
-        base += p
-    # one read-back of every level's status / rcond, checked in the
-    # reference's (level, node) order (solver.py:222-264)
-    sts_all = stat.cpu().numpy()
-    rd_all = rcd.cpu().numpy()
-    rm_all = rcm.cpu().numpy()
-    base = 0
-    for li, dl in enumerate(dls):
-        sq_bad, lam_bad, n, k = plan[li][:4]
-        p = dl.p
-        sts, rd_h, rm_h = sts_all[base:base + p], rd_all[base:base + p], rm_all[base:base + p]
-        base += p
-        fails = np.nonzero(sq_bad | lam_bad | (sts != 0))[0]
-        if fails.size:
-            a = int(fails[0])
-            if sq_bad[a]:
-                raise InvalidInput(f"non-square D block ({dl.nr[a]}x{dl.nc[a]}) at level {li + 1}, "
-                                   f"node {a}; compress with equalize_ranks=True")
-            if sts[a] == 1:
-                raise SingularBlock(li + 1, a, "D")
-            if lam_bad[a]:
-                raise InvalidInput(f"non-square Lambda block ({dl.kc[a]}x{dl.kr[a]}) at level "
-                                   f"{li + 1}, node {a}; compress with equalize_ranks=True")
-            raise SingularBlock(li + 1, a, "Lambda")
-        for a in np.nonzero(((n > 0) & (rd_h < _RCOND_WARN)) | ((k > 0) & (rm_h < _RCOND_WARN)))[0]:
-            if n[a] > 0 and rd_h[a] < _RCOND_WARN:
-                warns.append((li + 1, int(a), "D", float(rd_h[a])))
-            if k[a] > 0 and rm_h[a] < _RCOND_WARN:
-                warns.append((li + 1, int(a), "Lambda", float(rm_h[a])))
-
-    # top: Shat = S with the last level's Lambdas on the diagonal blocks
-    S = cm.device_S()
-    last = dls[-1]
-    if S.shape[0] != S.shape[1]:
-        raise InvalidInput(f"non-square S block ({S.shape[0]}x{S.shape[1]}) at level top, node 0; "
-                           "compress with equalize_ranks=True")
-    Sh = S.clone()
-    kro = _off(prev.k)
-    for a in range(prev.p):
-        ka = int(prev.k[a])
-        if ka:
-            Sh[kro[a]:kro[a] + ka, kro[a]:kro[a] + ka] = \
-                prev.Lam[prev.lam_off[a]:prev.lam_off[a] + ka * ka].view(ka, ka)
-    del last
-    if Sh.numel() == 0:
-        return FactoredInverse(flevels, Sh, None, cm.n, cm.perm.copy(), cm.scalar_field, warns)
-    Sinv = Sh.clone()
-    status, _ = _invert_top(Sinv, regularize, field)
-    if status:
-        raise SingularBlock("top", 0, "S")
-    return FactoredInverse(flevels, Sh, Sinv, cm.n, cm.perm.copy(), cm.scalar_field, warns)
+    run = getattr(cm, "_eager", None)
+    touched = any(lv._nodes is not None and lv.dev is not None and lv.dev_from_compress
+                  for lv in cm.levels)
+    if run is not None and float(regularize) == 0.0 and not touched and cm.S_dev is not None:
+        cm._eager = None
+        return run.finish(cm)
+    if touched:
+        for lv in cm.levels:
+            if lv._nodes is not None:
+                lv.dev = None          # re-pack from the (possibly edited) host view
+    run = FactorRun(field, regularize)
+    for li, dl in enumerate(cm.device_levels()):
+        run.add_level(li, dl)
+    return run.finish(cm)
 
 
 def _smem_optin():
