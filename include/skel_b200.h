@@ -111,6 +111,7 @@ typedef struct {
   int32_t* flags;            /* bit0/1: |P| > 2 (row/col); bit2: ranks differ */
   void* scratch;             /* global fallback for targets over the smem limit */
   int64_t scratch_bytes;
+  int32_t debug_skip;        /* developer timing only: 1 = assembly only, 2 = + norms */
 } SkelLevel;
 
 /* Assemble + ID + equalize every box of one cover, both sides.
@@ -124,6 +125,12 @@ typedef struct {
 int skel_id_level(const SkelSource* src, const SkelLevel* lv, const int32_t* box_order,
                   int32_t nbox_run, int32_t max_m, int32_t max_n, int64_t max_w,
                   int32_t field, void* stream);
+
+/* D = A(rd, cd) of every box of a cover with the children's diagonal
+ * blocks zeroed (skel.py:344-348), into lv->D at lv->d_off.  max_n bounds
+ * n_r and n_c. */
+int skel_assemble_D(const SkelSource* src, const SkelLevel* lv, int32_t max_n, int32_t field,
+                    void* stream);
 
 /* Dense top-level skeleton matrix S = A(row_skel_a, col_skel_b), a != b,
  * zero diagonal blocks (skel.py:399-408). rows/cols: tree positions; rbox/cbox:

@@ -49,7 +49,7 @@ class SkelLevel(ctypes.Structure):
         ("d_off", c_vp), ("l_off", c_vp), ("r_off", c_vp),
         ("D", c_vp), ("L", c_vp), ("R", c_vp),
         ("rskel", c_vp), ("cskel", c_vp), ("kr", c_vp), ("kc", c_vp), ("flags", c_vp),
-        ("scratch", c_vp), ("scratch_bytes", c_i64),
+        ("scratch", c_vp), ("scratch_bytes", c_i64), ("debug_skip", c_i32),
     ]
 
 
@@ -71,6 +71,7 @@ class SkelFactorLevel(ctypes.Structure):
 _P = ctypes.POINTER
 _SIGS = {
     "skel_id_level": [_P(SkelSource), _P(SkelLevel), c_vp, c_i32, c_i32, c_i32, c_i64, c_i32, c_vp],
+    "skel_assemble_D": [_P(SkelSource), _P(SkelLevel), c_i32, c_i32, c_vp],
     "skel_assemble_S": [_P(SkelSource), c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp],
     "skel_eval_block": [_P(SkelSource), c_vp, c_i32, c_vp, c_i32, c_vp, c_i32, c_vp],
     "skel_id_batched": [c_vp, c_vp, c_vp, c_vp, c_i32, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp,
@@ -98,7 +99,7 @@ _SIGS = {
 _lib = None
 
 # entry points that launch kernels (the tree builder / queries run on the host)
-_LAUNCHING = {"skel_id_level", "skel_assemble_S", "skel_eval_block", "skel_id_batched",
+_LAUNCHING = {"skel_id_level", "skel_assemble_D", "skel_assemble_S", "skel_eval_block", "skel_id_batched",
               "skel_factor_level", "skel_dense_inverse", "skel_sweep_up_ex",
               "skel_sweep_down_ex", "skel_dense_apply", "skel_permute_rows",
               "skel_compact_i32", "skel_dense_matvec", "skel_fp64_probe"}

@@ -34,7 +34,11 @@ class _PinnedRing:
         while self.pending:
             s, e, ev = self.pending[0]
             if s < hi and lo < e:
-                ev.synchronize()
+                if not ev.query():
+                    # the copy that reads this region is still queued behind
+                    # other work (e.g. on the eager-factor stream): never
+                    # block the host on it, use a one-off pinned block
+                    return None, 0
                 self.pending.popleft()
             else:
                 break

@@ -15,6 +15,7 @@
 // re-run with min_rank = k because the CPQR is a deterministic state machine
 // whose first steps do not depend on min_rank.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "cpqr.cuh"
 #include "entries.cuh"
@@ -43,6 +44,7 @@ static __host__ __device__ inline size_t level_smem_fixed(int max_n) {
   s += align_up(sizeof(Pt) * (size_t)max_n, 16);
   s += align_up(3 * sizeof(double) * (size_t)max_n, 16);
   s += align_up(2 * sizeof(int) * (size_t)max_n, 16);
+  s += align_up(6 * sizeof(double) * (size_t)max_n, 16);   // fast-path column SoA
   return s;
 }
 
@@ -50,6 +52,129 @@ __device__ __forceinline__ int find_run(const int* pref, int cnt, int i) {
   int q = 0;
   while (q + 1 < cnt && pref[q + 1] <= i) ++q;
   return q;
+}
+
+// Fast K1 for the 2D Laplace double-layer BIE (BASELINE configs 1/2/5):
+// per-source constants hoisted (n.w/(2 pi), curvature limit), r^2 instead of
+// sqrt(r)^2, log(r^2)/(4 pi) for the single-layer proxies, four entries per
+// iteration for ILP.  Differs from numpy's evaluation order by a few ulps.
+__device__ __noinline__ void assemble_bie_lap2(const SkelSource& S, const SkelLevel& L, int a,
+                                               int side, int n, int m, int m_nbr, int nnb_c,
+                                               const int* nbr_pref, const int* nbr_box,
+                                               const int32_t* mydofs, const Pt* cp, double* fsoa,
+                                               int max_n, double* W, int ld) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const double inv2pi = 1.0 / SKEL_TWO_PI, inv4pi = 1.0 / SKEL_FOUR_PI;
+  const double tol2 = S.coincide_tol * S.coincide_tol;
+  const double ic = S.identity_coef;
+  double* fx = fsoa;
+  double* fy = fsoa + max_n;
+  double* fa = fsoa + 2 * max_n;   // side 1 sources: nx w / 2pi
+  double* fb = fsoa + 3 * max_n;   //                 ny w / 2pi
+  double* fc = fsoa + 4 * max_n;   //                 curvature limit * w
+  double* fw = fsoa + 5 * max_n;   //                 -w / 4pi (column proxies)
+  for (int j = tid; j < n; j += nt) {
+    const Pt q = cp[j];
+    fx[j] = q.x;
+    fy[j] = q.y;
+    fa[j] = q.nx * q.w * inv2pi;
+    fb[j] = q.ny * q.w * inv2pi;
+    fc[j] = (-q.kap * inv4pi) * q.w;
+    fw[j] = -q.w * inv4pi;
+  }
+  __syncthreads();
+  const int pb = L.pxy_begin[a];
+  const double rr = L.box_r[a];
+  const double cx = L.box_c[(int64_t)a * 2], cy = L.box_c[(int64_t)a * 2 + 1];
+  const double rowp = -S.wscale * inv4pi;
+  for (int i = tid; i < m; i += nt) {
+    double* Wi = W + i;
+    if (i < m_nbr) {
+      int q = find_run(nbr_pref, nnb_c + 1, i);
+      int b = nbr_box[q];
+      int off = i - nbr_pref[q];
+      const int32_t idx = side == 0 ? L.cdofs[L.cdof_off[b] + off] : L.rdofs[L.rdof_off[b] + off];
+      const double px = __ldg(S.x + idx), py = __ldg(S.y + idx);
+      if (side == 0) {
+        // row point is the SOURCE, box points are targets: t_row.T[i][j] = A(rd_j, nbr_i)
+        const double w = __ldg(S.w + idx);
+        const double sa = __ldg(S.nx + idx) * w * inv2pi, sb = __ldg(S.ny + idx) * w * inv2pi;
+        const double sc = (-__ldg(S.curv + idx) * inv4pi) * w;
+        int j = 0;
+        for (; j + 3 < n; j += 4) {
+          double v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double dx = fx[j + u] - px, dy = fy[j + u] - py;
+            const double r2 = dx * dx + dy * dy;
+            double e = (dx * sa + dy * sb) / r2;
+            if (r2 < tol2) e = sc;
+            if (mydofs[j + u] == idx) e += ic;
+            v[u] = e;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) Wi[(int64_t)(j + u) * ld] = v[u];
+        }
+        for (; j < n; ++j) {
+          const double dx = fx[j] - px, dy = fy[j] - py;
+          const double r2 = dx * dx + dy * dy;
+          double e = (dx * sa + dy * sb) / r2;
+          if (r2 < tol2) e = sc;
+          if (mydofs[j] == idx) e += ic;
+          Wi[(int64_t)j * ld] = e;
+        }
+      } else {
+        // row point is the TARGET, box points are sources: t_col[i][j] = A(nbr_i, cd_j)
+        int j = 0;
+        for (; j + 3 < n; j += 4) {
+          double v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double dx = px - fx[j + u], dy = py - fy[j + u];
+            const double r2 = dx * dx + dy * dy;
+            double e = (dx * fa[j + u] + dy * fb[j + u]) / r2;
+            if (r2 < tol2) e = fc[j + u];
+            if (mydofs[j + u] == idx) e += ic;
+            v[u] = e;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) Wi[(int64_t)(j + u) * ld] = v[u];
+        }
+        for (; j < n; ++j) {
+          const double dx = px - fx[j], dy = py - fy[j];
+          const double r2 = dx * dx + dy * dy;
+          double e = (dx * fa[j] + dy * fb[j]) / r2;
+          if (r2 < tol2) e = fc[j];
+          if (mydofs[j] == idx) e += ic;
+          Wi[(int64_t)j * ld] = e;
+        }
+      }
+    } else {
+      const int pr = pb + (i - m_nbr);
+      const double px = __dadd_rn(cx, __dmul_rn(rr, L.pxy_unit[(int64_t)pr * 2]));
+      const double py = __dadd_rn(cy, __dmul_rn(rr, L.pxy_unit[(int64_t)pr * 2 + 1]));
+      int j = 0;
+      for (; j + 3 < n; j += 4) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double dx = fx[j + u] - px, dy = fy[j + u] - py;
+          const double r2 = dx * dx + dy * dy;
+          // row proxy: wscale * (-log r / 2pi); column proxy: -log r / 2pi * w_j
+          const double g = log(r2);
+          v[u] = r2 < tol2 ? 0.0 : (side == 0 ? g * rowp : g * fw[j + u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) Wi[(int64_t)(j + u) * ld] = v[u];
+      }
+      for (; j < n; ++j) {
+        const double dx = fx[j] - px, dy = fy[j] - py;
+        const double r2 = dx * dx + dy * dy;
+        const double g = log(r2);
+        Wi[(int64_t)j * ld] = r2 < tol2 ? 0.0 : (side == 0 ? g * rowp : g * fw[j]);
+      }
+    }
+  }
 }
 
 template <class T, int GL, int RPL, bool GW>
@@ -71,12 +196,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
   int* piv = reinterpret_cast<int*>(p);
   int* pos = piv + max_n;
   p += align_up(2 * sizeof(int) * (size_t)max_n, 16);
+  double* fsoa = reinterpret_cast<double*>(p);
+  p += align_up(6 * sizeof(double) * (size_t)max_n, 16);
   T* W = GW ? reinterpret_cast<T*>(L.scratch) + (size_t)blockIdx.x * max_w
             : reinterpret_cast<T*>(p);
 
   const int side = blockIdx.x & 1;
   const int a = order[blockIdx.x >> 1];
   const int tid = threadIdx.x, nt = blockDim.x;
+  if (L.debug_skip == 3) { if (tid == 0) (side == 0 ? L.kr : L.kc)[a] = 0; return; }
   const bool eq = L.equalize != 0;
   if (eq) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
 
@@ -122,7 +250,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
   const int ld = m;
 
   // ---- K1: assemble the proxy-compressed target, column-major ----------
-  if (n > 0) {
+  const bool fast = sizeof(T) == sizeof(double) && S.kind == SKEL_SRC_BIE &&
+                    S.equation == SKEL_EQ_LAPLACE && S.dim == 2 && !S.kr10 && S.curvature_limit;
+  if (fast && n > 0) {
+    assemble_bie_lap2(S, L, a, side, n, m, m_nbr, nnb_c, hd.nbr_pref, hd.nbr_box, mydofs, cp,
+                      fsoa, max_n, reinterpret_cast<double*>(W), ld);
+  } else if (n > 0) {
     const int pb = L.pxy_begin[a];
     const double rr = L.box_r[a];
     const int dim = S.dim;
@@ -152,32 +285,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
       }
     }
   }
-  // ---- D = A(rd, cd), children's diagonal blocks zeroed ------------------
-  // rows split between the two CTAs of the cluster; side 1 holds cd in smem
-  if (nr > 0 && nc > 0) {
-    T* D = reinterpret_cast<T*>(L.D) + L.d_off[a];
-    const int nch = hd.nch;
-    const int half = (nr + 1) / 2;
-    const int ib = side == 0 ? 0 : half, ie = side == 0 ? half : nr;
-    const int cnt = (ie - ib) * nc;
-    for (int e = tid; e < cnt; e += nt) {
-      int i = ib + e / nc, j = e - (e / nc) * nc;
-      bool zero = false;
-      if (nch > 0) zero = find_run(hd.rsplit, nch + 1, i) == find_run(hd.csplit, nch + 1, j);
-      T v = T(0.0);
-      if (!zero) {
-        const Pt tp = side == 0 ? cp[i] : load_pt(S, L.rdofs[r0 + i]);
-        const Pt sp = side == 1 ? cp[j] : load_pt(S, L.cdofs[c0 + j]);
-        v = entry_A<T>(S, tp, sp);
-      }
-      D[(int64_t)i * nc + j] = v;
-    }
-  }
   __syncthreads();
 
   // ---- K2: CPQR ID ---------------------------------------------------------
+  if (L.debug_skip == 1) { if (tid == 0) (side == 0 ? L.kr : L.kc)[a] = 0; return; }
   cpqr_init<T>(W, m, n, ld, nrm, ref, xn2, piv, sh);
   __syncthreads();
+  if (L.debug_skip == 2) { if (tid == 0) (side == 0 ? L.kr : L.kc)[a] = 0; return; }
   cpqr_run<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, L.eps, 0);
   int min_rank = 0;
   if (eq) {
@@ -224,6 +338,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
     (side == 0 ? L.kr : L.kc)[a] = K;
     int f = (sh.bigP > 2.0 ? (1 << side) : 0) | (hd.err ? 8 : 0);
     if (f) atomicOr(L.flags + a, f);
+  }
+}
+
+// D = A(rd, cd) with the children's diagonal blocks zeroed (skel.py:344-348),
+// one CTA per box, both point sets staged in shared memory (SoA).
+template <class T>
+__global__ void __launch_bounds__(128) k_assemble_D(const SkelSource S, const SkelLevel L, int max_n) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Pt* rp = reinterpret_cast<Pt*>(smem);
+  Pt* cpp = rp + max_n;
+  __shared__ int rsplit[SKEL_MAX_CHILD + 1], csplit[SKEL_MAX_CHILD + 1], nch_s;
+  const int a = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int64_t r0 = L.rdof_off[a], c0 = L.cdof_off[a];
+  const int nr = (int)(L.rdof_off[a + 1] - r0), nc = (int)(L.cdof_off[a + 1] - c0);
+  if (nr == 0 || nc == 0) return;
+  if (tid == 0) {
+    int nch = 0;
+    rsplit[0] = 0; csplit[0] = 0;
+    if (L.child_off) {
+      const int64_t ch0 = L.child_off[a];
+      nch = (int)(L.child_off[a + 1] - ch0);
+      if (nch > SKEL_MAX_CHILD) nch = SKEL_MAX_CHILD;
+      for (int q = 0; q < nch; ++q) {
+        rsplit[q + 1] = rsplit[q] + L.prev_kr[ch0 + q];
+        csplit[q + 1] = csplit[q] + L.prev_kc[ch0 + q];
+      }
+    }
+    nch_s = nch;
+  }
+  for (int i = tid; i < nr; i += nt) rp[i] = load_pt(S, L.rdofs[r0 + i]);
+  for (int j = tid; j < nc; j += nt) cpp[j] = load_pt(S, L.cdofs[c0 + j]);
+  __syncthreads();
+  const int nch = nch_s;
+  T* D = reinterpret_cast<T*>(L.D) + L.d_off[a];
+  const bool fast = sizeof(T) == sizeof(double) && S.kind == SKEL_SRC_BIE &&
+                    S.equation == SKEL_EQ_LAPLACE && S.dim == 2 && !S.kr10 && S.curvature_limit;
+  const double inv2pi = 1.0 / SKEL_TWO_PI, inv4pi = 1.0 / SKEL_FOUR_PI;
+  const double tol2 = S.coincide_tol * S.coincide_tol;
+  for (int i = tid / 32; i < nr; i += nt / 32) {
+    const int ci = nch > 0 ? find_run(rsplit, nch + 1, i) : -1;
+    const Pt tp = rp[i];
+    for (int j = tid & 31; j < nc; j += 32) {
+      T v = T(0.0);
+      const bool zero = nch > 0 && ci == find_run(csplit, nch + 1, j);
+      if (!zero) {
+        if (fast) {
+          const Pt& sp = cpp[j];
+          const double dx = tp.x - sp.x, dy = tp.y - sp.y;
+          const double r2 = dx * dx + dy * dy;
+          double e = (dx * (sp.nx * sp.w * inv2pi) + dy * (sp.ny * sp.w * inv2pi)) / r2;
+          if (r2 < tol2) e = (-sp.kap * inv4pi) * sp.w;
+          if (tp.o == sp.o) e += S.identity_coef;
+          v = as_T<T>(e);
+        } else {
+          v = entry_A<T>(S, tp, cpp[j]);
+        }
+      }
+      D[(int64_t)i * nc + j] = v;
+    }
   }
 }
 
@@ -339,8 +512,21 @@ static int launch_id_level(const SkelSource* src, const SkelLevel* lv, const int
                            int nrun, int64_t max_w, int max_n, size_t smem, cudaStream_t st) {
   auto kern = k_id_level<T, GL, RPL, GW>;
   SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<2 * nrun, 128, smem, st>>>(*src, *lv, order, max_w, max_n);
+  // thread-per-column CPQR (RPL < 0): GL threads per column
+  const int threads = RPL < 0 ? 64 : 128;
+  kern<<<2 * nrun, threads, smem, st>>>(*src, *lv, order, max_w, max_n);
   return skel_last_error();
+}
+
+// CPQR update variant: 1 = thread per column (default), 0 = lane groups
+// (SKEL_ID_MODE environment override, read once)
+static int skel_id_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("SKEL_ID_MODE");
+    mode = (e && e[0] >= '0' && e[0] <= '9') ? e[0] - '0' : 1;
+  }
+  return mode;
 }
 
 // register tile: GL lanes per column, RPL rows per lane (GL * RPL >= max_m)
@@ -349,6 +535,11 @@ static int dispatch_id_level(const SkelSource* src, const SkelLevel* lv, const i
                              int nrun, int max_m, int64_t max_w, int max_n, size_t smem,
                              cudaStream_t st) {
 #define SKEL_L(GL_, RPL_) launch_id_level<T, GL_, RPL_, GW>(src, lv, order, nrun, max_w, max_n, smem, st)
+  if (skel_id_mode() == 1) {
+    if (max_n <= 40) return SKEL_L(2, -1);
+    return SKEL_L(1, -1);
+  }
+  if (skel_id_mode() == 2) return SKEL_L(4, -1);
   if constexpr (sizeof(T) == 8) {
     if (max_m <= 64) return SKEL_L(8, 8);
     if (max_m <= 128) return SKEL_L(8, 16);
@@ -430,6 +621,22 @@ int skel_id_level(const SkelSource* src, const SkelLevel* lv, const int32_t* box
   cudaStream_t st = (cudaStream_t)stream;
   if (field == 0) return id_level_impl<double>(src, lv, box_order, nbox_run, max_m, max_n, max_w, st);
   return id_level_impl<zc>(src, lv, box_order, nbox_run, max_m, max_n, max_w, st);
+}
+
+int skel_assemble_D(const SkelSource* src, const SkelLevel* lv, int32_t max_n, int32_t field,
+                    void* stream) {
+  if (lv->nbox <= 0) return 0;
+  if (max_n < 1) max_n = 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  size_t smem = 2 * sizeof(Pt) * (size_t)max_n;
+  if (field == 0) {
+    SKEL_TRY(cudaFuncSetAttribute(k_assemble_D<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_assemble_D<double><<<lv->nbox, 128, smem, st>>>(*src, *lv, max_n);
+  } else {
+    SKEL_TRY(cudaFuncSetAttribute(k_assemble_D<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_assemble_D<zc><<<lv->nbox, 128, smem, st>>>(*src, *lv, max_n);
+  }
+  return skel_last_error();
 }
 
 int skel_id_batched(const void* A, const int64_t* a_off, const int32_t* m, const int32_t* n,

@@ -19,6 +19,10 @@
 // the reference's lists.
 #include <algorithm>
 #include <array>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -185,7 +189,14 @@ struct TopItem {
   int64_t parent_item;
 };
 
+static double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
+  const bool timing = getenv("SKEL_TREE_TIMING") != nullptr;
+  double t0 = now_ms();
   T.dim = d;
   T.n = n;
   double lo_c[3] = {INFINITY, INFINITY, INFINITY}, hi_c[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -205,15 +216,39 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
   double scale = std::max(std::max(hw0, cabs), 1.0);
   hw0 = hw0 * (1.0 + kRootPad) + kRootPad * scale;
 
-  std::vector<int64_t> perm(n), tmpi(n);
-  std::vector<double> pxv[3], tmpx[3];
+  // scratch buffers are cached across builds: fresh multi-MB allocations
+  // cost more in first-touch page faults than the whole partitioning
+  static std::mutex scratch_mu;
+  static std::vector<int64_t> s_tmpi;
+  static std::vector<double> s_px[3], s_tmpx[3];
+  static std::vector<uint8_t> s_code;
+  std::lock_guard<std::mutex> guard(scratch_mu);
+  std::vector<int64_t> perm(n);
+  std::vector<int64_t>& tmpi = s_tmpi;
+  if ((int64_t)tmpi.size() < n) tmpi.resize(n);
+  std::vector<double>* pxv = s_px;
+  std::vector<double>* tmpx = s_tmpx;
   for (int a = 0; a < d; ++a) {
-    pxv[a].resize(n);
-    tmpx[a].resize(n);
-    for (int64_t i = 0; i < n; ++i) pxv[a][i] = X[i * d + a];
+    if ((int64_t)pxv[a].size() < n) pxv[a].resize(n);
+    if ((int64_t)tmpx[a].size() < n) tmpx[a].resize(n);
   }
-  for (int64_t i = 0; i < n; ++i) perm[i] = i;
-  std::vector<uint8_t> code(n);
+  {
+    unsigned hc = std::thread::hardware_concurrency();
+    const int T = (int)std::max(1u, std::min(hc == 0 ? 1u : hc, 32u));
+    const int64_t chunk = (n + T - 1) / T;
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+      th.emplace_back([&, t]() {
+        const int64_t a0 = t * chunk, a1 = std::min(n, a0 + chunk);
+        for (int64_t i = a0; i < a1; ++i) {
+          perm[i] = i;
+          for (int a = 0; a < d; ++a) pxv[a][i] = X[i * d + a];
+        }
+      });
+    for (auto& x : th) x.join();
+  }
+  std::vector<uint8_t>& code = s_code;
+  if ((int64_t)code.size() < n) code.resize(n);
   Builder B;
   B.d = d;
   B.max_leaf = max_leaf;
@@ -225,44 +260,101 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
     B.tmpx[a] = &tmpx[a];
   }
 
-  // serial top part down to a frontier with enough subtrees for the threads
+  double t0b = now_ms();
+  // top part, breadth first: all open nodes of a depth are split together
+  // (in parallel across nodes, or with the parallel counting sort for the
+  // few huge ones), down to a frontier of ranges small enough to become
+  // independent subtree tasks
   unsigned hwc = std::thread::hardware_concurrency();
   const int nthreads = (int)std::max(1u, std::min(hwc == 0 ? 1u : hwc, 32u));
   B.nthreads = nthreads;
-  const int64_t frontier_size = std::max<int64_t>(4 * max_leaf, n / (8 * nthreads));
-  std::vector<TopItem> items;
-  struct Fr { int64_t lo, hi; double c[3]; double hw; int64_t depth, parent_item; };
-  std::vector<Fr> stack;
-  stack.push_back({0, n, {c0[0], c0[1], c0[2]}, hw0, 0, -1});
-  while (!stack.empty()) {
-    Fr f = stack.back();
-    stack.pop_back();
-    TopItem it;
-    for (int a = 0; a < 3; ++a) it.rec.c[a] = f.c[a];
-    it.rec.hw = f.hw; it.rec.lo = f.lo; it.rec.hi = f.hi; it.rec.depth = f.depth;
-    it.rec.parent = -1; it.rec.nchild = 0;
-    it.parent_item = f.parent_item;
-    const int64_t sz = f.hi - f.lo;
-    const bool leaf = sz <= max_leaf || f.depth >= kMaxDepth;
-    it.task = !leaf && sz <= frontier_size;
-    const int64_t me = (int64_t)items.size();
-    if (f.parent_item >= 0) items[f.parent_item].rec.nchild += 1;
-    items.push_back(it);
-    if (leaf || it.task) continue;
-    int64_t cnt[8];
-    B.split(f.lo, f.hi, f.c, cnt);
-    std::vector<Fr> kids;
-    int64_t s = f.lo;
-    for (int c = 0; c < (1 << d); ++c) {
-      if (cnt[c] == 0) continue;
-      Fr k;
-      for (int a = 0; a < 3; ++a) k.c[a] = a < d ? f.c[a] + (((c >> a) & 1) ? 0.5 : -0.5) * f.hw : 0.0;
-      k.lo = s; k.hi = s + cnt[c]; k.hw = 0.5 * f.hw; k.depth = f.depth + 1; k.parent_item = me;
-      kids.push_back(k);
-      s += cnt[c];
-    }
-    for (auto it2 = kids.rbegin(); it2 != kids.rend(); ++it2) stack.push_back(*it2);
+  const int64_t frontier_size = std::max<int64_t>(4 * max_leaf, n / (4 * nthreads));
+  struct TNode {
+    NodeRec rec;
+    bool task, leaf;
+    std::vector<int64_t> kids;
+  };
+  std::vector<TNode> top;
+  {
+    TNode r;
+    for (int a = 0; a < 3; ++a) r.rec.c[a] = c0[a];
+    r.rec.hw = hw0; r.rec.lo = 0; r.rec.hi = n; r.rec.depth = 0; r.rec.parent = -1; r.rec.nchild = 0;
+    top.push_back(r);
   }
+  std::vector<int64_t> open = {0};
+  while (!open.empty()) {
+    std::vector<int64_t> to_split;
+    for (int64_t id : open) {
+      TNode& t = top[id];
+      const int64_t sz = t.rec.hi - t.rec.lo;
+      t.leaf = sz <= max_leaf || t.rec.depth >= kMaxDepth;
+      t.task = !t.leaf && sz <= frontier_size;
+      if (!t.leaf && !t.task) to_split.push_back(id);
+    }
+    std::vector<std::array<int64_t, 8>> counts(to_split.size());
+    const int big = (int)std::count_if(to_split.begin(), to_split.end(), [&](int64_t id) {
+      return top[id].rec.hi - top[id].rec.lo >= ((int64_t)1 << 17);
+    });
+    if ((int)to_split.size() < nthreads || big == (int)to_split.size()) {
+      for (size_t q = 0; q < to_split.size(); ++q) {
+        const NodeRec& r = top[to_split[q]].rec;
+        B.split(r.lo, r.hi, r.c, counts[q].data());
+      }
+    } else {
+      std::atomic_int next(0);
+      Builder Bs = B;
+      Bs.nthreads = 1;
+      std::vector<std::thread> pool;
+      auto worker = [&]() {
+        for (;;) {
+          int q = next.fetch_add(1);
+          if (q >= (int)to_split.size()) break;
+          const NodeRec& r = top[to_split[q]].rec;
+          Bs.split(r.lo, r.hi, r.c, counts[q].data());
+        }
+      };
+      for (int i = 0; i < nthreads; ++i) pool.emplace_back(worker);
+      for (auto& th : pool) th.join();
+    }
+    std::vector<int64_t> nxt;
+    for (size_t q = 0; q < to_split.size(); ++q) {
+      const int64_t id = to_split[q];
+      int64_t s0 = top[id].rec.lo;
+      for (int c = 0; c < (1 << d); ++c) {
+        const int64_t cnt = counts[q][c];
+        if (cnt == 0) continue;
+        TNode k;
+        const NodeRec& pr = top[id].rec;
+        for (int a = 0; a < 3; ++a) k.rec.c[a] = a < d ? pr.c[a] + (((c >> a) & 1) ? 0.5 : -0.5) * pr.hw : 0.0;
+        k.rec.hw = 0.5 * pr.hw; k.rec.lo = s0; k.rec.hi = s0 + cnt; k.rec.depth = pr.depth + 1;
+        k.rec.parent = id; k.rec.nchild = 0;
+        s0 += cnt;
+        top.push_back(k);
+        top[id].kids.push_back((int64_t)top.size() - 1);
+        top[id].rec.nchild += 1;
+        nxt.push_back((int64_t)top.size() - 1);
+      }
+    }
+    open.swap(nxt);
+  }
+  // preorder item list of the top part (children in code order)
+  std::vector<TopItem> items;
+  {
+    std::vector<std::pair<int64_t, int64_t>> st = {{0, -1}};   // (top node, parent item)
+    while (!st.empty()) {
+      auto [id, pitem] = st.back();
+      st.pop_back();
+      TopItem it;
+      it.rec = top[id].rec;
+      it.task = top[id].task;
+      it.parent_item = pitem;
+      const int64_t me = (int64_t)items.size();
+      items.push_back(it);
+      const std::vector<int64_t>& ks = top[id].kids;
+      for (auto r = ks.rbegin(); r != ks.rend(); ++r) st.push_back({*r, me});
+    }
+  }
+  double t1 = now_ms();
   // parallel subtrees (ranges are disjoint, so the in-place sorts do not race)
   std::vector<int64_t> task_ids;
   for (int64_t i = 0; i < (int64_t)items.size(); ++i)
@@ -283,6 +375,7 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
     for (int i = 0; i < nt; ++i) pool.emplace_back(worker);
     for (auto& th : pool) th.join();
   }
+  double t2 = now_ms();
   // splice in preorder
   std::vector<int64_t> item_gid(items.size());
   int64_t gid = 0;
@@ -317,15 +410,20 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
     }
   }
   T.perm = std::move(perm);
+  double t3 = now_ms();
   // covers in id order == sorted by range start (preorder, disjoint ranges)
   int64_t maxd = 0;
   for (int64_t i = 0; i < nn; ++i) maxd = std::max(maxd, T.depth[i]);
   T.covers.assign(maxd + 1, {});
-  for (int64_t f = maxd; f >= 0; --f) {
-    std::vector<int64_t>& cov = T.covers[maxd - f];
-    for (int64_t i = 0; i < nn; ++i)
-      if (T.depth[i] == f || (T.nchild[i] == 0 && T.depth[i] < f)) cov.push_back(i);
+  // node i lies in cover f iff depth == f, or it is a leaf shallower than f;
+  // visiting nodes in id order keeps every cover sorted by range start
+  for (int64_t i = 0; i < nn; ++i) {
+    const int64_t f1 = T.nchild[i] == 0 ? maxd : T.depth[i];
+    for (int64_t f = T.depth[i]; f <= f1; ++f) T.covers[maxd - f].push_back(i);
   }
+  if (timing)
+    fprintf(stderr, "tree: setup %.2f ms, top %.2f, subtrees %.2f ms (%zu tasks, %d threads), splice %.2f ms, covers %.2f ms\n",
+            t0b - t0, t1 - t0b, t2 - t1, task_ids.size(), nthreads, t3 - t2, now_ms() - t3);
 }
 
 inline bool touch(const Tree& T, int64_t na, int64_t nb, double tol) {

@@ -414,6 +414,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
     tdt = _native.torch_dtype(field)
     covers = tree.levels
     top = next(i for i, c in enumerate(covers) if len(c) == 1)
+    top_run = min(top, _DEBUG_MAX_LEVELS[0]) if _DEBUG_MAX_LEVELS[0] else top
     L = _native.lib()
     st = _native.stream_ptr()
     p_ = _native.ptr
@@ -437,7 +438,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
     if eager_factor:
         from .solver import FactorRun
         run = FactorRun(field, 0.0, stream=eager_stream())
-    for li in range(top):
+    for li in range(top_run):
         lev_ctx = _profile.timed("level", level=li)
         lev_rec = lev_ctx.__enter__()
         ids = covers[li]
@@ -499,6 +500,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         lvd = _native.SkelLevel()
         lvd.nbox, lvd.level, lvd.equalize, lvd.n_unit = p, li, int(bool(equalize_ranks)), unit.shape[0]
         lvd.eps = float(eps)
+        lvd.debug_skip = _DEBUG_SKIP[0]
         lvd.rdof_off, lvd.rdofs = p_(t["rdof_off"]), p_(rdofs)
         lvd.cdof_off, lvd.cdofs = p_(t["cdof_off"]), p_(cdofs)
         if li > 0:
@@ -514,7 +516,12 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         lvd.kr, lvd.kc, lvd.flags = p_(kk[:p]), p_(kk[p:2 * p]), p_(kk[2 * p:])
         scratch_keep = []
         recs = []
-        streams = fork(len(buckets)) if len(buckets) > 1 else None
+        streams = fork(len(buckets) + 1)
+        # D blocks on their own stream, concurrent with the ID buckets
+        with torch.cuda.stream(streams[-1]):
+            with _profile.timed("assemble_D", level=li):
+                _native.check(L.skel_assemble_D(desc, lvd, int(max(nr.max(initial=0), nc.max(initial=0), 1)),
+                                                field, _native.stream_ptr()), "skel_assemble_D")
         for bi, sel in enumerate(buckets):
             max_m, max_n = int(need_m[sel].max()), int(need_n[sel].max())
             max_w = int((need_m[sel] * need_n[sel]).max())
@@ -535,8 +542,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
                                   f"skel_id_level (level {li})")
             if rec is not None:
                 recs.append(rec)
-        if streams:
-            join(streams)
+        join(streams)
         kk_h = kk.cpu().numpy()
         kr = kk_h[:p].astype(np.int64)
         kc = kk_h[p:2 * p].astype(np.int64)
@@ -582,6 +588,8 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             run.add_level(li, dl)
         lev_ctx.__exit__(None, None, None)
 
+    if top_run < top:      # developer benchmarking only: partial sweep
+        return levels
     last = prev
     Kr, Kc = int(last.kr.sum()), int(last.kc.sum())
     S = torch.zeros((max(Kr, 0), max(Kc, 0)), dtype=tdt, device=dev)
@@ -596,6 +604,8 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
 
 
 _OPTIN = None
+_DEBUG_MAX_LEVELS = [0]      # developer benchmarking: stop the sweep after this many levels
+_DEBUG_SKIP = [0]            # developer benchmarking: 1 = assembly only, 2 = + column norms
 
 
 class _nullctx:
@@ -623,7 +633,7 @@ def _level_smem_fixed(max_n, field):
     al = lambda v: (v + 15) // 16 * 16  # noqa: E731
     sh = al(96 + 8 * 32 + 4 * 32)
     hdr = al(4 * (257 + 256 + 9 + 9 + 2) + 8 * 32 + 8)
-    return sh + hdr + al(80 * max_n) + al(24 * max_n) + al(8 * max_n)
+    return sh + hdr + al(80 * max_n) + al(24 * max_n) + al(8 * max_n) + al(48 * max_n)
 
 
 # ---------------------------------------------------------------------------

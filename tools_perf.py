@@ -6,7 +6,7 @@ import torch
 import paper_1110_3105_b200 as sk
 from paper_1110_3105_b200 import _profile
 
-def run(n, eps, R, reps=2, detail=True):
+def run(n, eps, R, reps=4, detail=True):
     curve = sk.bie.ellipse(2.0, 1.0, n)
     system = sk.bie.discretize_dirichlet(curve, sk.KernelSpec("laplace", 2))
     for rep in range(reps):
