@@ -85,38 +85,64 @@ __device__ void cpqr_init(const T* W, int m, int n, int ld, double* nrm, double*
   if (lane == 0) { sh.cand_v[warp] = bv; sh.cand_i[warp] = bi; }
 }
 
-// Phase A of step s (thread 0).
+// Phase A of step s (warp 0).  Lane 0 merges the per-warp candidates into
+// the pivot (first maximum), applies the stop rule and swaps the position
+// bookkeeping; the exact |x| of the pivot column is either the trailing norm
+// the update phase maintained (xn2 != NULL) or a warp reduction over rows s..m-1.
 template <class T>
-__device__ void cpqr_pivot(T* W, int n, int ld, double* nrm, double* xn2, int* piv,
+__device__ void cpqr_pivot(T* W, int m, int n, int ld, double* nrm, double* xn2, int* piv,
                            CpqrShared<T>& sh, int s, double eps, int min_rank, int nw) {
-  double bv = -1.0;
-  int j = 0x7fffffff;
-  for (int w = 0; w < nw; ++w) cand_merge(bv, j, sh.cand_v[w], sh.cand_i[w]);
-  if (j >= n) { sh.stop = 1; return; }
-  double pn = sqrt(fmax(nrm[j], 0.0));
-  if (s == 0) {
-    sh.p0 = pn;
-    if (pn == 0.0) { sh.stop = 1; return; }
+  const int lane = threadIdx.x & 31;
+  int stop = 0, pc = 0;
+  double nx2 = 0.0;
+  if (lane == 0) {
+    double bv = -1.0;
+    int j = 0x7fffffff;
+    for (int w = 0; w < nw; ++w) cand_merge(bv, j, sh.cand_v[w], sh.cand_i[w]);
+    if (j >= n) {
+      stop = 1;
+    } else {
+      double pn = sqrt(fmax(nrm[j], 0.0));
+      if (s == 0) {
+        sh.p0 = pn;
+        if (pn == 0.0) stop = 1;
+      }
+      if (!stop && ((s >= min_rank && pn <= eps * sh.p0) || pn == 0.0)) stop = 1;
+      if (!stop) {
+        if (j != s) {
+          double t = nrm[s]; nrm[s] = nrm[j]; nrm[j] = t;
+          if (xn2) { t = xn2[s]; xn2[s] = xn2[j]; xn2[j] = t; }
+          int q = piv[s]; piv[s] = piv[j]; piv[j] = q;
+        }
+        pc = piv[s];
+        if (xn2) nx2 = xn2[s];
+        else if (s == 0) nx2 = nrm[s];          // exact full norm at step 0
+      }
+    }
+    sh.stop = stop;
   }
-  if ((s >= min_rank && pn <= eps * sh.p0) || pn == 0.0) { sh.stop = 1; return; }
-  if (j != s) {
-    double t = nrm[s]; nrm[s] = nrm[j]; nrm[j] = t;
-    t = xn2[s]; xn2[s] = xn2[j]; xn2[j] = t;
-    int q = piv[s]; piv[s] = piv[j]; piv[j] = q;
+  stop = __shfl_sync(0xffffffffu, stop, 0);
+  if (stop) return;
+  pc = __shfl_sync(0xffffffffu, pc, 0);
+  if (!xn2 && s > 0) {
+    const T* x = W + (int64_t)pc * ld;
+    double acc = 0.0;
+    for (int i = s + lane; i < m; i += SKEL_WARP) acc += sk_abs2(x[i]);
+    nx2 = warp_sum(acc);
   }
-  const int pc = piv[s];
-  const T x0 = W[(int64_t)pc * ld + s];
-  const double ax0 = sk_abs(x0);
-  const double normx = sqrt(xn2[s]);
-  T phase = T(1.0);
-  if (ax0 != 0.0) phase = sk_unit_phase(x0, ax0);   // x0 / |x0|
-  const T alpha = -(phase * normx);
-  const double vv = 2.0 * normx * (normx + ax0);    // |x - alpha e1|^2
-  sh.v0 = x0 - alpha;
-  sh.alpha = alpha;
-  sh.beta = vv > 0.0 ? 2.0 / vv : 0.0;
-  sh.pc = pc;
-  sh.stop = 0;
+  if (lane == 0) {
+    const T x0 = W[(int64_t)pc * ld + s];
+    const double ax0 = sk_abs(x0);
+    const double normx = sqrt(nx2);
+    T phase = T(1.0);
+    if (ax0 != 0.0) phase = sk_unit_phase(x0, ax0);   // x0 / |x0|
+    const T alpha = -(phase * normx);
+    const double vv = 2.0 * normx * (normx + ax0);    // |x - alpha e1|^2
+    sh.v0 = x0 - alpha;
+    sh.alpha = alpha;
+    sh.beta = vv > 0.0 ? 2.0 / vv : 0.0;
+    sh.pc = pc;
+  }
 }
 
 // Phase B of step s (all warps).  Register path: a column is handled by a
@@ -161,26 +187,37 @@ __device__ void cpqr_update(T* W, int m, int n, int ld, double* nrm, double* ref
 #pragma unroll
       for (int o = GL / 2; o > 0; o >>= 1) dot += shfl_xor_T(dot, o);
       const T f = dot * beta;
-      double x4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int r = 0; r < RPL; ++r) {
         int i = s + gl + GL * r;
         if (beta != 0.0) wr[r] -= vr[r] * f;
-        if (i < m) {
-          if (beta != 0.0 && act) wc[i] = wr[r];
-          if (i > s) x4[r & 3] += sk_abs2(wr[r]);
-        }
+        if (i < m && beta != 0.0 && act) wc[i] = wr[r];
       }
-      double xa = (x4[0] + x4[1]) + (x4[2] + x4[3]);
-#pragma unroll
-      for (int o = GL / 2; o > 0; o >>= 1) xa += __shfl_xor_sync(0xffffffffu, xa, o);
+      // downdate; the exact trailing norm is only needed on the rare
+      // renormalisation / stale steps (lowrank.py:71-81)
+      double t = 0.0;
+      int need = 0;
       if (gl == 0 && act) {
         // wr[0] of the group leader is row s of the updated column (R[s, c])
-        double t = nrm[c] - sk_abs2(wr[0]);
+        t = nrm[c] - sk_abs2(wr[0]);
         t = t > 0.0 ? t : 0.0;
-        if (renorm || t < 1e-8 * ref[c]) { t = xa; ref[c] = xa; }
+        need = (s1 < kmax) && (renorm || t < 1e-8 * ref[c]);
+      }
+      need = __shfl_sync(0xffffffffu, need, g * GL);
+      if (__any_sync(0xffffffffu, need)) {
+        double x4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          int i = s + gl + GL * r;
+          if (i < m && i > s) x4[r & 3] += sk_abs2(wr[r]);
+        }
+        double xa = (x4[0] + x4[1]) + (x4[2] + x4[3]);
+#pragma unroll
+        for (int o = GL / 2; o > 0; o >>= 1) xa += __shfl_xor_sync(0xffffffffu, xa, o);
+        if (gl == 0 && need) { t = xa; ref[c] = xa; }
+      }
+      if (gl == 0 && act) {
         nrm[c] = t;
-        xn2[c] = xa;
         cand_merge(bv, bi, t, c);
       }
     }
@@ -312,7 +349,9 @@ __device__ void cpqr_run(T* W, int m, int n, int ld, double* nrm, double* ref, d
   const int nw = blockDim.x >> 5;
   int s = sh.rank;
   while (s < kmax) {
-    if (threadIdx.x == 0) cpqr_pivot<T>(W, n, ld, nrm, xn2, piv, sh, s, eps, min_rank, nw);
+    if (threadIdx.x < 32)
+      cpqr_pivot<T>(W, m, n, ld, nrm, (RPL < 0 || RPL == 0) ? xn2 : nullptr, piv, sh, s, eps,
+                    min_rank, nw);
     __syncthreads();
     if (sh.stop) break;
     if constexpr (RPL < 0) cpqr_update_lpc<T, GL>(W, m, n, ld, nrm, ref, xn2, piv, sh, s, kmax);

@@ -518,13 +518,14 @@ static int launch_id_level(const SkelSource* src, const SkelLevel* lv, const int
   return skel_last_error();
 }
 
-// CPQR update variant: 1 = thread per column (default), 0 = lane groups
+// CPQR update variant: 0 = lane groups (default), 1 = thread per column,
+// 2 = four threads per column
 // (SKEL_ID_MODE environment override, read once)
 static int skel_id_mode() {
   static int mode = -1;
   if (mode < 0) {
     const char* e = getenv("SKEL_ID_MODE");
-    mode = (e && e[0] >= '0' && e[0] <= '9') ? e[0] - '0' : 1;
+    mode = (e && e[0] >= '0' && e[0] <= '9') ? e[0] - '0' : 0;
   }
   return mode;
 }
