@@ -212,21 +212,23 @@ int skel_dense_inverse(void* A, void* lu, int32_t* ipiv, int32_t K, double regul
 /* ---- multi-RHS solve / apply sweeps (solver.py:279-318, skel.py:206-249) */
 
 /* out[koff[a]+t, :] = sum_j M_a[t, j] u[noff[a]+j, :]   (M_a: k x n row-major
- * at m_off[a]); vectors row-major with R values per row.  max_n bounds n.
+ * at m_off[a]); vectors row-major with R values per row.  max_n / max_k bound
+ * n and k over the processed boxes: order[0..nbox) when order != NULL (a
+ * size bucket), else boxes 0..nbox-1.
  * Up-sweep of solve (solver.py:295-302) / apply (skel.py:225-232). */
 int skel_sweep_up_ex(int32_t nbox, const int32_t* n, const int32_t* k,
                      const int64_t* noff, const int64_t* koff, const int64_t* m_off,
                      const void* M, const void* u, void* out, int32_t R, int32_t field,
-                     int32_t max_n, void* stream);
+                     int32_t max_n, int32_t max_k, const int32_t* order, void* stream);
 
 /* w[noff[a]+i, :] = sum_j A_a[i,j] u[noff[a]+j, :] + sum_t B_a[i,t] v[koff[a]+t, :]
- * (A_a: n x n at a_off[a], B_a: n x k at b_off[a], row-major); max_nk bounds
- * n + k.  Down-sweep of solve (solver.py:304-314) / apply (skel.py:235-244). */
+ * (A_a: n x n at a_off[a], B_a: n x k at b_off[a], row-major); max_n / max_k
+ * bound n and k.  Down-sweep of solve (solver.py:304-314) / apply (skel.py:235-244). */
 int skel_sweep_down_ex(int32_t nbox, const int32_t* n, const int32_t* k,
                        const int64_t* noff, const int64_t* koff, const int64_t* a_off,
                        const void* A, const int64_t* b_off, const void* B,
                        const void* u, const void* v, void* w, int32_t R, int32_t field,
-                       int32_t max_nk, void* stream);
+                       int32_t max_n, int32_t max_k, const int32_t* order, void* stream);
 
 /* y = M x for a dense K x K row-major M, R columns (top-level S^-1 / S). */
 int skel_dense_apply(const void* M, int32_t K, int32_t Kc, const void* x, void* y,

@@ -79,9 +79,9 @@ _SIGS = {
     "skel_factor_level": [_P(SkelFactorLevel), c_i32, c_i32, c_i32, c_vp],
     "skel_dense_inverse": [c_vp, c_vp, c_vp, c_i32, c_f64, c_vp, c_vp, c_i32, c_vp, c_vp],
     "skel_sweep_up_ex": [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32,
-                         c_i32, c_vp],
+                         c_i32, c_i32, c_vp, c_vp],
     "skel_sweep_down_ex": [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                           c_vp, c_i32, c_i32, c_i32, c_vp],
+                           c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp],
     "skel_dense_apply": [c_vp, c_i32, c_i32, c_vp, c_vp, c_i32, c_i32, c_vp],
     "skel_permute_rows": [c_vp, c_i64, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp],
     "skel_compact_i32": [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],

@@ -90,6 +90,26 @@ __device__ __forceinline__ zc shfl(zc v, int src) {
 }
 
 // ---------------------------------------------------------------------------
+// cp.async (LDGSTS): global -> shared without a register round trip, so a
+// thread keeps all of its staging loads in flight at once
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// copy `count` elements of T from global to shared (8-byte words, async)
+template <class T>
+__device__ __forceinline__ void cp_async_block(T* dst, const T* src, int64_t count) {
+  constexpr int W = sizeof(T) / 8;
+  double* d = reinterpret_cast<double*>(dst);
+  const double* s = reinterpret_cast<const double*>(src);
+  for (int64_t e = threadIdx.x; e < count * W; e += blockDim.x) cp_async8(d + e, s + e);
+}
+
+// ---------------------------------------------------------------------------
 // error plumbing
 #define SKEL_TRY(expr)                                   \
   do {                                                   \

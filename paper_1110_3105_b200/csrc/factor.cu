@@ -18,6 +18,14 @@
 #include "common.cuh"
 
 template <class T>
+__device__ __forceinline__ void cp_async_block_one(T* dst, const T* src) {
+  constexpr int W = sizeof(T) / 8;
+#pragma unroll
+  for (int w = 0; w < W; ++w)
+    cp_async8(reinterpret_cast<double*>(dst) + w, reinterpret_cast<const double*>(src) + w);
+}
+
+template <class T>
 struct FacShared {
   int status;
   int piv_row;
@@ -191,7 +199,21 @@ __global__ void __launch_bounds__(256) k_factor_level(const SkelFactorLevel F, i
   T* colk = M + (size_t)k * k;
 
   const T* D = reinterpret_cast<const T*>(F.D) + F.d_off[a];
-  for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) A[e] = D[e];
+  const T* Lg = reinterpret_cast<const T*>(F.L) + F.l_off[a];
+  const T* Rg = reinterpret_cast<const T*>(F.R) + F.r_off[a];
+  if constexpr (!GW) {
+    cp_async_block<T>(A, D, (int64_t)n * n);
+    cp_async_block<T>(Lb, Lg, (int64_t)n * k);
+    cp_async_block<T>(Rb, Rg, (int64_t)n * k);
+    cp_async_commit();
+    cp_async_wait<0>();
+  } else {
+    for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) A[e] = D[e];
+    for (int64_t e = threadIdx.x; e < (int64_t)n * k; e += blockDim.x) {
+      Lb[e] = Lg[e];
+      Rb[e] = Rg[e];
+    }
+  }
   __syncthreads();
   if (F.child_off) {
     // children's Lambda on the diagonal blocks (solver.py:226-233)
@@ -202,21 +224,20 @@ __global__ void __launch_bounds__(256) k_factor_level(const SkelFactorLevel F, i
       const T* lam = reinterpret_cast<const T*>(F.prev_lam) + F.prev_lam_off[c];
       for (int e = threadIdx.x; e < kc * kc; e += blockDim.x) {
         int i = e / kc, j = e - i * kc;
-        A[(int64_t)(ro + i) * n + ro + j] = lam[e];
+        if constexpr (!GW) cp_async_block_one(A + (int64_t)(ro + i) * n + ro + j, lam + e);
+        else A[(int64_t)(ro + i) * n + ro + j] = lam[e];
       }
       ro += kc;
+    }
+    if constexpr (!GW) {
+      cp_async_commit();
+      cp_async_wait<0>();
     }
   }
   __syncthreads();
   if (F.regularize != 0.0) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) A[(int64_t)i * n + i] += T(F.regularize);
     __syncthreads();
-  }
-  const T* Lg = reinterpret_cast<const T*>(F.L) + F.l_off[a];
-  const T* Rg = reinterpret_cast<const T*>(F.R) + F.r_off[a];
-  for (int64_t e = threadIdx.x; e < (int64_t)n * k; e += blockDim.x) {
-    Lb[e] = Lg[e];
-    Rb[e] = Rg[e];
   }
   double nA = sm_norm1<T>(A, n, n, n, sh);
   int bad = sm_invert<T>(A, n, n, colk, ipiv, sh);

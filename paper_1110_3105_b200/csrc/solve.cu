@@ -12,88 +12,298 @@
 // output (row, column) pair.
 #include "common.cuh"
 
-#define SWEEP_CB 32   // RHS columns per CTA chunk
+// Block GEMM of one tree level, per box a and its slice of RHS columns:
+//   O[o_off[a] + i, c] = sum_j A_a[i, j] X[x_off[a] + j, c] (+ sum_t B_a[i, t] Y[y_off[a] + t, c])
+// A_a (p x q) and B_a (p x r) are contiguous row-major blocks streamed from HBM
+// into shared memory ONCE per CTA; the CTA then walks its columns in chunks
+// of CB, staging the X / Y chunk with cp.async (double buffered, the next
+// chunk's copy overlaps this chunk's FMAs); each thread accumulates a TM x TN
+// register tile.  STAGE = false is the fallback for blocks too large for
+// shared memory (3D coarse levels): operands are read through L1 directly.
 
-template <class T>
-__global__ void __launch_bounds__(256) k_sweep_up(const int32_t* __restrict__ nn, const int32_t* __restrict__ kk,
-                                                  const int64_t* __restrict__ noff, const int64_t* __restrict__ koff,
-                                                  const int64_t* __restrict__ m_off, const T* __restrict__ M,
-                                                  const T* __restrict__ u, T* __restrict__ out, int R) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  T* su = reinterpret_cast<T*>(smem);
-  const int a = blockIdx.x;
-  const int n = nn[a], k = kk[a];
-  if (k == 0) return;
-  const int c0 = blockIdx.y * SWEEP_CB;
-  const int cb = min(SWEEP_CB, R - c0);
-  const T* ua = u + noff[a] * R;
-  for (int e = threadIdx.x; e < n * cb; e += blockDim.x) {
-    int j = e / cb, c = e - j * cb;
-    su[e] = ua[(int64_t)j * R + c0 + c];
+template <class T, int CB>
+__device__ __forceinline__ void stage_chunk(T* sX, const T* Xg, int q, int R, int c0, int cb) {
+  constexpr int W = sizeof(T) / 8;   // 8-byte words per element
+  for (int e = threadIdx.x; e < q * CB * W; e += blockDim.x) {
+    const int el = e / W, wd = e - el * W;
+    const int j = el / CB, c = el - j * CB;
+    double* d = reinterpret_cast<double*>(sX + el) + wd;
+    if (c < cb) cp_async8(d, reinterpret_cast<const double*>(Xg + (int64_t)j * R + c0 + c) + wd);
+    else *d = 0.0;
   }
-  __syncthreads();
-  const T* Ma = M + m_off[a];
-  T* oa = out + koff[a] * R;
-  for (int e = threadIdx.x; e < k * cb; e += blockDim.x) {
-    int t = e / cb, c = e - t * cb;
-    const T* mr = Ma + (int64_t)t * n;
-    T acc = T(0.0);
-    for (int j = 0; j < n; ++j) acc += __ldg_T(mr + j) * su[j * cb + c];
-    oa[(int64_t)t * R + c0 + c] = acc;
+}
+
+template <class T, int TM, int TN, int CB, bool STAGE>
+__global__ void __launch_bounds__(128) k_level_gemm(
+    const int32_t* __restrict__ pp, const int32_t* __restrict__ qq, const int32_t* __restrict__ rr,
+    const int64_t* __restrict__ a_off, const T* __restrict__ A,
+    const int64_t* __restrict__ b_off, const T* __restrict__ Bm,
+    const int64_t* __restrict__ x_off, const T* __restrict__ X,
+    const int64_t* __restrict__ y_off, const T* __restrict__ Y,
+    const int64_t* __restrict__ o_off, T* __restrict__ O, int R, int cols_per_cta, int max_q,
+    int max_r, const int32_t* __restrict__ order) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int a = order ? order[blockIdx.x] : blockIdx.x;
+  const int p = pp[a], q = qq[a], r = rr ? rr[a] : 0;
+  if (p == 0) return;
+  const int cbeg = blockIdx.y * cols_per_cta;
+  const int cend = min(R, cbeg + cols_per_cta);
+  if (cbeg >= cend) return;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const T* Ag = A + a_off[a];
+  const T* Bg = r ? Bm + b_off[a] : nullptr;
+  const T* Xg = X + x_off[a] * R;
+  const T* Yg = r ? Y + y_off[a] * R : nullptr;
+  T* Og = O + o_off[a] * R;
+  T* sA = reinterpret_cast<T*>(smem);
+  T* sB = sA + (STAGE ? (size_t)p * q : 0);
+  T* const sXY0 = sB + (STAGE ? (size_t)p * r : 0);
+  const size_t sxy_stride = (size_t)(max_q + max_r) * CB;
+  if (STAGE) {
+    // every operand byte goes global -> shared with cp.async: all loads in
+    // flight at once instead of one load-to-store round trip per element
+    constexpr int W = sizeof(T) / 8;
+    for (int e = tid; e < p * q * W; e += nt)
+      cp_async8(reinterpret_cast<double*>(sA) + e, reinterpret_cast<const double*>(Ag) + e);
+    for (int e = tid; e < p * r * W; e += nt)
+      cp_async8(reinterpret_cast<double*>(sB) + e, reinterpret_cast<const double*>(Bg) + e);
+    stage_chunk<T, CB>(sXY0, Xg, q, R, cbeg, min(CB, cend - cbeg));
+    if (r) stage_chunk<T, CB>(sXY0 + (size_t)q * CB, Yg, r, R, cbeg, min(CB, cend - cbeg));
+    cp_async_commit();
+  }
+  constexpr int NCT = CB / TN;
+  const int nrt = (p + TM - 1) / TM;
+  int buf = 0;
+  for (int c0 = cbeg; c0 < cend; c0 += CB, buf ^= 1) {
+    const int cb = min(CB, cend - c0);
+    const T* sX = sXY0 + buf * sxy_stride;
+    const T* sY = sX + (size_t)q * CB;
+    if (STAGE) {
+      const int c1 = c0 + CB;
+      if (c1 < cend) {
+        T* nb = sXY0 + (buf ^ 1) * sxy_stride;
+        stage_chunk<T, CB>(nb, Xg, q, R, c1, min(CB, cend - c1));
+        if (r) stage_chunk<T, CB>(nb + (size_t)q * CB, Yg, r, R, c1, min(CB, cend - c1));
+      }
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncthreads();
+    }
+    for (int t = tid; t < nrt * NCT; t += nt) {
+      const int rt = t / NCT, ct = t - rt * NCT;
+      const int i0 = rt * TM, j0 = ct * TN;
+      T acc[TM][TN];
+#pragma unroll
+      for (int u = 0; u < TM; ++u)
+#pragma unroll
+        for (int v = 0; v < TN; ++v) acc[u][v] = T(0.0);
+      for (int j = 0; j < q; ++j) {
+        T av[TM], xv[TN];
+#pragma unroll
+        for (int u = 0; u < TM; ++u)
+          av[u] = (i0 + u < p) ? (STAGE ? sA[(i0 + u) * q + j] : __ldg_T(Ag + (int64_t)(i0 + u) * q + j)) : T(0.0);
+#pragma unroll
+        for (int v = 0; v < TN; ++v)
+          xv[v] = STAGE ? sX[j * CB + j0 + v]
+                        : ((j0 + v < cb) ? __ldg_T(Xg + (int64_t)j * R + c0 + j0 + v) : T(0.0));
+#pragma unroll
+        for (int u = 0; u < TM; ++u)
+#pragma unroll
+          for (int v = 0; v < TN; ++v) acc[u][v] += av[u] * xv[v];
+      }
+      for (int j = 0; j < r; ++j) {
+        T av[TM], xv[TN];
+#pragma unroll
+        for (int u = 0; u < TM; ++u)
+          av[u] = (i0 + u < p) ? (STAGE ? sB[(i0 + u) * r + j] : __ldg_T(Bg + (int64_t)(i0 + u) * r + j)) : T(0.0);
+#pragma unroll
+        for (int v = 0; v < TN; ++v)
+          xv[v] = STAGE ? sY[j * CB + j0 + v]
+                        : ((j0 + v < cb) ? __ldg_T(Yg + (int64_t)j * R + c0 + j0 + v) : T(0.0));
+#pragma unroll
+        for (int u = 0; u < TM; ++u)
+#pragma unroll
+          for (int v = 0; v < TN; ++v) acc[u][v] += av[u] * xv[v];
+      }
+#pragma unroll
+      for (int u = 0; u < TM; ++u)
+#pragma unroll
+        for (int v = 0; v < TN; ++v)
+          if (i0 + u < p && j0 + v < cb) Og[(int64_t)(i0 + u) * R + c0 + j0 + v] = acc[u][v];
+    }
+    if (STAGE) __syncthreads();   // buffer `buf` is refilled two chunks later
+  }
+}
+
+// DMMA (mma.sync.m8n8k4.f64) variant for many RHS: [A | B] (p x (q+r)) and
+// [X; Y] ((q+r) x CB) are treated as one GEMM; each warp owns 8-row x 32-col
+// output tiles (4 accumulators of 8x8), one A fragment and four B fragments
+// per k-step of 4.  X/Y chunks are double buffered with cp.async; the chunk
+// row stride is CB+8 doubles so a B-fragment load hits every bank pair once.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int CB>
+__global__ void __launch_bounds__(128) k_level_dmma(
+    const int32_t* __restrict__ pp, const int32_t* __restrict__ qq, const int32_t* __restrict__ rr,
+    const int64_t* __restrict__ a_off, const double* __restrict__ A,
+    const int64_t* __restrict__ b_off, const double* __restrict__ Bm,
+    const int64_t* __restrict__ x_off, const double* __restrict__ X,
+    const int64_t* __restrict__ y_off, const double* __restrict__ Y,
+    const int64_t* __restrict__ o_off, double* __restrict__ O, int R, int cols_per_cta, int max_p,
+    int max_k, const int32_t* __restrict__ order) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int LDX = CB + 8;
+  const int a = order ? order[blockIdx.x] : blockIdx.x;
+  const int p = pp[a], q = qq[a], r = rr ? rr[a] : 0;
+  if (p == 0) return;
+  const int cbeg = blockIdx.y * cols_per_cta;
+  const int cend = min(R, cbeg + cols_per_cta);
+  if (cbeg >= cend) return;
+  const int K = q + r, Kp = (K + 3) & ~3, P8 = (p + 7) & ~7;
+  const int ldA = Kp + 1;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  double* sA = reinterpret_cast<double*>(smem);
+  double* sX0 = sA + (((size_t)max_p + 7) & ~(size_t)7) * (max_k + 1);
+  const size_t xstride = (size_t)max_k * LDX;
+  const double* Ag = A + a_off[a];
+  const double* Bg = r ? Bm + b_off[a] : nullptr;
+  const double* Xg = X + x_off[a] * R;
+  const double* Yg = r ? Y + y_off[a] * R : nullptr;
+  double* Og = O + o_off[a] * R;
+  for (int e = tid; e < P8 * Kp; e += nt) {
+    const int i = e / Kp, j = e - i * Kp;
+    double* d = sA + i * ldA + j;
+    if (i < p && j < K) cp_async8(d, j < q ? Ag + (int64_t)i * q + j : Bg + (int64_t)i * r + (j - q));
+    else *d = 0.0;
+  }
+  auto stage = [&](double* dst, int c0) {
+    const int cb = min(CB, cend - c0);
+    for (int e = tid; e < Kp * CB; e += nt) {
+      const int j = e / CB, c = e - j * CB;
+      double* d = dst + j * LDX + c;
+      if (j < K && c < cb) cp_async8(d, j < q ? Xg + (int64_t)j * R + c0 + c : Yg + (int64_t)(j - q) * R + c0 + c);
+      else *d = 0.0;
+    }
+  };
+  stage(sX0, cbeg);
+  cp_async_commit();
+  const int g = lane >> 2, t4 = lane & 3;
+  const int ntask = (P8 / 8) * (CB / 32);
+  int buf = 0;
+  for (int c0 = cbeg; c0 < cend; c0 += CB, buf ^= 1) {
+    const int cb = min(CB, cend - c0);
+    const double* sX = sX0 + buf * xstride;
+    if (c0 + CB < cend) stage(sX0 + (buf ^ 1) * xstride, c0 + CB);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    for (int task = warp; task < ntask; task += nt >> 5) {
+      const int rt = task / (CB / 32), cg = task - rt * (CB / 32);
+      double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      const double* arow = sA + (rt * 8 + g) * ldA + t4;
+      const double* xcol = sX + t4 * LDX + cg * 32 + g;
+      for (int k0 = 0; k0 < Kp; k0 += 4) {
+        const double av = arow[k0];
+        const double* xk = xcol + k0 * LDX;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma884(acc[u][0], acc[u][1], av, xk[u * 8]);
+      }
+      const int row = rt * 8 + g;
+      if (row < p) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int col = cg * 32 + u * 8 + 2 * t4;
+          if (col < cb) Og[(int64_t)row * R + c0 + col] = acc[u][0];
+          if (col + 1 < cb) Og[(int64_t)row * R + c0 + col + 1] = acc[u][1];
+        }
+      }
+    }
+    __syncthreads();
   }
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k_sweep_down(const int32_t* __restrict__ nn, const int32_t* __restrict__ kk,
-                                                    const int64_t* __restrict__ noff, const int64_t* __restrict__ koff,
-                                                    const int64_t* __restrict__ a_off, const T* __restrict__ A,
-                                                    const int64_t* __restrict__ b_off, const T* __restrict__ B,
-                                                    const T* __restrict__ u, const T* __restrict__ v,
-                                                    T* __restrict__ w, int R) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int a = blockIdx.x;
-  const int n = nn[a], k = kk[a];
-  if (n == 0) return;
-  const int c0 = blockIdx.y * SWEEP_CB;
-  const int cb = min(SWEEP_CB, R - c0);
-  T* su = reinterpret_cast<T*>(smem);
-  T* sv = su + (size_t)n * cb;
-  const T* ua = u + noff[a] * R;
-  const T* va = v + koff[a] * R;
-  for (int e = threadIdx.x; e < n * cb; e += blockDim.x) {
-    int j = e / cb, c = e - j * cb;
-    su[e] = ua[(int64_t)j * R + c0 + c];
+static int level_gemm(int nbox, const int32_t* p, const int32_t* q, const int32_t* r,
+                      const int64_t* a_off, const void* A, const int64_t* b_off, const void* B,
+                      const int64_t* x_off, const void* X, const int64_t* y_off, const void* Y,
+                      const int64_t* o_off, void* O, int R, int max_p, int max_q, int max_r,
+                      const int32_t* order, cudaStream_t st) {
+  // nbox = number of CTAs' boxes: order[0..nbox) when order != NULL
+  if (nbox <= 0 || R <= 0) return 0;
+  const size_t optin = (size_t)skel_smem_optin();
+  auto go = [&](auto kern_s, auto kern_g, int CB) -> int {
+    // columns per CTA: enough chunks to amortise staging A, enough CTAs to fill the GPU
+    int chunks = (R + CB - 1) / CB;
+    int per = 1;
+    while (per < chunks && (long long)nbox * ((chunks + per * 2 - 1) / (per * 2)) >= 4LL * 148 * 4) per *= 2;
+    const int cols = per * CB;
+    dim3 grid(nbox, (R + cols - 1) / cols);
+    size_t smem = ((size_t)max_p * max_q + (size_t)max_p * max_r +
+                   2 * (size_t)(max_q + max_r) * CB) * sizeof(T);
+    if (smem <= optin) {
+      SKEL_TRY(cudaFuncSetAttribute(kern_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern_s<<<grid, 128, smem, st>>>(p, q, r, a_off, (const T*)A, b_off, (const T*)B, x_off,
+                                      (const T*)X, y_off, (const T*)Y, o_off, (T*)O, R, cols, max_q,
+                                      max_r, order);
+    } else {
+      kern_g<<<grid, 128, 0, st>>>(p, q, r, a_off, (const T*)A, b_off, (const T*)B, x_off,
+                                   (const T*)X, y_off, (const T*)Y, o_off, (T*)O, R, cols, max_q,
+                                   max_r, order);
+    }
+    return skel_last_error();
+  };
+  if constexpr (sizeof(T) == sizeof(double)) {
+    if (R >= 64) {
+      constexpr int CB = 32;
+      const int maxk = max_q + max_r;
+      size_t smem = ((((size_t)max_p + 7) & ~(size_t)7) * (maxk + 1 + 4) +
+                     2 * (size_t)(maxk + 4) * (CB + 8)) * sizeof(double);
+      if (smem <= optin) {
+        int chunks = (R + CB - 1) / CB;
+        int per = 1;
+        while (per < chunks && (long long)nbox * ((chunks + per * 2 - 1) / (per * 2)) >= 4LL * 148 * 4) per *= 2;
+        const int cols = per * CB;
+        dim3 grid(nbox, (R + cols - 1) / cols);
+        SKEL_TRY(cudaFuncSetAttribute(k_level_dmma<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_level_dmma<CB><<<grid, 128, smem, st>>>(p, q, r, a_off, (const double*)A, b_off,
+                                                  (const double*)B, x_off, (const double*)X, y_off,
+                                                  (const double*)Y, o_off, (double*)O, R, cols, max_p,
+                                                  maxk + 4, order);
+        return skel_last_error();
+      }
+    }
   }
-  for (int e = threadIdx.x; e < k * cb; e += blockDim.x) {
-    int j = e / cb, c = e - j * cb;
-    sv[e] = va[(int64_t)j * R + c0 + c];
-  }
-  __syncthreads();
-  const T* Aa = A + a_off[a];
-  const T* Ba = B + b_off[a];
-  T* wa = w + noff[a] * R;
-  for (int e = threadIdx.x; e < n * cb; e += blockDim.x) {
-    int i = e / cb, c = e - i * cb;
-    const T* ar = Aa + (int64_t)i * n;
-    T acc = T(0.0);
-    for (int j = 0; j < n; ++j) acc += __ldg_T(ar + j) * su[j * cb + c];
-    const T* br = Ba + (int64_t)i * k;
-    T acc2 = T(0.0);
-    for (int t = 0; t < k; ++t) acc2 += __ldg_T(br + t) * sv[t * cb + c];
-    wa[(int64_t)i * R + c0 + c] = (k > 0) ? acc + acc2 : acc;
-  }
+  if (R <= 8) return go(k_level_gemm<T, 4, 1, 8, true>, k_level_gemm<T, 4, 1, 8, false>, 8);
+  if (R <= 16) return go(k_level_gemm<T, 4, 1, 16, true>, k_level_gemm<T, 4, 1, 16, false>, 16);
+  if (R <= 32) return go(k_level_gemm<T, 4, 1, 32, true>, k_level_gemm<T, 4, 1, 32, false>, 32);
+  return go(k_level_gemm<T, 4, 4, 64, true>, k_level_gemm<T, 4, 4, 64, false>, 64);
 }
 
+// y (K x R) = M (K x Kc) x (Kc x R): one warp per output row, lanes over
+// columns; the row of M is read once per warp (broadcast), four partial sums
 template <class T>
-__global__ void k_dense_apply(const T* __restrict__ M, int K, int Kc, const T* __restrict__ x,
-                              T* __restrict__ y, int R) {
-  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)K * R) return;
-  int i = (int)(e / R), c = (int)(e - (int64_t)i * R);
+__global__ void __launch_bounds__(256) k_dense_apply(const T* __restrict__ M, int K, int Kc,
+                                                     const T* __restrict__ x, T* __restrict__ y, int R) {
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= K) return;
+  const int lane = threadIdx.x & 31;
   const T* mr = M + (int64_t)i * Kc;
-  T acc = T(0.0);
-  for (int j = 0; j < Kc; ++j) acc += mr[j] * x[(int64_t)j * R + c];
-  y[e] = acc;
+  for (int c = blockIdx.y * 32 + lane; c < R && c < (int)(blockIdx.y + 1) * 32; c += 32) {
+    T a0 = T(0.0), a1 = T(0.0), a2 = T(0.0), a3 = T(0.0);
+    int j = 0;
+    for (; j + 3 < Kc; j += 4) {
+      a0 += __ldg_T(mr + j) * x[(int64_t)j * R + c];
+      a1 += __ldg_T(mr + j + 1) * x[(int64_t)(j + 1) * R + c];
+      a2 += __ldg_T(mr + j + 2) * x[(int64_t)(j + 2) * R + c];
+      a3 += __ldg_T(mr + j + 3) * x[(int64_t)(j + 3) * R + c];
+    }
+    for (; j < Kc; ++j) a0 += __ldg_T(mr + j) * x[(int64_t)j * R + c];
+    y[(int64_t)i * R + c] = (a0 + a1) + (a2 + a3);
+  }
 }
 
 // one row per thread group of R lanes (R <= 32) or one thread per row chunk
@@ -120,62 +330,42 @@ __global__ void k_compact(int nseg, const int64_t* src_off, const int32_t* len, 
   for (int t = lane; t < L; t += 32) d[t] = s[t];
 }
 
-template <class T>
-static int sweep_up_impl(int nbox, const int32_t* n, const int32_t* k, const int64_t* noff,
-                         const int64_t* koff, const int64_t* m_off, const void* M, const void* u,
-                         void* out, int R, int max_n, cudaStream_t st) {
-  if (nbox <= 0 || R <= 0) return 0;
-  dim3 grid(nbox, (R + SWEEP_CB - 1) / SWEEP_CB);
-  size_t smem = (size_t)max_n * SWEEP_CB * sizeof(T);
-  auto kern = k_sweep_up<T>;
-  SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<grid, 128, smem, st>>>(n, k, noff, koff, m_off, (const T*)M, (const T*)u, (T*)out, R);
-  return skel_last_error();
-}
-
-template <class T>
-static int sweep_down_impl(int nbox, const int32_t* n, const int32_t* k, const int64_t* noff,
-                           const int64_t* koff, const int64_t* a_off, const void* A,
-                           const int64_t* b_off, const void* B, const void* u, const void* v,
-                           void* w, int R, int max_nk, cudaStream_t st) {
-  if (nbox <= 0 || R <= 0) return 0;
-  dim3 grid(nbox, (R + SWEEP_CB - 1) / SWEEP_CB);
-  size_t smem = (size_t)max_nk * SWEEP_CB * sizeof(T);
-  auto kern = k_sweep_down<T>;
-  SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<grid, 128, smem, st>>>(n, k, noff, koff, a_off, (const T*)A, b_off, (const T*)B, (const T*)u,
-                                (const T*)v, (T*)w, R);
-  return skel_last_error();
-}
-
 extern "C" {
 
 int skel_sweep_up_ex(int32_t nbox, const int32_t* n, const int32_t* k, const int64_t* noff,
                      const int64_t* koff, const int64_t* m_off, const void* M, const void* u,
-                     void* out, int32_t R, int32_t field, int32_t max_n, void* stream) {
+                     void* out, int32_t R, int32_t field, int32_t max_n, int32_t max_k,
+                     const int32_t* order, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (field == 0) return sweep_up_impl<double>(nbox, n, k, noff, koff, m_off, M, u, out, R, max_n, st);
-  return sweep_up_impl<zc>(nbox, n, k, noff, koff, m_off, M, u, out, R, max_n, st);
+  // out (k x R) = M (k x n) u (n x R)
+  if (field == 0)
+    return level_gemm<double>(nbox, k, n, nullptr, m_off, M, nullptr, nullptr, noff, u, nullptr,
+                              nullptr, koff, out, R, max_k, max_n, 0, order, st);
+  return level_gemm<zc>(nbox, k, n, nullptr, m_off, M, nullptr, nullptr, noff, u, nullptr, nullptr,
+                        koff, out, R, max_k, max_n, 0, order, st);
 }
 
 int skel_sweep_down_ex(int32_t nbox, const int32_t* n, const int32_t* k, const int64_t* noff,
                        const int64_t* koff, const int64_t* a_off, const void* A,
                        const int64_t* b_off, const void* B, const void* u, const void* v, void* w,
-                       int32_t R, int32_t field, int32_t max_nk, void* stream) {
+                       int32_t R, int32_t field, int32_t max_n, int32_t max_k,
+                       const int32_t* order, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  // w (n x R) = A (n x n) u (n x R) + B (n x k) v (k x R)
   if (field == 0)
-    return sweep_down_impl<double>(nbox, n, k, noff, koff, a_off, A, b_off, B, u, v, w, R, max_nk, st);
-  return sweep_down_impl<zc>(nbox, n, k, noff, koff, a_off, A, b_off, B, u, v, w, R, max_nk, st);
+    return level_gemm<double>(nbox, n, n, k, a_off, A, b_off, B, noff, u, koff, v, noff, w, R, max_n,
+                              max_n, max_k, order, st);
+  return level_gemm<zc>(nbox, n, n, k, a_off, A, b_off, B, noff, u, koff, v, noff, w, R, max_n, max_n,
+                        max_k, order, st);
 }
 
 int skel_dense_apply(const void* M, int32_t K, int32_t Kc, const void* x, void* y, int32_t R,
                      int32_t field, void* stream) {
-  int64_t tot = (int64_t)K * R;
-  if (tot == 0) return 0;
-  int blocks = (int)((tot + 255) / 256);
+  if ((int64_t)K * R == 0) return 0;
+  dim3 grid((K + 7) / 8, (R + 31) / 32);
   cudaStream_t st = (cudaStream_t)stream;
-  if (field == 0) k_dense_apply<double><<<blocks, 256, 0, st>>>((const double*)M, K, Kc, (const double*)x, (double*)y, R);
-  else k_dense_apply<zc><<<blocks, 256, 0, st>>>((const zc*)M, K, Kc, (const zc*)x, (zc*)y, R);
+  if (field == 0) k_dense_apply<double><<<grid, 256, 0, st>>>((const double*)M, K, Kc, (const double*)x, (double*)y, R);
+  else k_dense_apply<zc><<<grid, 256, 0, st>>>((const zc*)M, K, Kc, (const zc*)x, (zc*)y, R);
   return skel_last_error();
 }
 

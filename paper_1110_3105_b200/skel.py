@@ -681,7 +681,8 @@ def apply(cm: CompressedMatrix, x) -> np.ndarray:
             nxt = torch.empty((int(dl.kc.sum()), Rn), dtype=X.dtype, device="cuda")
             _native.check(L.skel_sweep_up_ex(dl.p, p_(dl.t_nr), p_(dl.t_kc), p_(dl.t_cdof_off),
                                              p_(dl.t_kc_off), p_(dl.t_r_off), p_(dl.R), p_(u),
-                                             p_(nxt), Rn, field, int(max(dl.nc.max(), 1)), st),
+                                             p_(nxt), Rn, field, int(max(dl.nc.max(), 1)),
+                                             int(dl.kc.max(initial=0)), None, st),
                           "sweep_up")
             us.append(nxt)
             u = nxt
@@ -692,7 +693,8 @@ def apply(cm: CompressedMatrix, x) -> np.ndarray:
             _native.check(L.skel_sweep_down_ex(dl.p, p_(dl.t_nr), p_(dl.t_kr), p_(dl.t_rdof_off),
                                                p_(dl.t_kr_off), p_(dl.t_d_off), p_(dl.D),
                                                p_(dl.t_l_off), p_(dl.L), p_(us[li]), p_(v), p_(w),
-                                               Rn, field, int(max((dl.nr + dl.kr).max(), 1)), st),
+                                               Rn, field, int(max(dl.nr.max(), 1)),
+                                               int(dl.kr.max(initial=0)), None, st),
                           "sweep_down")
             v = w
         yt = v

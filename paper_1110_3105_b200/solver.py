@@ -47,6 +47,24 @@ class DevFactorLevel:
         self._buf = t["_buffer"]
         self.max_n = int(max(n.max(initial=0), 1))
         self.max_nk = int(max((n + k).max(initial=0), 1))
+        self.max_k = int(k.max(initial=0))
+        # solve-sweep size buckets: (device order, count, max_n, max_k)
+        self.solve_buckets = [(t[f"sv{bi}"], int(sel.size), int(n[sel].max()), int(k[sel].max()))
+                              for bi, sel in enumerate(_solve_buckets(n))]
+
+
+_SOLVE_CLASSES = (24, 40, 56, 72, 96, 128)
+
+
+def _solve_buckets(n):
+    """Boxes grouped by size so each sweep launch sizes its shared memory for
+    its own boxes (more CTAs per SM for the many small ones)."""
+    cls = np.searchsorted(np.asarray(_SOLVE_CLASSES), n, side="left")
+    out = []
+    for c in np.unique(cls[n > 0]):
+        sel = np.nonzero((cls == c) & (n > 0))[0]
+        out.append(sel[np.argsort(-n[sel], kind="stable")].astype(np.int32))
+    return out
 
 
 class FactoredLevel:
@@ -184,6 +202,8 @@ class FactorRun:
             pk.add("dd_off", dd_off).add("ld_off", ld_off).add("lam_off", lam_off)
             for bi, sel in enumerate(buckets):
                 pk.add(f"order{bi}", sel)
+            for bi, sel in enumerate(_solve_buckets(n)):
+                pk.add(f"sv{bi}", sel)
             t = pk.upload()
             Dd = torch.empty(max(int(dd_off[-1]), 1), dtype=tdt, device=dev)
             Ld = torch.empty(max(int(ld_off[-1]), 1), dtype=tdt, device=dev)
@@ -351,6 +371,33 @@ def solve(fi: FactoredInverse, b):
     return x[:, 0] if single else x
 
 
+def _sweep_launch(L, d, direction, u, v, out, Rn, field):
+    """One level of the up- or down-sweep: size buckets on side streams."""
+    torch = _native.require_cuda()
+    p_ = _native.ptr
+    bks = d.solve_buckets
+    if not bks:
+        return
+    streams = fork(len(bks), tag="solve") if len(bks) > 1 else None
+    for bi, (order, cnt, mn, mk) in enumerate(bks):
+        ctx = torch.cuda.stream(streams[bi]) if streams else _nullctx()
+        with ctx:
+            st = _native.stream_ptr()
+            if direction == "up":
+                if mk == 0:
+                    continue
+                _native.check(L.skel_sweep_up_ex(cnt, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
+                                                 p_(d.t_ld_off), p_(d.Rd), p_(u), p_(out), Rn, field,
+                                                 mn, mk, p_(order), st), "sweep_up")
+            else:
+                _native.check(L.skel_sweep_down_ex(cnt, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
+                                                   p_(d.t_dd_off), p_(d.Dd), p_(d.t_ld_off), p_(d.Ld),
+                                                   p_(u), p_(v), p_(out), Rn, field, mn, mk, p_(order),
+                                                   st), "sweep_down")
+    if streams:
+        join(streams)
+
+
 def _sweep_work(rec, d, Rn, field, up):
     """Algorithmic flops / bytes of one sweep launch: factor
     blocks read once, vectors read and written once."""
@@ -365,7 +412,40 @@ def _sweep_work(rec, d, Rn, field, up):
         rec.nbytes = it * float((n * n + n * k).sum() + Rn * (2 * n.sum() + k.sum()))
 
 
-def solve_device(fi: FactoredInverse, B):
+_GRAPH_CACHE = 4
+
+
+def solve_device(fi: FactoredInverse, B, graph: bool = True):
+    """Device-resident solve of an (N, R) CUDA tensor (original ordering).
+
+    The ~30-40 launches of one solve (gather, per-level size-bucketed sweeps
+    on side streams, top GEMM, scatter) are captured once per (R, dtype) into
+    a CUDA graph and replayed; B is copied into the graph's static input and
+    the result copied out."""
+    torch = _native.require_cuda()
+    if not graph or _profile.enabled or torch.cuda.is_current_stream_capturing():
+        return _solve_device_eager(fi, B)
+    key = (int(B.shape[1]), B.dtype)
+    cache = fi.__dict__.setdefault("_graphs", {})
+    ent = cache.get(key)
+    if ent is None:
+        static_B = torch.empty_like(B)
+        static_B.copy_(B)
+        _solve_device_eager(fi, static_B)          # warm-up: kernel attributes, allocator
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            static_X = _solve_device_eager(fi, static_B)
+        if len(cache) >= _GRAPH_CACHE:
+            cache.pop(next(iter(cache)))
+        ent = cache[key] = (g, static_B, static_X)
+    g, static_B, static_X = ent
+    static_B.copy_(B)
+    g.replay()
+    return static_X.clone()
+
+
+def _solve_device_eager(fi: FactoredInverse, B):
     """Device-resident solve of an (N, R) CUDA tensor (original ordering)."""
     torch = _native.require_cuda()
     L = _native.lib()
@@ -385,9 +465,7 @@ def solve_device(fi: FactoredInverse, B):
             d = lv.dev
             nxt = torch.empty((int(d.k.sum()), Rn), dtype=B.dtype, device="cuda")
             with _profile.timed("sweep", dir="up") as rec:
-                _native.check(L.skel_sweep_up_ex(d.p, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
-                                                 p_(d.t_ld_off), p_(d.Rd), p_(u), p_(nxt), Rn, field,
-                                                 d.max_n, st), "sweep_up")
+                _sweep_launch(L, d, "up", u, None, nxt, Rn, field)
             if rec is not None:
                 _sweep_work(rec, d, Rn, field, up=True)
             us.append(nxt)
@@ -397,10 +475,7 @@ def solve_device(fi: FactoredInverse, B):
             d = fi.levels[li].dev
             w = torch.empty((int(d.n.sum()), Rn), dtype=B.dtype, device="cuda")
             with _profile.timed("sweep", dir="down") as rec:
-                _native.check(L.skel_sweep_down_ex(d.p, p_(d.t_n), p_(d.t_k), p_(d.t_noff),
-                                                   p_(d.t_koff), p_(d.t_dd_off), p_(d.Dd),
-                                                   p_(d.t_ld_off), p_(d.Ld), p_(us[li]), p_(v), p_(w),
-                                                   Rn, field, d.max_nk, st), "sweep_down")
+                _sweep_launch(L, d, "down", us[li], v, w, Rn, field)
             if rec is not None:
                 _sweep_work(rec, d, Rn, field, up=False)
             v = w
