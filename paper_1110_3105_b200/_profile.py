@@ -45,3 +45,29 @@ def summary(kind):
     """(launches, total ms, total flops, total bytes) over records of kind."""
     rs = [r for r in records if r.kind == kind]
     return (len(rs), sum(r.ms() for r in rs), sum(r.flops for r in rs), sum(r.nbytes for r in rs))
+
+
+def union_ms(kind, group="level"):
+    """Device time covered by the union of the records' [start, end] intervals,
+    per value of meta[group] (concurrent launches on side streams overlap)."""
+    rs = [r for r in records if r.kind == kind]
+    if not rs:
+        return 0.0
+    ref = rs[0].start
+    groups = {}
+    for r in rs:
+        a = ref.elapsed_time(r.start)
+        b = ref.elapsed_time(r.end)
+        groups.setdefault(r.meta.get(group), []).append((a, b))
+    tot = 0.0
+    for iv in groups.values():
+        iv.sort()
+        cs, ce = iv[0]
+        for a, b in iv[1:]:
+            if a > ce:
+                tot += ce - cs
+                cs, ce = a, b
+            else:
+                ce = max(ce, b)
+        tot += ce - cs
+    return tot

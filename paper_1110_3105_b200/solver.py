@@ -427,7 +427,13 @@ def solve_device(fi: FactoredInverse, B, graph: bool = True):
         return _solve_device_eager(fi, B)
     key = (int(B.shape[1]), B.dtype)
     cache = fi.__dict__.setdefault("_graphs", {})
+    seen = fi.__dict__.setdefault("_graph_seen", set())
     ent = cache.get(key)
+    if ent is None and key not in seen:
+        # first solve with this shape runs eagerly; a repeat (the multi-RHS
+        # reuse pattern) pays the one-time capture and replays from then on
+        seen.add(key)
+        return _solve_device_eager(fi, B)
     if ent is None:
         static_B = torch.empty_like(B)
         static_B.copy_(B)
