@@ -258,89 +258,6 @@ __device__ void cpqr_update(T* W, int m, int n, int ld, double* nrm, double* ref
   if (lane == 0) { sh.cand_v[warp] = bv; sh.cand_i[warp] = bi; }
 }
 
-// Phase B, thread-per-column variant: TPC threads (1, 2 or 4; adjacent
-// lanes) own one trailing column and split its rows (i = s+1+sub+TPC*t).
-// Reflector entries are shared-memory broadcasts, the v^H w dot product and
-// the trailing norm are thread-local sums finished with log2(TPC) shuffles,
-// and the row loops are unrolled by 8 with all loads issued first so each
-// thread keeps 16 shared-memory loads in flight.
-template <class T, int TPC>
-__device__ void cpqr_update_lpc(T* W, int m, int n, int ld, double* nrm, double* ref,
-                                double* xn2, const int* piv, CpqrShared<T>& sh, int s, int kmax) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int sub = threadIdx.x & (TPC - 1);
-  const int cpass = blockDim.x / TPC;
-  const T v0 = sh.v0;
-  const double beta = sh.beta;
-  const int s1 = s + 1;
-  const bool renorm = (s1 < kmax) && (s1 % 32 == 0);
-  const T* vcol = W + (int64_t)sh.pc * ld;
-  double bv = -1.0;
-  int bi = 0x7fffffff;
-  constexpr int U = 8;
-  constexpr int STEP = U * TPC;
-  for (int cb = s1; cb < n; cb += cpass) {
-    const int c = cb + (int)(threadIdx.x / TPC);
-    const bool act = c < n;
-    T* w = W + (int64_t)piv[act ? c : s1] * ld;
-    T dsum[4] = {T(0.0), T(0.0), T(0.0), T(0.0)};
-    if (sub == 0) dsum[0] = sk_conj(v0) * w[s];
-    int i = s1 + sub;
-    for (; i + (U - 1) * TPC < m; i += STEP) {
-      T vv[U], ww[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) { vv[u] = vcol[i + u * TPC]; ww[u] = w[i + u * TPC]; }
-#pragma unroll
-      for (int u = 0; u < U; ++u) dsum[u & 3] += sk_conj(vv[u]) * ww[u];
-    }
-    for (; i < m; i += TPC) dsum[0] += sk_conj(vcol[i]) * w[i];
-    T dot = (dsum[0] + dsum[1]) + (dsum[2] + dsum[3]);
-#pragma unroll
-    for (int o = TPC / 2; o > 0; o >>= 1) dot += shfl_xor_T(dot, o);
-    const T f = dot * beta;
-    const T row = w[s] - v0 * f;
-    double xs[4] = {0.0, 0.0, 0.0, 0.0};
-    i = s1 + sub;
-    if (beta != 0.0) {
-      for (; i + (U - 1) * TPC < m; i += STEP) {
-        T vv[U], ww[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) { vv[u] = vcol[i + u * TPC]; ww[u] = w[i + u * TPC]; }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          ww[u] -= vv[u] * f;
-          xs[u & 3] += sk_abs2(ww[u]);
-        }
-        if (act) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) w[i + u * TPC] = ww[u];
-        }
-      }
-      for (; i < m; i += TPC) {
-        T a = w[i] - vcol[i] * f;
-        if (act) w[i] = a;
-        xs[0] += sk_abs2(a);
-      }
-    } else {
-      for (; i < m; i += TPC) xs[0] += sk_abs2(w[i]);
-    }
-    double xa = (xs[0] + xs[1]) + (xs[2] + xs[3]);
-#pragma unroll
-    for (int o = TPC / 2; o > 0; o >>= 1) xa += __shfl_xor_sync(0xffffffffu, xa, o);
-    if (sub == 0 && act) {
-      if (beta != 0.0) w[s] = row;
-      double t = nrm[c] - sk_abs2(beta != 0.0 ? row : w[s]);
-      t = t > 0.0 ? t : 0.0;
-      if (renorm || t < 1e-8 * ref[c]) { t = xa; ref[c] = xa; }
-      nrm[c] = t;
-      xn2[c] = xa;
-      cand_merge(bv, bi, t, c);
-    }
-  }
-  warp_cand(bv, bi);
-  if (lane == 0) { sh.cand_v[warp] = bv; sh.cand_i[warp] = bi; }
-}
-
 // Run CPQR steps from sh.rank until the stop rule (with min_rank) fires.
 template <class T, int GL, int RPL>
 __device__ void cpqr_run(T* W, int m, int n, int ld, double* nrm, double* ref, double* xn2,
@@ -350,12 +267,10 @@ __device__ void cpqr_run(T* W, int m, int n, int ld, double* nrm, double* ref, d
   int s = sh.rank;
   while (s < kmax) {
     if (threadIdx.x < 32)
-      cpqr_pivot<T>(W, m, n, ld, nrm, (RPL < 0 || RPL == 0) ? xn2 : nullptr, piv, sh, s, eps,
-                    min_rank, nw);
+      cpqr_pivot<T>(W, m, n, ld, nrm, RPL == 0 ? xn2 : nullptr, piv, sh, s, eps, min_rank, nw);
     __syncthreads();
     if (sh.stop) break;
-    if constexpr (RPL < 0) cpqr_update_lpc<T, GL>(W, m, n, ld, nrm, ref, xn2, piv, sh, s, kmax);
-    else cpqr_update<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, s, kmax);
+    cpqr_update<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, s, kmax);
     if (threadIdx.x == 0) {
       W[(int64_t)sh.pc * ld + s] = sh.alpha;
       sh.rank = s + 1;

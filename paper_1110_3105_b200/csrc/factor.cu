@@ -176,8 +176,8 @@ static __host__ __device__ inline size_t fac_elems(int n, int k) {
   return (size_t)n * n + 4 * (size_t)n * k + (size_t)k * k + 3 * (size_t)n;
 }
 
-template <class T, bool GW>
-__global__ void __launch_bounds__(256) k_factor_level(const SkelFactorLevel F, int max_n, int max_k) {
+template <class T, bool GW, int NT>
+__global__ void __launch_bounds__(NT) k_factor_level(const SkelFactorLevel F, int max_n, int max_k) {
   extern __shared__ __align__(16) unsigned char smem[];
   FacShared<T>& sh = *reinterpret_cast<FacShared<T>*>(smem);
   int* ipiv = reinterpret_cast<int*>(smem + 512);
@@ -292,14 +292,22 @@ static int factor_level_impl(const SkelFactorLevel* F, int max_n, int max_k, cud
   if (max_n < 1) max_n = 1;
   size_t hdr = 512 + ((sizeof(int) * (size_t)max_n + 15) / 16) * 16;
   size_t need = hdr + fac_elems<T>(max_n, max_k) * sizeof(T);
+  // few boxes (upper levels): per-box latency is the critical path -> 1024 threads
+  const bool wide = nrun < skel_sm_count();
   if (need <= (size_t)skel_smem_optin()) {
-    auto kern = k_factor_level<T, false>;
-    SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
-    kern<<<nrun, 256, need, st>>>(*F, max_n, max_k);
+    if (wide) {
+      auto kern = k_factor_level<T, false, 1024>;
+      SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+      kern<<<nrun, 1024, need, st>>>(*F, max_n, max_k);
+    } else {
+      auto kern = k_factor_level<T, false, 256>;
+      SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+      kern<<<nrun, 256, need, st>>>(*F, max_n, max_k);
+    }
   } else {
     if (!F->scratch || (size_t)F->scratch_bytes < (size_t)nrun * fac_elems<T>(max_n, max_k) * sizeof(T))
       return -2;
-    auto kern = k_factor_level<T, true>;
+    auto kern = k_factor_level<T, true, 256>;
     SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hdr));
     kern<<<nrun, 256, hdr, st>>>(*F, max_n, max_k);
   }

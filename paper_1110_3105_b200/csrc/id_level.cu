@@ -15,7 +15,6 @@
 // re-run with min_rank = k because the CPQR is a deterministic state machine
 // whose first steps do not depend on min_rank.
 #include <cooperative_groups.h>
-#include <cstdlib>
 
 #include "cpqr.cuh"
 #include "entries.cuh"
@@ -177,8 +176,8 @@ __device__ __noinline__ void assemble_bie_lap2(const SkelSource& S, const SkelLe
   }
 }
 
-template <class T, int GL, int RPL, bool GW>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
+template <class T, int GL, int RPL, bool GW, int NT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
     k_id_level(const SkelSource S, const SkelLevel L, const int32_t* __restrict__ order,
                int64_t max_w, int max_n) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -510,24 +509,18 @@ __global__ void __launch_bounds__(256) k_dense_matvec(const SkelSource S, const 
 template <class T, int GL, int RPL, bool GW>
 static int launch_id_level(const SkelSource* src, const SkelLevel* lv, const int32_t* order,
                            int nrun, int64_t max_w, int max_n, size_t smem, cudaStream_t st) {
-  auto kern = k_id_level<T, GL, RPL, GW>;
-  SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  // thread-per-column CPQR (RPL < 0): GL threads per column
-  const int threads = RPL < 0 ? 64 : 128;
-  kern<<<2 * nrun, threads, smem, st>>>(*src, *lv, order, max_w, max_n);
-  return skel_last_error();
-}
-
-// CPQR update variant: 0 = lane groups (default), 1 = thread per column,
-// 2 = four threads per column
-// (SKEL_ID_MODE environment override, read once)
-static int skel_id_mode() {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("SKEL_ID_MODE");
-    mode = (e && e[0] >= '0' && e[0] <= '9') ? e[0] - '0' : 0;
+  // few boxes (upper levels): the per-box CPQR latency is the critical path,
+  // so give each box-side 16 warps instead of 4
+  if (2 * nrun < 2 * skel_sm_count()) {
+    auto kern = k_id_level<T, GL, RPL, GW, 512>;
+    SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<2 * nrun, 512, smem, st>>>(*src, *lv, order, max_w, max_n);
+  } else {
+    auto kern = k_id_level<T, GL, RPL, GW, 128>;
+    SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<2 * nrun, 128, smem, st>>>(*src, *lv, order, max_w, max_n);
   }
-  return mode;
+  return skel_last_error();
 }
 
 // register tile: GL lanes per column, RPL rows per lane (GL * RPL >= max_m)
@@ -536,11 +529,6 @@ static int dispatch_id_level(const SkelSource* src, const SkelLevel* lv, const i
                              int nrun, int max_m, int64_t max_w, int max_n, size_t smem,
                              cudaStream_t st) {
 #define SKEL_L(GL_, RPL_) launch_id_level<T, GL_, RPL_, GW>(src, lv, order, nrun, max_w, max_n, smem, st)
-  if (skel_id_mode() == 1) {
-    if (max_n <= 40) return SKEL_L(2, -1);
-    return SKEL_L(1, -1);
-  }
-  if (skel_id_mode() == 2) return SKEL_L(4, -1);
   if constexpr (sizeof(T) == 8) {
     if (max_m <= 64) return SKEL_L(8, 8);
     if (max_m <= 128) return SKEL_L(8, 16);

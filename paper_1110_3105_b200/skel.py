@@ -438,9 +438,12 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
     if eager_factor:
         from .solver import FactorRun
         run = FactorRun(field, 0.0, stream=eager_stream())
+    nvtx = _NVTX
     for li in range(top_run):
         lev_ctx = _profile.timed("level", level=li)
         lev_rec = lev_ctx.__enter__()
+        if nvtx:
+            torch.cuda.nvtx.range_push(f"level{li}")
         ids = covers[li]
         p = ids.size
         noff, nidx = tree.cover_neighbors(li)
@@ -587,6 +590,8 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             run.stream.wait_event(ev)
             run.add_level(li, dl)
         lev_ctx.__exit__(None, None, None)
+        if nvtx:
+            torch.cuda.nvtx.range_pop()
 
     if top_run < top:      # developer benchmarking only: partial sweep
         return levels
@@ -606,6 +611,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
 _OPTIN = None
 _DEBUG_MAX_LEVELS = [0]      # developer benchmarking: stop the sweep after this many levels
 _DEBUG_SKIP = [0]            # developer benchmarking: 1 = assembly only, 2 = + column norms
+_NVTX = bool(__import__("os").environ.get("SKEL_NVTX"))   # per-level NVTX ranges (profiling)
 
 
 class _nullctx:
