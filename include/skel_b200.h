@@ -127,10 +127,11 @@ int skel_id_level(const SkelSource* src, const SkelLevel* lv, const int32_t* box
                   int32_t field, void* stream);
 
 /* D = A(rd, cd) of every box of a cover with the children's diagonal
- * blocks zeroed (skel.py:344-348), into lv->D at lv->d_off.  max_n bounds
- * n_r and n_c. */
-int skel_assemble_D(const SkelSource* src, const SkelLevel* lv, int32_t max_n, int32_t field,
-                    void* stream);
+ * blocks zeroed (skel.py:344-348), into lv->D at lv->d_off.  order (nrun
+ * box indices) restricts the launch to a subset (a rank's own boxes); NULL
+ * = all lv->nbox boxes.  max_n bounds n_r and n_c. */
+int skel_assemble_D(const SkelSource* src, const SkelLevel* lv, const int32_t* order, int32_t nrun,
+                    int32_t max_n, int32_t field, void* stream);
 
 /* Dense top-level skeleton matrix S = A(row_skel_a, col_skel_b), a != b,
  * zero diagonal blocks (skel.py:399-408). rows/cols: tree positions; rbox/cbox:

@@ -71,7 +71,7 @@ class SkelFactorLevel(ctypes.Structure):
 _P = ctypes.POINTER
 _SIGS = {
     "skel_id_level": [_P(SkelSource), _P(SkelLevel), c_vp, c_i32, c_i32, c_i32, c_i64, c_i32, c_vp],
-    "skel_assemble_D": [_P(SkelSource), _P(SkelLevel), c_i32, c_i32, c_vp],
+    "skel_assemble_D": [_P(SkelSource), _P(SkelLevel), c_vp, c_i32, c_i32, c_i32, c_vp],
     "skel_assemble_S": [_P(SkelSource), c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp],
     "skel_eval_block": [_P(SkelSource), c_vp, c_i32, c_vp, c_i32, c_vp, c_i32, c_vp],
     "skel_id_batched": [c_vp, c_vp, c_vp, c_vp, c_i32, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp,

@@ -203,17 +203,18 @@ def point_source_data(curve: Curve2D, source, spec: KernelSpec) -> np.ndarray:
 
 
 def compress_system(system: BieSystem, eps, max_leaf_size=None, proxy: ProxyConfig | None = None,
-                    mode="proxy", seed=0):
-    """Tree over the curve nodes + GPU skeletonization (bie.py:265-272)."""
+                    mode="proxy", seed=0, shard=None):
+    """Tree over the curve nodes + GPU skeletonization (bie.py:265-272).
+    ``shard`` (extension): see compress_source."""
     tree = build_tree(system.points, max_leaf_size)
     cm = compress_source(BieSource(system, tree.perm), tree, eps, proxy=proxy, mode=mode,
-                         seed=seed)
+                         seed=seed, shard=shard)
     return tree, cm
 
 
-def solve_dirichlet(system: BieSystem, rhs, eps, max_leaf_size=None):
+def solve_dirichlet(system: BieSystem, rhs, eps, max_leaf_size=None, shard=None):
     """compress, factor, solve (bie.py:275-279).  Returns (density, cm, fi)."""
-    _, cm = compress_system(system, eps, max_leaf_size)
+    _, cm = compress_system(system, eps, max_leaf_size, shard=shard)
     fi = factor(cm)
     return solve(fi, rhs), cm, fi
 

@@ -343,12 +343,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
 // D = A(rd, cd) with the children's diagonal blocks zeroed (skel.py:344-348),
 // one CTA per box, both point sets staged in shared memory (SoA).
 template <class T>
-__global__ void __launch_bounds__(128) k_assemble_D(const SkelSource S, const SkelLevel L, int max_n) {
+__global__ void __launch_bounds__(128) k_assemble_D(const SkelSource S, const SkelLevel L, int max_n,
+                                                    const int32_t* __restrict__ order) {
   extern __shared__ __align__(16) unsigned char smem[];
   Pt* rp = reinterpret_cast<Pt*>(smem);
   Pt* cpp = rp + max_n;
   __shared__ int rsplit[SKEL_MAX_CHILD + 1], csplit[SKEL_MAX_CHILD + 1], nch_s;
-  const int a = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int a = order ? order[blockIdx.x] : (int)blockIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
   const int64_t r0 = L.rdof_off[a], c0 = L.cdof_off[a];
   const int nr = (int)(L.rdof_off[a + 1] - r0), nc = (int)(L.cdof_off[a + 1] - c0);
   if (nr == 0 || nc == 0) return;
@@ -612,18 +614,19 @@ int skel_id_level(const SkelSource* src, const SkelLevel* lv, const int32_t* box
   return id_level_impl<zc>(src, lv, box_order, nbox_run, max_m, max_n, max_w, st);
 }
 
-int skel_assemble_D(const SkelSource* src, const SkelLevel* lv, int32_t max_n, int32_t field,
-                    void* stream) {
-  if (lv->nbox <= 0) return 0;
+int skel_assemble_D(const SkelSource* src, const SkelLevel* lv, const int32_t* order, int32_t nrun,
+                    int32_t max_n, int32_t field, void* stream) {
+  const int nb = order ? nrun : lv->nbox;
+  if (nb <= 0) return 0;
   if (max_n < 1) max_n = 1;
   cudaStream_t st = (cudaStream_t)stream;
   size_t smem = 2 * sizeof(Pt) * (size_t)max_n;
   if (field == 0) {
     SKEL_TRY(cudaFuncSetAttribute(k_assemble_D<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_assemble_D<double><<<lv->nbox, 128, smem, st>>>(*src, *lv, max_n);
+    k_assemble_D<double><<<nb, 128, smem, st>>>(*src, *lv, max_n, order);
   } else {
     SKEL_TRY(cudaFuncSetAttribute(k_assemble_D<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_assemble_D<zc><<<lv->nbox, 128, smem, st>>>(*src, *lv, max_n);
+    k_assemble_D<zc><<<nb, 128, smem, st>>>(*src, *lv, max_n, order);
   }
   return skel_last_error();
 }

@@ -168,9 +168,10 @@ class DevLevel:
     packed upload per level)."""
 
     def __init__(self, li, nr, nc, kr, kc, d_off, l_off, r_off, D, L, R, rskel, cskel, child_off,
-                 dtype, t=None):
+                 dtype, t=None, mine=None):
         from ._staging import Packer
         self.li = li
+        self.mine = mine          # sharded level: boolean mask of this rank's boxes
         self.p = nr.size
         self.nr, self.nc = nr.astype(np.int64), nc.astype(np.int64)
         self.kr, self.kc = kr.astype(np.int64), kc.astype(np.int64)
@@ -195,6 +196,8 @@ class DevLevel:
         self.t_rdof_off, self.t_cdof_off = t["rdof_off"], t["cdof_off"]
         self.t_kr_off, self.t_kc_off = t["kr_off"], t["kc_off"]
         self.t_child_off = t.get("child_off")
+        self.t_own = t.get("own")
+        self.n_own = None if mine is None else int(mine.sum())
 
 
 class CompressedLevel:
@@ -221,6 +224,8 @@ class CompressedLevel:
     def nodes(self):
         if self._nodes is None:
             d = self.dev
+            if getattr(d, "mine", None) is not None:
+                raise InvalidInput("per-node blocks of a sharded level live on their owning ranks")
             D = d.D.cpu().numpy()
             L = d.L.cpu().numpy()
             R = d.R.cpu().numpy()
@@ -264,6 +269,7 @@ class CompressedMatrix:
         self.scalar_field = scalar_field
         self.tree = tree
         self._eager = None
+        self.shard = None          # shard.ShardPlan when compressed across ranks
 
     @property
     def S(self):
@@ -384,9 +390,16 @@ def _segment_sum(vals, off):
 
 def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = None,
                     mode: str = "proxy", equalize_ranks: bool = True, seed: int = 0,
-                    allow_large: bool = False, eager_factor: bool = True) -> CompressedMatrix:
+                    allow_large: bool = False, eager_factor: bool = True,
+                    shard=None) -> CompressedMatrix:
     """GPU compression sweep over a matrix source with a device descriptor
     (skel.py:286-411).
+
+    ``shard`` (extension): a ``shard.ShardPlan`` (or "auto" = one rank per
+    process of the current torch.distributed job) splits the boxes of the
+    levels at and below the plan's split level across ranks; every rank
+    ends with the skeletons of all boxes and the blocks of its own (see
+    shard.py).  Results are bit-identical to the unsharded sweep.
 
     ``eager_factor`` (extension, default on): each level's telescoping
     factorization is launched on a side stream as soon as the level is
@@ -414,6 +427,11 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
     tdt = _native.torch_dtype(field)
     covers = tree.levels
     top = next(i for i, c in enumerate(covers) if len(c) == 1)
+    if isinstance(shard, str):
+        if shard != "auto":
+            raise InvalidInput(f"unknown shard option {shard!r}")
+        from .shard import default_plan
+        shard = default_plan(tree)
     top_run = min(top, _DEBUG_MAX_LEVELS[0]) if _DEBUG_MAX_LEVELS[0] else top
     L = _native.lib()
     st = _native.stream_ptr()
@@ -437,7 +455,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
     run = None
     if eager_factor:
         from .solver import FactorRun
-        run = FactorRun(field, 0.0, stream=eager_stream())
+        run = FactorRun(field, 0.0, stream=eager_stream(), shard=shard)
     nvtx = _NVTX
     for li in range(top_run):
         lev_ctx = _profile.timed("level", level=li)
@@ -446,6 +464,8 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             torch.cuda.nvtx.range_push(f"level{li}")
         ids = covers[li]
         p = ids.size
+        mine = shard.mine(li) if shard is not None else None
+        own = np.ones(p, dtype=np.int64) if mine is None else mine.astype(np.int64)
         noff, nidx = tree.cover_neighbors(li)
         if li == 0:
             nr = (tree.hi[ids] - tree.lo[ids]).astype(np.int64)
@@ -469,7 +489,8 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         unit = np.concatenate(tables, axis=0)
         m0 = _segment_sum(nc[nidx], noff) + neff
         m1 = _segment_sum(nr[nidx], noff) + neff
-        d_off, l_off, r_off = _off(nr * nc), _off(nr * nr), _off(nc * nc)
+        # slab slots only for this rank's boxes (all boxes when unsharded)
+        d_off, l_off, r_off = _off(nr * nc * own), _off(nr * nr * own), _off(nc * nc * own)
         # size buckets: each launch gets a tight shared-memory footprint (so
         # small boxes run several CTAs per SM) and a register tile matched to
         # its tallest target; buckets run concurrently on side streams
@@ -479,7 +500,8 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         cls = (np.searchsorted(np.asarray(_W_CLASSES), wb, side="left") * 16
                + np.searchsorted(np.asarray(_M_CLASSES), need_m, side="left"))
         buckets = []
-        for c in np.unique(cls):
+        cls = np.where(own > 0, cls, -1)
+        for c in np.unique(cls[cls >= 0]):
             sel = np.nonzero(cls == c)[0]
             sel = sel[np.argsort(-wb[sel], kind="stable")].astype(np.int32)
             buckets.append(sel)
@@ -493,6 +515,10 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             pk.add("child_off", child_off)
         for bi, sel in enumerate(buckets):
             pk.add(f"order{bi}", sel)
+        own_idx = None
+        if mine is not None:
+            own_idx = np.nonzero(mine)[0].astype(np.int32)
+            pk.add("own", own_idx)
         t = pk.upload()
         Dt = torch.empty(max(int(d_off[-1]), 1), dtype=tdt, device=dev)
         Lt = torch.empty(max(int(l_off[-1]), 1), dtype=tdt, device=dev)
@@ -523,7 +549,9 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         # D blocks on their own stream, concurrent with the ID buckets
         with torch.cuda.stream(streams[-1]):
             with _profile.timed("assemble_D", level=li):
-                _native.check(L.skel_assemble_D(desc, lvd, int(max(nr.max(initial=0), nc.max(initial=0), 1)),
+                _native.check(L.skel_assemble_D(desc, lvd, p_(t["own"]) if own_idx is not None else None,
+                                                0 if own_idx is None else own_idx.size,
+                                                int(max(nr.max(initial=0), nc.max(initial=0), 1)),
                                                 field, _native.stream_ptr()), "skel_assemble_D")
         for bi, sel in enumerate(buckets):
             max_m, max_n = int(need_m[sel].max()), int(need_n[sel].max())
@@ -546,6 +574,8 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             if rec is not None:
                 recs.append(rec)
         join(streams)
+        if mine is not None:
+            shard.all_reduce(kk)          # non-owned entries are zero on each rank
         kk_h = kk.cpu().numpy()
         kr = kk_h[:p].astype(np.int64)
         kc = kk_h[p:2 * p].astype(np.int64)
@@ -569,19 +599,35 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         pk2.add("kr_off", kro).add("kc_off", kco)
         t2 = pk2.upload()
         t2.update({k: t[k] for k in ("rdof_off", "cdof_off", "nr")})
+        if own_idx is not None:
+            t2["own"] = t["own"]
         if li > 0:
             t2["child_off"] = t["child_off"]
         t2["_buffer0"] = t["_buffer"]
-        rsk = torch.empty(max(int(kro[-1]), 1), dtype=torch.int32, device=dev)
-        csk = torch.empty(max(int(kco[-1]), 1), dtype=torch.int32, device=dev)
-        _native.check(L.skel_compact_i32(p, p_(t["rdof_off"]), p_(t2["kr"]), p_(t2["kr_off"]),
+        if mine is None:
+            rsk = torch.empty(max(int(kro[-1]), 1), dtype=torch.int32, device=dev)
+            csk = torch.empty(max(int(kco[-1]), 1), dtype=torch.int32, device=dev)
+            klen_r, klen_c = t2["kr"], t2["kc"]
+        else:
+            # each rank compacts its own boxes' skeletons; the sum over ranks
+            # (one integer all-reduce of both lists) is the full list
+            sk = torch.zeros(max(int(kro[-1]) + int(kco[-1]), 1), dtype=torch.int32, device=dev)
+            rsk, csk = sk[:int(kro[-1])], sk[int(kro[-1]):]
+            pk3 = Packer()
+            pk3.add("kr", (kr * own).astype(np.int32)).add("kc", (kc * own).astype(np.int32))
+            t3 = pk3.upload()
+            klen_r, klen_c = t3["kr"], t3["kc"]
+            t2["_buffer3"] = t3["_buffer"]
+        _native.check(L.skel_compact_i32(p, p_(t["rdof_off"]), p_(klen_r), p_(t2["kr_off"]),
                                          p_(rskel), p_(rsk), st), "skel_compact_i32")
-        _native.check(L.skel_compact_i32(p, p_(t["cdof_off"]), p_(t2["kc"]), p_(t2["kc_off"]),
+        _native.check(L.skel_compact_i32(p, p_(t["cdof_off"]), p_(klen_c), p_(t2["kc_off"]),
                                          p_(cskel), p_(csk), st), "skel_compact_i32")
+        if mine is not None:
+            shard.all_reduce(sk)
         rsk, csk = rsk[:int(kro[-1])], csk[:int(kco[-1])]
         # L is stored nr x kr inside an nr x nr slot, R kc x nc inside nc x nc
         dl = DevLevel(li, nr, nc, kr, kc, d_off, l_off, r_off, Dt, Lt, Rt, rsk, csk, child_off,
-                      dtype, t=t2)
+                      dtype, t=t2, mine=mine)
         levels.append(CompressedLevel(dev=dl))
         prev = dl
         if run is not None:
@@ -605,6 +651,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
                                         p_(cbox), Kc, p_(S), field, st), "skel_assemble_S")
     cm = CompressedMatrix(levels, None, n, eps, tree.perm.copy(), sfield, tree, S_dev=S)
     cm._eager = run
+    cm.shard = shard
     return cm
 
 
@@ -683,25 +730,34 @@ def apply(cm: CompressedMatrix, x) -> np.ndarray:
         dls = cm.device_levels()
         us = [xt]
         u = xt
+        shard = getattr(cm, "shard", None)
         for dl in dls:
+            sh = dl.mine is not None
             nxt = torch.empty((int(dl.kc.sum()), Rn), dtype=X.dtype, device="cuda")
-            _native.check(L.skel_sweep_up_ex(dl.p, p_(dl.t_nr), p_(dl.t_kc), p_(dl.t_cdof_off),
-                                             p_(dl.t_kc_off), p_(dl.t_r_off), p_(dl.R), p_(u),
-                                             p_(nxt), Rn, field, int(max(dl.nc.max(), 1)),
-                                             int(dl.kc.max(initial=0)), None, st),
+            _native.check(L.skel_sweep_up_ex(dl.n_own if sh else dl.p, p_(dl.t_nr), p_(dl.t_kc),
+                                             p_(dl.t_cdof_off), p_(dl.t_kc_off), p_(dl.t_r_off),
+                                             p_(dl.R), p_(u), p_(nxt), Rn, field,
+                                             int(max(dl.nc.max(), 1)), int(dl.kc.max(initial=0)),
+                                             p_(dl.t_own) if sh else None, st),
                           "sweep_up")
+            if sh and dl.li == shard.split:
+                shard.gather_rows(nxt, _off(dl.kc), dl.li)
             us.append(nxt)
             u = nxt
         v = _dense_apply(cm.device_S(), u, field)
         for li in range(cm.nlevels - 1, -1, -1):
             dl = dls[li]
+            sh = dl.mine is not None
             w = torch.empty((int(dl.nr.sum()), Rn), dtype=X.dtype, device="cuda")
-            _native.check(L.skel_sweep_down_ex(dl.p, p_(dl.t_nr), p_(dl.t_kr), p_(dl.t_rdof_off),
-                                               p_(dl.t_kr_off), p_(dl.t_d_off), p_(dl.D),
-                                               p_(dl.t_l_off), p_(dl.L), p_(us[li]), p_(v), p_(w),
-                                               Rn, field, int(max(dl.nr.max(), 1)),
-                                               int(dl.kr.max(initial=0)), None, st),
+            _native.check(L.skel_sweep_down_ex(dl.n_own if sh else dl.p, p_(dl.t_nr), p_(dl.t_kr),
+                                               p_(dl.t_rdof_off), p_(dl.t_kr_off), p_(dl.t_d_off),
+                                               p_(dl.D), p_(dl.t_l_off), p_(dl.L), p_(us[li]), p_(v),
+                                               p_(w), Rn, field, int(max(dl.nr.max(), 1)),
+                                               int(dl.kr.max(initial=0)),
+                                               p_(dl.t_own) if sh else None, st),
                           "sweep_down")
+            if sh and li == 0:
+                shard.gather_rows(w, _off(dl.nr), 0)
             v = w
         yt = v
     out = torch.empty_like(yt)

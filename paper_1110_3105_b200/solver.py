@@ -35,8 +35,10 @@ class FactoredNode:
 
 
 class DevFactorLevel:
-    def __init__(self, n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, child_off, t):
+    def __init__(self, n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, child_off, t, n_own=None,
+                 mine=None):
         self.p = n.size
+        self.mine = mine            # sharded level: boolean mask of this rank's boxes
         self.n, self.k = n, k
         self.dd_off, self.ld_off, self.lam_off = dd_off, ld_off, lam_off
         self.Dd, self.Ld, self.Rd, self.Lam = Dd, Ld, Rd, Lam
@@ -49,8 +51,9 @@ class DevFactorLevel:
         self.max_nk = int(max((n + k).max(initial=0), 1))
         self.max_k = int(k.max(initial=0))
         # solve-sweep size buckets: (device order, count, max_n, max_k)
+        n_own = n if n_own is None else n_own
         self.solve_buckets = [(t[f"sv{bi}"], int(sel.size), int(n[sel].max()), int(k[sel].max()))
-                              for bi, sel in enumerate(_solve_buckets(n))]
+                              for bi, sel in enumerate(_solve_buckets(n_own))]
 
 
 _SOLVE_CLASSES = (24, 40, 56, 72, 96, 128)
@@ -82,6 +85,8 @@ class FactoredLevel:
     def nodes(self):
         if self._nodes is None:
             d = self.dev
+            if d.mine is not None:
+                raise InvalidInput("per-node blocks of a sharded level live on their owning ranks")
             Dd, Ld, Rd, Lam = (t.cpu().numpy() for t in (d.Dd, d.Ld, d.Rd, d.Lam))
             out = []
             for a in range(d.p):
@@ -99,8 +104,9 @@ class FactoredInverse:
     """Telescoping inverse held on the device (solver.py:162-176).
     ``S_hat`` / ``S_inv`` are the top matrix and its inverse (device)."""
 
-    def __init__(self, levels, S_hat, S_inv, n, perm, scalar_field, warnings):
+    def __init__(self, levels, S_hat, S_inv, n, perm, scalar_field, warnings, shard=None):
         self.levels = levels
+        self.shard = shard
         self.S_hat = S_hat
         self.S_inv = S_inv
         self.n = n
@@ -165,8 +171,9 @@ class FactorRun:
     drives one of these on a side stream so level l's factor overlaps level
     l+1's compression."""
 
-    def __init__(self, field, regularize=0.0, stream=None):
+    def __init__(self, field, regularize=0.0, stream=None, shard=None):
         self.torch = _native.require_cuda()
+        self.shard = shard
         self.field = field
         self.regularize = float(regularize)
         self.stream = stream
@@ -186,12 +193,16 @@ class FactorRun:
         lam_bad = (~sq_bad) & (dl.nr > 0) & (dl.kr != dl.kc)
         n = np.where(sq_bad | lam_bad, 0, dl.nr).astype(np.int64)
         k = np.where(n > 0, dl.kr, 0).astype(np.int64)
-        dd_off, ld_off, lam_off = _off(n * n), _off(n * k), _off(k * k)
+        mine = getattr(dl, "mine", None)
+        # sharded level: Dd / Ld / Rd slots for this rank's boxes only; the
+        # Lambda slab keeps every box's slot (parents above the split read it)
+        n_own = n if mine is None else n * mine
+        dd_off, ld_off, lam_off = _off(n_own * n_own), _off(n_own * k), _off(k * k)
         need = (n * n + 4 * n * k + k * k + 3 * n) * elem
         cls = np.searchsorted(np.asarray(_FAC_CLASSES), need, side="left")
         buckets = []
-        for c in np.unique(cls[n > 0]):
-            sel = np.nonzero((cls == c) & (n > 0))[0]
+        for c in np.unique(cls[n_own > 0]):
+            sel = np.nonzero((cls == c) & (n_own > 0))[0]
             buckets.append(sel[np.argsort(-need[sel], kind="stable")].astype(np.int32))
         p = dl.p
         outer = torch.cuda.stream(self.stream) if self.stream is not None else _nullctx()
@@ -202,17 +213,20 @@ class FactorRun:
             pk.add("dd_off", dd_off).add("ld_off", ld_off).add("lam_off", lam_off)
             for bi, sel in enumerate(buckets):
                 pk.add(f"order{bi}", sel)
-            for bi, sel in enumerate(_solve_buckets(n)):
+            for bi, sel in enumerate(_solve_buckets(n_own)):
                 pk.add(f"sv{bi}", sel)
             t = pk.upload()
             Dd = torch.empty(max(int(dd_off[-1]), 1), dtype=tdt, device=dev)
             Ld = torch.empty(max(int(ld_off[-1]), 1), dtype=tdt, device=dev)
             Rd = torch.empty(max(int(ld_off[-1]), 1), dtype=tdt, device=dev)
-            Lam = torch.empty(max(int(lam_off[-1]), 1), dtype=tdt, device=dev)
+            gather_lam = mine is not None and li == self.shard.split
+            Lam = (torch.zeros if gather_lam else torch.empty)(max(int(lam_off[-1]), 1), dtype=tdt,
+                                                               device=dev)
             status = torch.zeros(p, dtype=torch.int32, device=dev)
             rcd = torch.ones(p, dtype=torch.float64, device=dev)
             rcm = torch.ones(p, dtype=torch.float64, device=dev)
-            fl = DevFactorLevel(n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, dl.child_off, t)
+            fl = DevFactorLevel(n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, dl.child_off, t,
+                                n_own=n_own, mine=mine)
             prev = self.levels[-1][1] if self.levels else None
             F = _native.SkelFactorLevel()
             F.nbox, F.level, F.regularize = p, li, self.regularize
@@ -250,6 +264,8 @@ class FactorRun:
                     rec.nbytes = float(((nf[b_] ** 2 + 2 * nf[b_] * kf[b_]) * 2 + kf[b_] ** 2).sum()) * elem
             if streams:
                 join(streams)
+            if gather_lam:
+                self.shard.all_reduce(Lam)       # the split cover's Lambdas, everywhere
         self.levels.append(((sq_bad, lam_bad, n, k), fl, status, rcd, rcm, dl))
 
     def finish(self, cm):
@@ -261,6 +277,10 @@ class FactorRun:
         warns = []
         flevels = []
         for li, ((sq_bad, lam_bad, n, k), fl, status, rcd, rcm, dl) in enumerate(self.levels):
+            if fl.mine is not None:
+                self.shard.all_reduce(status, "max")
+                self.shard.all_reduce(rcd, "min")
+                self.shard.all_reduce(rcm, "min")
             sts, rd_h, rm_h = status.cpu().numpy(), rcd.cpu().numpy(), rcm.cpu().numpy()
             fails = np.nonzero(sq_bad | lam_bad | (sts != 0))[0]
             if fails.size:
@@ -294,12 +314,14 @@ class FactorRun:
                 Sh[kro[a]:kro[a] + ka, kro[a]:kro[a] + ka] = \
                     prev.Lam[prev.lam_off[a]:prev.lam_off[a] + ka * ka].view(ka, ka)
         if Sh.numel() == 0:
-            return FactoredInverse(flevels, Sh, None, cm.n, cm.perm.copy(), cm.scalar_field, warns)
+            return FactoredInverse(flevels, Sh, None, cm.n, cm.perm.copy(), cm.scalar_field, warns,
+                                   shard=self.shard)
         Sinv = Sh.clone()
         status, _ = _invert_top(Sinv, self.regularize, self.field)
         if status:
             raise SingularBlock("top", 0, "S")
-        return FactoredInverse(flevels, Sh, Sinv, cm.n, cm.perm.copy(), cm.scalar_field, warns)
+        return FactoredInverse(flevels, Sh, Sinv, cm.n, cm.perm.copy(), cm.scalar_field, warns,
+                               shard=self.shard)
 
 
 def factor(cm: CompressedMatrix, regularize: float = 0.0) -> FactoredInverse:
@@ -333,7 +355,7 @@ def factor(cm: CompressedMatrix, regularize: float = 0.0) -> FactoredInverse:
         for lv in cm.levels:
             if lv._nodes is not None:
                 lv.dev = None          # re-pack from the (possibly edited) host view
-    run = FactorRun(field, regularize)
+    run = FactorRun(field, regularize, shard=getattr(cm, "shard", None))
     for li, dl in enumerate(cm.device_levels()):
         run.add_level(li, dl)
     return run.finish(cm)
@@ -423,7 +445,8 @@ def solve_device(fi: FactoredInverse, B, graph: bool = True):
     a CUDA graph and replayed; B is copied into the graph's static input and
     the result copied out."""
     torch = _native.require_cuda()
-    if not graph or _profile.enabled or torch.cuda.is_current_stream_capturing():
+    if (not graph or _profile.enabled or torch.cuda.is_current_stream_capturing()
+            or fi.shard is not None):
         return _solve_device_eager(fi, B)
     key = (int(B.shape[1]), B.dtype)
     cache = fi.__dict__.setdefault("_graphs", {})
@@ -467,11 +490,16 @@ def _solve_device_eager(fi: FactoredInverse, B):
     else:
         us = [bt]
         u = bt
-        for lv in fi.levels:
+        shard = fi.shard
+        for li, lv in enumerate(fi.levels):
             d = lv.dev
+            sh = d.mine is not None
             nxt = torch.empty((int(d.k.sum()), Rn), dtype=B.dtype, device="cuda")
             with _profile.timed("sweep", dir="up") as rec:
                 _sweep_launch(L, d, "up", u, None, nxt, Rn, field)
+            if sh and li == shard.split:
+                # split-level vector: every rank's rows, on every rank
+                shard.gather_rows(nxt, _off(d.k), li)
             if rec is not None:
                 _sweep_work(rec, d, Rn, field, up=True)
             us.append(nxt)
@@ -479,9 +507,12 @@ def _solve_device_eager(fi: FactoredInverse, B):
         v = _dense_apply(fi.S_inv, u, field) if (fi.S_inv is not None and u.shape[0]) else u
         for li in range(len(fi.levels) - 1, -1, -1):
             d = fi.levels[li].dev
+            sh = d.mine is not None
             w = torch.empty((int(d.n.sum()), Rn), dtype=B.dtype, device="cuda")
             with _profile.timed("sweep", dir="down") as rec:
                 _sweep_launch(L, d, "down", us[li], v, w, Rn, field)
+            if sh and li == 0:
+                shard.gather_rows(w, _off(d.n), 0)   # every rank's solution rows
             if rec is not None:
                 _sweep_work(rec, d, Rn, field, up=False)
             v = w
