@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=2 ** 20)
+    ap.add_argument("--points", dest="n", type=int, default=2 ** 20)
     ap.add_argument("--eps", type=float, default=1e-12)
     ap.add_argument("--nrhs", type=int, default=16)
     ap.add_argument("--nrhs-big", type=int, default=1024)
@@ -204,12 +204,16 @@ def run_ours(args):
     from paper_1110_3105_b200 import _native, _profile
 
     ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % max(torch.cuda.device_count(), 1))
     dist = None
     if ws > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SKEL_DIST_BACKEND", "nccl")   # gloo: code-path checks only
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if dist is not None:
@@ -246,7 +250,7 @@ def run_ours(args):
         sk.solve_device(fi, B_dev)
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local % max(torch.cuda.device_count(), 1))
     clocks.start()
     fts, sts = [], []
     launches0 = _native.launch_count[0]
@@ -333,14 +337,28 @@ def run_ours(args):
                   "unit": "GB/s", "peak_source": hbm_src, "launches": sc}
     roof_solve["frac"] = roof_solve["achieved"] / hbm_pk
 
-    # config 5: 1024 RHS on the same factorization (same block on every rank)
+    # config 5: 1024 RHS on the same factorization.  N>1: the sharded factor
+    # is replicated once (one all-gather per slab, timed and reported), then
+    # the RHS columns are sharded with no further traffic
     big = None
     if args.nrhs_big > 0:
-        bc = args.nrhs_big
+        rep_ms = None
+        fi_big = fi
+        if ws > 1:
+            torch.cuda.synchronize()
+            barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            fi_big = fi.replicate()
+            b.record()
+            torch.cuda.synchronize()
+            rep_ms = max_over_ranks(a.elapsed_time(b))
+        bc = np.array_split(np.arange(args.nrhs_big), ws)[rank].size
         g = torch.Generator(device="cuda")
-        g.manual_seed(1234)
+        g.manual_seed(1234 + rank)
         Bb = torch.randn((n, bc), dtype=torch.float64, device="cuda", generator=g)
-        sk.solve_device(fi, Bb)
+        sk.solve_device(fi_big, Bb)
         torch.cuda.synchronize()
         ts = []
         _profile.reset()
@@ -350,7 +368,7 @@ def run_ours(args):
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record()
-            sk.solve_device(fi, Bb)
+            sk.solve_device(fi_big, Bb)
             b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b) * 1e-3)
@@ -358,11 +376,12 @@ def run_ours(args):
         _, bms, bflops, bbytes = _profile.summary("sweep")
         tb = max_over_ranks(statistics.mean(ts))
         big = {"R": args.nrhs_big, "nrhs_per_s": n * args.nrhs_big / tb, "ms": tb * 1e3,
+               "columns_per_rank": bc, "replicate_factor_ms": rep_ms,
                "roofline": {"kernel": "k_sweep_up/k_sweep_down", "bound": "fp64",
                             "achieved": bflops / (bms * 1e-3) / 1e12 if bms else 0.0,
                             "peak": fp64_pk, "unit": "TFLOP/s"}}
         big["roofline"]["frac"] = big["roofline"]["achieved"] / fp64_pk
-        del Bb
+        del Bb, fi_big
 
     # end to end through the public API, host buffers in and out
     e2e_ts = []

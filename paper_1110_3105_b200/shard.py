@@ -64,33 +64,44 @@ class ShardPlan:
         o = self.owners[li]
         return int(np.searchsorted(o, q, side="left")), int(np.searchsorted(o, q, side="right"))
 
+    def bounds(self, off, li):
+        """Per-rank [lo, hi) of an offset array over the level-li boxes."""
+        out = []
+        for q in range(self.world):
+            b0, b1 = self.box_range(li, q)
+            out.append((int(off[b0]), int(off[b1])))
+        return out
+
+    def all_gather_var(self, local, bounds, out):
+        """out[bounds[q]] = rank q's ``local`` (rows; every rank's block is
+        contiguous).  One all_gather of equal-size padded blocks."""
+        import torch
+        import torch.distributed as dist
+        width = int(np.prod(out.shape[1:])) if out.dim() > 1 else 1
+        flat = out.view(out.shape[0], width)
+        mx = max(max(hi - lo for lo, hi in bounds), 1)
+        lo, hi = bounds[self.rank]
+        mine = torch.zeros((mx, width), dtype=out.dtype, device=out.device)
+        mine[:hi - lo].copy_(local.reshape(hi - lo, width))
+        if out.is_cuda and self._backend() == "gloo":
+            parts = [torch.empty((mx, width), dtype=out.dtype) for _ in range(self.world)]
+            dist.all_gather(parts, mine.cpu(), group=self.group)
+            buf = torch.cat(parts).to(out.device)
+        else:
+            buf = torch.empty((self.world * mx, width), dtype=out.dtype, device=out.device)
+            dist.all_gather_into_tensor(buf, mine, group=self.group)
+        for q, (a, b) in enumerate(bounds):
+            if b > a:
+                flat[a:b].copy_(buf[q * mx:q * mx + (b - a)])
+        return out
+
     def gather_rows(self, t, off, li):
         """All-gather of a row-sharded (rows, R) tensor: rank q holds rows
         off[b0_q]:off[b1_q] of the level-li box ranges; afterwards every rank
-        holds all rows (one all_gather of padded equal-size blocks)."""
-        import torch
-        import torch.distributed as dist
-        bounds = []
-        for q in range(self.world):
-            b0, b1 = self.box_range(li, q)
-            bounds.append((int(off[b0]), int(off[b1])))
-        width = int(np.prod(t.shape[1:])) if t.dim() > 1 else 1
-        flat = t.view(t.shape[0], width)
-        mx = max(max(hi - lo for lo, hi in bounds), 1)
-        lo, hi = bounds[self.rank]
-        mine = torch.zeros((mx, width), dtype=t.dtype, device=t.device)
-        mine[:hi - lo].copy_(flat[lo:hi])
-        if t.is_cuda and self._backend() == "gloo":
-            parts = [torch.empty((mx, width), dtype=t.dtype) for _ in range(self.world)]
-            dist.all_gather(parts, mine.cpu(), group=self.group)
-            buf = torch.cat(parts).to(t.device)
-        else:
-            buf = torch.empty((self.world * mx, width), dtype=t.dtype, device=t.device)
-            dist.all_gather_into_tensor(buf, mine, group=self.group)
-        for q, (a, b) in enumerate(bounds):
-            if q != self.rank and b > a:
-                flat[a:b].copy_(buf[q * mx:q * mx + (b - a)])
-        return t
+        holds all rows."""
+        bd = self.bounds(off, li)
+        lo, hi = bd[self.rank]
+        return self.all_gather_var(t[lo:hi], bd, t)
 
     def sharded(self, li):
         return li <= self.split

@@ -138,6 +138,42 @@ class FactoredInverse:
     def solve(self, b):
         return solve(self, b)
 
+    def replicate(self):
+        """Sharded factorization -> a full copy on every rank (SURVEY 8(e),
+        config 5: replicate the factor once, then shard RHS columns with no
+        further traffic).  One variable-size all-gather per sharded slab;
+        returns a new, unsharded FactoredInverse (self unchanged)."""
+        if self.shard is None:
+            return self
+        torch = _native.require_cuda()
+        sp = self.shard
+        levels = []
+        for li, lv in enumerate(self.levels):
+            d = lv.dev
+            if d.mine is None:
+                levels.append(lv)
+                continue
+            n, k = d.n, d.k
+            dd_off, ld_off = _off(n * n), _off(n * k)
+            slabs = []
+            for src, off in ((d.Dd, dd_off), (d.Ld, ld_off), (d.Rd, ld_off)):
+                full = torch.empty(max(int(off[-1]), 1), dtype=src.dtype, device=src.device)
+                bd = sp.bounds(off, li)
+                lo, hi = bd[sp.rank]
+                sp.all_gather_var(src[:hi - lo], bd, full[:int(off[-1])])
+                slabs.append(full)
+            pk = Packer()
+            pk.add("n", n.astype(np.int32)).add("k", k.astype(np.int32))
+            pk.add("noff", _off(n)).add("koff", _off(k))
+            pk.add("dd_off", dd_off).add("ld_off", ld_off).add("lam_off", d.lam_off)
+            for bi, sel in enumerate(_solve_buckets(n)):
+                pk.add(f"sv{bi}", sel)
+            t = pk.upload()
+            levels.append(FactoredLevel(DevFactorLevel(n, k, dd_off, ld_off, d.lam_off, slabs[0],
+                                                       slabs[1], slabs[2], d.Lam, d.child_off, t)))
+        return FactoredInverse(levels, self.S_hat, self.S_inv, self.n, self.perm, self.scalar_field,
+                               self.warnings)
+
     def factor_bytes(self):
         it = np.dtype(self.dtype).itemsize
         tot = 0

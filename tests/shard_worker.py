@@ -91,8 +91,18 @@ def solve(out, n, eps):
     Xs = sk.solve(fi, B)
     Y = sk.apply(cm, B[:, 0])
     kr = np.concatenate([lv.dev.kr for lv in cm.levels])
+    # replicated factor + column-sharded RHS (config-5 layout): rank r solves
+    # columns r::world locally; gathered here only for the check
+    fr = fi.replicate()
+    assert fr.shard is None
+    Xr = sk.solve(fr, B[:, rank::world])
+    parts = [None] * world
+    dist.all_gather_object(parts, Xr)
+    Xc = np.empty_like(Xs)
+    for q in range(world):
+        Xc[:, q::world] = parts[q]
     if rank == 0:
-        np.savez(out, X=Xs, Y=Y, kr=kr, split=cm.shard.split, S=cm.S_dev.cpu().numpy())
+        np.savez(out, X=Xs, Xc=Xc, Y=Y, kr=kr, split=cm.shard.split, S=cm.S_dev.cpu().numpy())
     dist.barrier()
     dist.destroy_process_group()
 

@@ -75,4 +75,5 @@ def test_sharded_solve_bit_identical(tmp_path, n, eps, world):
     np.testing.assert_array_equal(d["kr"], kr)
     np.testing.assert_array_equal(d["S"], cm.S_dev.cpu().numpy())
     np.testing.assert_array_equal(d["X"], X)
+    np.testing.assert_array_equal(d["Xc"], X)
     np.testing.assert_array_equal(d["Y"], Y)
