@@ -72,19 +72,32 @@ class ResidentPoints:
     once; tree orderings are gathered from it on the device)."""
 
     def __init__(self, coords, normals=None, weights=None, curvatures=None):
-        torch = _native.require_cuda()
+        _native.require_cuda()
+        from ._staging import Packer
         coords = np.asarray(coords, dtype=np.float64)
         self.n, self.dim = coords.shape
-        put = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to("cuda")  # noqa: E731
-        self.x, self.y = put(coords[:, 0]), put(coords[:, 1])
-        self.z = put(coords[:, 2]) if self.dim == 3 else None
+        # one pinned staging block, one async copy for all SoA arrays
+        pk = Packer()
+        names = ["x", "y", "z"][:self.dim]
+        cols = [np.ascontiguousarray(coords[:, j]) for j in range(self.dim)]
+        for j, nm in enumerate(names):
+            pk.add(nm, cols[j])
         if normals is not None:
             nt = np.asarray(normals, dtype=np.float64)
-            self.nx, self.ny = put(nt[:, 0]), put(nt[:, 1])
-            self.nz = put(nt[:, 2]) if self.dim == 3 else None
-        else:
-            self.nx = self.ny = self.nz = None
-        self.w = None if weights is None else put(weights)
-        self.curv = None if curvatures is None else put(curvatures)
-        span = max(float(np.ptp(coords, axis=0).max()), float(np.abs(coords).max()), 1.0)
+            for j, nm in enumerate(["nx", "ny", "nz"][:self.dim]):
+                pk.add(nm, nt[:, j])
+        if weights is not None:
+            pk.add("w", np.asarray(weights, dtype=np.float64).reshape(-1))
+        if curvatures is not None:
+            pk.add("curv", np.asarray(curvatures, dtype=np.float64).reshape(-1))
+        t = pk.upload()
+        self._buf = t["_buffer"]
+        for nm in ("x", "y", "z", "nx", "ny", "nz", "w", "curv"):
+            setattr(self, nm, t.get(nm))
+        # ptp / |.|max from per-column extrema (contiguous reductions; a
+        # strided axis-0 reduce of an (N, d) array is ~20x slower)
+        lo = [float(v.min()) for v in cols]
+        hi = [float(v.max()) for v in cols]
+        span = max(max(h - l for l, h in zip(lo, hi)), max(max(abs(l), abs(h)) for l, h in zip(lo, hi)),
+                   1.0)
         self.coincide_tol = 1e-14 * span

@@ -201,3 +201,12 @@ def torch_dtype(field):
 
 def field_of(dtype):
     return 1 if np.issubdtype(np.dtype(dtype), np.complexfloating) else 0
+
+
+def to_host(t):
+    """Device tensor -> numpy through a (cached) pinned host block: a DMA
+    copy instead of the pageable staging path."""
+    torch = require_cuda()
+    h = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h.numpy()

@@ -41,7 +41,8 @@ class PointSet:
             nrm = np.ascontiguousarray(self.normals, dtype=np.float64)
             if nrm.shape != c.shape:
                 raise InvalidInput("normals must match coords shape")
-            if np.any(np.abs(np.linalg.norm(nrm, axis=1) - 1.0) > 1e-12):
+            # |n| per row (same sum of squares and sqrt as np.linalg.norm(axis=1))
+            if np.any(np.abs(np.sqrt(np.einsum("ij,ij->i", nrm, nrm)) - 1.0) > 1e-12):
                 raise InvalidInput("normals must be unit vectors (|n| = 1 within 1e-12)")
             self.normals = nrm
         for name in ("weights", "curvatures"):

@@ -764,7 +764,7 @@ def apply(cm: CompressedMatrix, x) -> np.ndarray:
     _native.check(L.skel_permute_rows(p_(perm), cm.n, p_(yt), p_(out), Rn, 1, field, st), "permute")
     if on_dev:
         return out[:, 0] if single else out
-    res = out.cpu().numpy()
+    res = _native.to_host(out)
     return res[:, 0] if single else res
 
 

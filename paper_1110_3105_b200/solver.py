@@ -425,7 +425,7 @@ def solve(fi: FactoredInverse, b):
     X = solve_device(fi, B)
     if on_dev:
         return X[:, 0] if single else X
-    x = X.cpu().numpy()
+    x = _native.to_host(X)
     return x[:, 0] if single else x
 
 
