@@ -210,6 +210,54 @@ int skel_dense_inverse(void* A, void* lu, int32_t* ipiv, int32_t K, double regul
                        int32_t* status, double* rcond, int32_t field, void* scratch,
                        void* stream);
 
+/* ---- big boxes (one box over the whole GPU; csrc/big.cu) ---------------
+ * Used for boxes whose target does not fit a per-box CTA (3D coarse levels)
+ * and for every target the reference sends to id_randomized
+ * (m > max(4096, 4n + 256), skel.py:419-421). */
+
+/* bytes of the CPQR state buffer for n columns */
+int64_t skel_big_state_bytes(int32_t n);
+
+/* Target of box `box`, side 0 = t_row.T, 1 = t_col (skel.py:349-368), into W
+ * (m x n column-major, leading dimension ld).  nbr_box / nbr_pref (device):
+ * the box's neighbours and the prefix sums of their dof counts (nnb + 1). */
+int skel_big_target(const SkelSource* src, const SkelLevel* lv, int32_t box, int32_t side,
+                    const int32_t* nbr_box, const int32_t* nbr_pref, int32_t nnb, int32_t m,
+                    int32_t n, void* W, int64_t ld, int32_t field, void* stream);
+
+/* Cooperative CPQR of W in place (pivoted_qr, lowrank.py:48-119); resume != 0
+ * continues from the state's rank with the new min_rank (equalisation). */
+int skel_cpqr_big(void* W, int32_t m, int32_t n, int64_t ld, double eps, int32_t min_rank,
+                  int32_t resume, void* state, int32_t field, void* stream);
+
+/* P = R11^-1 R12 in place + padding to min_rank (lowrank.py:122-161). */
+int skel_big_interp(void* W, int32_t n, int64_t ld, void* state, int32_t min_rank, int32_t field,
+                    void* stream);
+
+/* Sorted skeletons, L or R, kr / kc and the |P| > 2 flag of box `box`. */
+int skel_big_output(const SkelLevel* lv, int32_t box, int32_t side, const void* W, int64_t ld,
+                    const void* state, int32_t n, int32_t field, void* stream);
+
+/* Y (m x n) = X^T A; X k x m, A k x n; column-major (the sketch Omega A). */
+int skel_gemm_tn(int32_t m, int32_t n, int32_t k, const void* X, int64_t ldx, const void* A,
+                 int64_t lda, void* Y, int64_t ldy, int32_t field, void* stream);
+
+/* y = A x (trans 0) or A^H x (trans 1); A m x n column-major. */
+int skel_gemv(int32_t trans, int32_t m, int32_t n, const void* A, int64_t lda, const void* x,
+              void* y, int32_t field, void* stream);
+
+/* Probe of id_randomized (lowrank.py:220-228): u = P v, z = A v - A[:, skel] u
+ * for the sketch's CPQR state (interp already applied to Ysk). */
+int skel_big_probe(int32_t m, int32_t n, const void* A, int64_t lda, const void* Ysk, int64_t ldy,
+                   const void* state, const void* v, void* u, void* z, int32_t field, void* stream);
+
+/* Cooperative Gauss-Jordan inverse (partial pivoting) of a big n x n
+ * row-major matrix in place; *status (zeroed by the caller) = 1 on an exact
+ * zero pivot.  scratch: skel_gj_scratch_bytes(n). */
+int64_t skel_gj_scratch_bytes(int32_t n);
+int skel_dense_inverse_big(void* A, int32_t n, double regularize, int32_t* status, int32_t field,
+                           void* scratch, void* stream);
+
 /* ---- multi-RHS solve / apply sweeps (solver.py:279-318, skel.py:206-249) */
 
 /* out[koff[a]+t, :] = sum_j M_a[t, j] u[noff[a]+j, :]   (M_a: k x n row-major

@@ -14,7 +14,8 @@ from .errors import (AccuracyWarning, InvalidInput, NotConverged, RefusedTooLarg
                      SingularBlock, SkelkitError)
 from .geom import OrthTree, PointSet, build_tree, level_neighbors, neighbors
 from .kernels import KernelSpec, eval_block
-from .lowrank import InterpDecomp, id_fixed_precision, id_fixed_precision_batched, id_rows
+from .lowrank import (InterpDecomp, id_fixed_precision, id_fixed_precision_batched,
+                      id_fixed_precision_large, id_randomized, id_rows)
 from .skel import (CompressedLevel, CompressedMatrix, CompressedNode, KernelSource, ProxyConfig,
                    apply, compress, compress_source, proxy_points)
 from .solver import FactoredInverse, factor, solve, solve_device
@@ -25,7 +26,7 @@ __all__ = [
     "AccuracyWarning", "InvalidInput", "NotConverged", "RefusedTooLarge", "SingularBlock",
     "SkelkitError", "OrthTree", "PointSet", "build_tree", "level_neighbors", "neighbors",
     "KernelSpec", "eval_block", "InterpDecomp", "id_fixed_precision",
-    "id_fixed_precision_batched", "id_rows", "CompressedLevel", "CompressedMatrix",
+    "id_fixed_precision_batched", "id_fixed_precision_large", "id_randomized", "id_rows", "CompressedLevel", "CompressedMatrix",
     "CompressedNode", "KernelSource", "ProxyConfig", "apply", "compress", "compress_source",
     "proxy_points", "FactoredInverse", "factor", "solve", "solve_device", "__version__",
 ]

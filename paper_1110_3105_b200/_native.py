@@ -94,7 +94,19 @@ _SIGS = {
     "skel_tree_free": [c_vp],
     "skel_device_query": [_P(c_i32), _P(c_i32), _P(c_i32), _P(c_i32)],
     "skel_fp64_probe": [c_i32, c_i32, c_vp, _P(c_f64), c_vp],
+    "skel_big_state_bytes": [c_i32],
+    "skel_big_target": [_P(SkelSource), _P(SkelLevel), c_i32, c_i32, c_vp, c_vp, c_i32, c_i32, c_i32,
+                        c_vp, c_i64, c_i32, c_vp],
+    "skel_cpqr_big": [c_vp, c_i32, c_i32, c_i64, c_f64, c_i32, c_i32, c_vp, c_i32, c_vp],
+    "skel_big_interp": [c_vp, c_i32, c_i64, c_vp, c_i32, c_i32, c_vp],
+    "skel_big_output": [_P(SkelLevel), c_i32, c_i32, c_vp, c_i64, c_vp, c_i32, c_i32, c_vp],
+    "skel_gemm_tn": [c_i32, c_i32, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i32, c_vp],
+    "skel_gemv": [c_i32, c_i32, c_i32, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp],
+    "skel_big_probe": [c_i32, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp],
+    "skel_gj_scratch_bytes": [c_i32],
+    "skel_dense_inverse_big": [c_vp, c_i32, c_f64, c_vp, c_i32, c_vp, c_vp],
 }
+_RESTYPE_I64 = {"skel_big_state_bytes", "skel_gj_scratch_bytes"}
 
 _lib = None
 
@@ -102,7 +114,9 @@ _lib = None
 _LAUNCHING = {"skel_id_level", "skel_assemble_D", "skel_assemble_S", "skel_eval_block", "skel_id_batched",
               "skel_factor_level", "skel_dense_inverse", "skel_sweep_up_ex",
               "skel_sweep_down_ex", "skel_dense_apply", "skel_permute_rows",
-              "skel_compact_i32", "skel_dense_matvec", "skel_fp64_probe"}
+              "skel_compact_i32", "skel_dense_matvec", "skel_fp64_probe", "skel_big_target",
+              "skel_cpqr_big", "skel_big_interp", "skel_big_output", "skel_gemm_tn", "skel_gemv",
+              "skel_big_probe", "skel_dense_inverse_big"}
 launch_count = [0]
 
 
@@ -150,7 +164,7 @@ def lib():
         for name, args in _SIGS.items():
             fn = getattr(L, name)
             fn.argtypes = args
-            fn.restype = c_i32
+            fn.restype = c_i64 if name in _RESTYPE_I64 else c_i32
         L.skel_version.restype = ctypes.c_char_p
         L.skel_version.argtypes = []
         _lib = _CountingLib(L)

@@ -1,0 +1,678 @@
+// big.cu -- the "big box" path: interpolative decompositions and dense
+// inverses too large for one CTA (3D coarse levels, BASELINE config 4; the
+// top-level Shat of large 3D problems).  Every kernel here spreads ONE box
+// over the whole GPU:
+//
+//   * k_big_target     one side's proxy-compressed target (t_row.T or t_col,
+//                      skel.py:349-368) assembled into a global column-major
+//                      slab, 2D grid over (row tiles, column chunks);
+//   * k_cpqr_big       cooperative (grid-synchronised) column-pivoted QR with
+//                      the exact pivot / norm / stop rules of lowrank.py:48-119
+//                      (the same state machine as cpqr.cuh, two grid barriers
+//                      per step, one warp per trailing column);
+//   * k_big_interp     P = R11^-1 R12 (lowrank.py:122-133), one thread/column;
+//   * k_big_output     sorted skeletons + L / R into the level slabs
+//                      (skel.py:384-391);
+//   * k_gemm_tn / k_gemv / k_probe_*  the Gaussian sketch Y = Omega A, the
+//                      power-iteration norm estimate and the 5-probe check of
+//                      id_randomized (lowrank.py:169-231; the random numbers
+//                      come from the host with the reference's generator);
+//   * k_gj_coop        cooperative Gauss-Jordan inverse with partial pivoting
+//                      (the top-level Shat, solver.py:269-274).
+#include <cooperative_groups.h>
+
+#include "cpqr.cuh"
+#include "entries.cuh"
+
+namespace cg = cooperative_groups;
+
+template <class T>
+struct BigState {
+  int rank, stop, pad, pc;
+  double p0, beta, bigP, pad0;
+  T v0, alpha;
+};
+
+static inline size_t big_state_hdr() { return 256; }
+
+template <class T>
+struct BigView {
+  BigState<T>* st;
+  double* nrm;
+  double* ref;
+  double* xn2;
+  int* piv;
+};
+
+template <class T>
+__host__ __device__ inline BigView<T> big_view(void* buf, int n) {
+  BigView<T> v;
+  unsigned char* p = reinterpret_cast<unsigned char*>(buf);
+  v.st = reinterpret_cast<BigState<T>*>(p);
+  v.nrm = reinterpret_cast<double*>(p + 256);
+  v.ref = v.nrm + n;
+  v.xn2 = v.ref + n;
+  v.piv = reinterpret_cast<int*>(v.xn2 + n);
+  return v;
+}
+
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ zc ldcg(const zc* p) {
+  double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+  return zc(v.x, v.y);
+}
+__device__ __forceinline__ int ldcg(const int* p) { return __ldcg(p); }
+
+// ---------------------------------------------------------------------------
+// target assembly: rows = neighbour dofs (nbr_pref/nbr_box) then proxies
+template <class T>
+__global__ void __launch_bounds__(128)
+    k_big_target(const SkelSource S, const SkelLevel L, int a, int side, const int32_t* nbr_box,
+                 const int32_t* nbr_pref, int nnb, int m, T* W, int64_t ld) {
+  __shared__ Pt cp[64];
+  const int64_t r0 = L.rdof_off[a], c0 = L.cdof_off[a];
+  const int n = side == 0 ? (int)(L.rdof_off[a + 1] - r0) : (int)(L.cdof_off[a + 1] - c0);
+  const int32_t* mydofs = side == 0 ? L.rdofs + r0 : L.cdofs + c0;
+  const int j0 = blockIdx.y * 64;
+  const int jn = min(64, n - j0);
+  if (jn <= 0) return;
+  for (int j = threadIdx.x; j < jn; j += blockDim.x) cp[j] = load_pt(S, mydofs[j0 + j]);
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int m_nbr = nbr_pref[nnb];
+  if (i < m_nbr) {
+    int lo = 0, hi = nnb;             // last q with nbr_pref[q] <= i
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (nbr_pref[mid] <= i) lo = mid; else hi = mid;
+    }
+    const int b = nbr_box[lo];
+    const int off = i - nbr_pref[lo];
+    const int32_t idx = side == 0 ? L.cdofs[L.cdof_off[b] + off] : L.rdofs[L.rdof_off[b] + off];
+    const Pt rp = load_pt(S, idx);
+    if (side == 0) {
+      for (int j = 0; j < jn; ++j) W[(int64_t)(j0 + j) * ld + i] = entry_A<T>(S, cp[j], rp);
+    } else {
+      for (int j = 0; j < jn; ++j) W[(int64_t)(j0 + j) * ld + i] = entry_A<T>(S, rp, cp[j]);
+    }
+  } else {
+    const int dim = S.dim;
+    const int pr = L.pxy_begin[a] + (i - m_nbr);
+    const double rr = L.box_r[a];
+    const double px = __dadd_rn(L.box_c[(int64_t)a * dim + 0], __dmul_rn(rr, L.pxy_unit[(int64_t)pr * dim + 0]));
+    const double py = __dadd_rn(L.box_c[(int64_t)a * dim + 1], __dmul_rn(rr, L.pxy_unit[(int64_t)pr * dim + 1]));
+    const double pz = dim == 3 ? __dadd_rn(L.box_c[(int64_t)a * dim + 2], __dmul_rn(rr, L.pxy_unit[(int64_t)pr * dim + 2])) : 0.0;
+    if (side == 0) {
+      for (int j = 0; j < jn; ++j) W[(int64_t)(j0 + j) * ld + i] = entry_proxy_row<T>(S, cp[j], px, py, pz);
+    } else {
+      for (int j = 0; j < jn; ++j) W[(int64_t)(j0 + j) * ld + i] = entry_proxy_col<T>(S, px, py, pz, cp[j]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// cooperative CPQR
+
+__device__ __forceinline__ void cmerge(double& bv, int& bi, double ov, int oi) {
+  if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+}
+
+// exact initial norms (lowrank.py:55-64), piv = identity, state reset
+template <class T>
+__global__ void k_cpqr_big_init(const T* W, int m, int n, int64_t ld, void* buf) {
+  BigView<T> v = big_view<T>(buf, n);
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int tw = (gridDim.x * blockDim.x) >> 5;
+  for (int c = gw; c < n; c += tw) {
+    const T* x = W + (int64_t)c * ld;
+    double s = 0.0;
+    for (int i = lane; i < m; i += 32) s += sk_abs2(x[i]);
+    s = warp_sum(s);
+    if (lane == 0) { v.nrm[c] = s; v.ref[c] = s; v.xn2[c] = s; v.piv[c] = c; }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    v.st->rank = 0; v.st->stop = 0; v.st->pad = 0; v.st->pc = 0;
+    v.st->p0 = 0.0; v.st->beta = 0.0; v.st->bigP = 0.0;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256)
+    k_cpqr_big(T* W, int m, int n, int64_t ld, double eps, int min_rank, void* buf) {
+  cg::grid_group grid = cg::this_grid();
+  BigView<T> v = big_view<T>(buf, n);
+  __shared__ double sv[8];
+  __shared__ int si[8];
+  const int kmax = m < n ? m : n;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int tw = (gridDim.x * blockDim.x) >> 5;
+  int s = ldcg(&v.st->rank);
+  while (s < kmax) {
+    // ---- phase A (CTA 0): first-maximum pivot, stop rule, swap, reflector
+    if (blockIdx.x == 0) {
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+      for (int c = s + threadIdx.x; c < n; c += blockDim.x) cmerge(bv, bi, ldcg(v.nrm + c), c);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        cmerge(bv, bi, ov, oi);
+      }
+      if (lane == 0) { sv[wid] = bv; si[wid] = bi; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double b = -1.0;
+        int j = 0x7fffffff;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) cmerge(b, j, sv[w], si[w]);
+        int stop = 0;
+        if (j >= n) {
+          stop = 1;
+        } else {
+          const double pn = sqrt(fmax(ldcg(v.nrm + j), 0.0));
+          if (s == 0) {
+            v.st->p0 = pn;
+            if (pn == 0.0) stop = 1;
+          }
+          const double p0 = s == 0 ? pn : ldcg(&v.st->p0);
+          if (!stop && ((s >= min_rank && pn <= eps * p0) || pn == 0.0)) stop = 1;
+        }
+        if (!stop) {
+          if (j != s) {
+            double t = ldcg(v.nrm + s); v.nrm[s] = ldcg(v.nrm + j); v.nrm[j] = t;
+            t = ldcg(v.xn2 + s); v.xn2[s] = ldcg(v.xn2 + j); v.xn2[j] = t;
+            int q = ldcg(v.piv + s); v.piv[s] = ldcg(v.piv + j); v.piv[j] = q;
+          }
+          const int pc = ldcg(v.piv + s);
+          const double nx2 = ldcg(v.xn2 + s);
+          const T x0 = ldcg(W + (int64_t)pc * ld + s);
+          const double ax0 = sk_abs(x0);
+          const double normx = sqrt(nx2);
+          T phase = T(1.0);
+          if (ax0 != 0.0) phase = sk_unit_phase(x0, ax0);
+          const T alpha = -(phase * normx);
+          const double vv = 2.0 * normx * (normx + ax0);
+          v.st->v0 = x0 - alpha;
+          v.st->alpha = alpha;
+          v.st->beta = vv > 0.0 ? 2.0 / vv : 0.0;
+          v.st->pc = pc;
+        }
+        v.st->stop = stop;
+      }
+    }
+    grid.sync();
+    if (ldcg(&v.st->stop)) break;
+    // ---- phase B (all warps): reflector on every trailing column + norms
+    {
+      const int pc = ldcg(&v.st->pc);
+      const double beta = ldcg(&v.st->beta);
+      const T v0 = ldcg(&v.st->v0);
+      const int s1 = s + 1;
+      const bool renorm = (s1 < kmax) && (s1 % 32 == 0);
+      const T* vcol = W + (int64_t)pc * ld;
+      for (int c = s1 + gw; c < n; c += tw) {
+        T* wc = W + (int64_t)ldcg(v.piv + c) * ld;
+        T dot = T(0.0);
+        for (int i = s + lane; i < m; i += 32) {
+          const T vi = (i == s) ? v0 : ldcg(vcol + i);
+          dot += sk_conj(vi) * ldcg(wc + i);
+        }
+        dot = warp_sum(dot);
+        const T f = dot * beta;
+        double acc = 0.0;
+        T row = T(0.0);
+        for (int i = s + lane; i < m; i += 32) {
+          const T vi = (i == s) ? v0 : ldcg(vcol + i);
+          T w = ldcg(wc + i);
+          if (beta != 0.0) {
+            w -= vi * f;
+            wc[i] = w;
+          }
+          if (i > s) acc += sk_abs2(w);
+          if (i == s) row = w;
+        }
+        acc = warp_sum(acc);
+        row = shfl(row, 0);
+        if (lane == 0) {
+          double t = ldcg(v.nrm + c) - sk_abs2(row);
+          t = t > 0.0 ? t : 0.0;
+          const double rf = ldcg(v.ref + c);
+          if (renorm || t < 1e-8 * rf) { t = acc; v.ref[c] = acc; }
+          v.nrm[c] = t;
+          v.xn2[c] = acc;
+        }
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        W[(int64_t)pc * ld + s] = ldcg(&v.st->alpha);
+        v.st->rank = s + 1;
+      }
+    }
+    grid.sync();
+    ++s;
+  }
+}
+
+// P = R11^-1 R12 in place (rows 0..r-1 of the non-pivot columns), max|P|,
+// padding count to min_rank (lowrank.py:122-161)
+template <class T>
+__global__ void k_big_interp(T* W, int n, int64_t ld, void* buf, int min_rank) {
+  BigView<T> v = big_view<T>(buf, n);
+  const int r = v.st->rank;
+  const int c = r + blockIdx.x * blockDim.x + threadIdx.x;
+  double big = 0.0;
+  if (c < n) {
+    T* x = W + (int64_t)v.piv[c] * ld;
+    for (int s = r - 1; s >= 0; --s) {
+      T xs = x[s];
+      if (xs != T(0.0)) {
+        const T* rs = W + (int64_t)v.piv[s] * ld;
+        xs = xs / rs[s];
+        x[s] = xs;
+        for (int t = 0; t < s; ++t) x[t] -= rs[t] * xs;
+      }
+    }
+    for (int s = 0; s < r; ++s) big = fmax(big, sk_abs(x[s]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) big = fmax(big, __shfl_xor_sync(0xffffffffu, big, o));
+  if ((threadIdx.x & 31) == 0 && big > 0.0)
+    atomicMax(reinterpret_cast<unsigned long long*>(&v.st->bigP), (unsigned long long)__double_as_longlong(big));
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int kmin = min_rank < n ? min_rank : n;
+    v.st->pad = (r < kmin) ? kmin - r : 0;
+  }
+}
+
+template <class T>
+__device__ __forceinline__ T big_interp_entry(const T* W, int64_t ld, const int* piv, int r, int kfin,
+                                              int s, int q) {
+  if (q < kfin) return (s == q) ? T(1.0) : T(0.0);
+  return (s < r) ? W[(int64_t)piv[q] * ld + s] : T(0.0);
+}
+
+// sorted skeletons and L (n x K) / R (K x n) into the level slabs, k into
+// kr / kc, the |P| > 2 warning flag (skel.py:384-391, lowrank.py:128-132)
+template <class T>
+__global__ void k_big_output(const SkelLevel L, int a, int side, const T* W, int64_t ld, const void* buf,
+                             int n) {
+  extern __shared__ int pos[];
+  BigView<T> v = big_view<T>(const_cast<void*>(buf), n);
+  const int r = v.st->rank;
+  const int K = r + v.st->pad;
+  const int* piv = v.piv;
+  for (int s = threadIdx.x; s < K; s += blockDim.x) {
+    const int ps = piv[s];
+    int c = 0;
+    for (int t = 0; t < K; ++t) c += piv[t] < ps;
+    pos[s] = c;
+  }
+  __syncthreads();
+  const int64_t r0 = L.rdof_off[a], c0 = L.cdof_off[a];
+  const int32_t* mydofs = side == 0 ? L.rdofs + r0 : L.cdofs + c0;
+  int32_t* skel = side == 0 ? L.rskel + r0 : L.cskel + c0;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s = tid; s < K; s += nt) skel[pos[s]] = mydofs[piv[s]];
+  const int64_t tot = (int64_t)n * K;
+  if (side == 0) {
+    T* Lo = reinterpret_cast<T*>(L.L) + L.l_off[a];
+    for (int64_t e = tid; e < tot; e += nt) {
+      const int q = (int)(e / K), s = (int)(e - (int64_t)q * K);
+      Lo[(int64_t)piv[q] * K + pos[s]] = big_interp_entry<T>(W, ld, piv, r, K, s, q);
+    }
+  } else {
+    T* Ro = reinterpret_cast<T*>(L.R) + L.r_off[a];
+    for (int64_t e = tid; e < tot; e += nt) {
+      const int s = (int)(e / n), q = (int)(e - (int64_t)s * n);
+      Ro[(int64_t)pos[s] * n + piv[q]] = big_interp_entry<T>(W, ld, piv, r, K, s, q);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    (side == 0 ? L.kr : L.kc)[a] = K;
+    if (v.st->bigP > 2.0) atomicOr(L.flags + a, 1 << side);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sketch / probes of id_randomized
+
+// Y (m x n, ld ldy) = X^T A, X k x m (ld ldx), A k x n (ld lda), column-major
+template <class T>
+__global__ void __launch_bounds__(256)
+    k_gemm_tn(int m, int n, int k, const T* __restrict__ X, int64_t ldx, const T* __restrict__ A,
+              int64_t lda, T* Y, int64_t ldy) {
+  __shared__ T xs[16][65];
+  __shared__ T as[16][65];
+  const int r0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  T acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int w = 0; w < 4; ++w) acc[u][w] = T(0.0);
+  for (int i0 = 0; i0 < k; i0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int ii = e & 15, cc = e >> 4;
+      const int i = i0 + ii;
+      xs[ii][cc] = (i < k && r0 + cc < m) ? X[(int64_t)(r0 + cc) * ldx + i] : T(0.0);
+      as[ii][cc] = (i < k && c0 + cc < n) ? A[(int64_t)(c0 + cc) * lda + i] : T(0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ii = 0; ii < 16; ++ii) {
+      T xr[4], ar[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { xr[u] = xs[ii][ty * 4 + u]; ar[u] = as[ii][tx * 4 + u]; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) acc[u][w] += xr[u] * ar[w];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int r = r0 + ty * 4 + u, c = c0 + tx * 4 + w;
+      if (r < m && c < n) Y[(int64_t)c * ldy + r] = acc[u][w];
+    }
+}
+
+// y = A x (trans 0: thread per row) or y = A^H x (trans 1: warp per column)
+template <class T>
+__global__ void k_gemv(int trans, int m, int n, const T* __restrict__ A, int64_t lda,
+                       const T* __restrict__ x, T* y) {
+  if (trans == 0) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    T s = T(0.0);
+    for (int j = 0; j < n; ++j) s += A[(int64_t)j * lda + i] * x[j];
+    y[i] = s;
+  } else {
+    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (j >= n) return;
+    T s = T(0.0);
+    for (int i = lane; i < m; i += 32) s += sk_conj(A[(int64_t)j * lda + i]) * x[i];
+    s = warp_sum(s);
+    if (lane == 0) y[j] = s;
+  }
+}
+
+// u = P v for the interpolation matrix of a CPQR state (P[:, piv[s]] = e_s,
+// P[:, piv[q]] = X[:, q] for q >= r), length r
+template <class T>
+__global__ void k_probe_pv(const T* W, int n, int64_t ld, const void* buf, const T* vin, T* u) {
+  BigView<T> v = big_view<T>(const_cast<void*>(buf), n);
+  const int r = v.st->rank;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= r) return;
+  T acc = vin[v.piv[s]];
+  for (int q = r; q < n; ++q) acc += W[(int64_t)v.piv[q] * ld + s] * vin[v.piv[q]];
+  u[s] = acc;
+}
+
+// z = A v - A[:, skel] u  (skel = piv[:r] of the sketch's CPQR state)
+template <class T>
+__global__ void k_probe_z(int m, int n, const T* __restrict__ A, int64_t lda, const void* buf,
+                          const T* vin, const T* u, T* z) {
+  BigView<T> v = big_view<T>(const_cast<void*>(buf), n);
+  const int r = v.st->rank;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  T s1 = T(0.0), s2 = T(0.0);
+  for (int j = 0; j < n; ++j) s1 += A[(int64_t)j * lda + i] * vin[j];
+  for (int q = 0; q < r; ++q) s2 += A[(int64_t)v.piv[q] * lda + i] * u[q];
+  z[i] = s1 - s2;
+}
+
+// ---------------------------------------------------------------------------
+// cooperative Gauss-Jordan inverse, partial pivoting, row-major n x n in place
+// (the reference LU-factors Shat, solver.py:269-274; the explicit inverse
+// turns the top solve into one GEMM)
+
+template <class T>
+__global__ void __launch_bounds__(256)
+    k_gj_coop(T* A, int n, double regularize, int32_t* status, double* part_v, int* part_i,
+              T* colc, int* swaps) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sv[8];
+  __shared__ int si[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  if (regularize != 0.0) {
+    for (int64_t i = gt; i < n; i += nt) A[i * n + i] += T(regularize);
+    grid.sync();
+  }
+  for (int c = 0; c < n; ++c) {
+    // pivot: first max of |A[r][c]| over r >= c (LAPACK i?amax order)
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int64_t r = c + gt; r < n; r += nt) cmerge(bv, bi, sk_pivabs(ldcg(A + r * n + c)), (int)r);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      cmerge(bv, bi, ov, oi);
+    }
+    if (lane == 0) { sv[wid] = bv; si[wid] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = -1.0;
+      int j = 0x7fffffff;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) cmerge(b, j, sv[w], si[w]);
+      part_v[blockIdx.x] = b;
+      part_i[blockIdx.x] = j;
+    }
+    grid.sync();
+    double b = -1.0;
+    int p = 0x7fffffff;
+    for (int q = 0; q < (int)gridDim.x; ++q) cmerge(b, p, ldcg(part_v + q), ldcg(part_i + q));
+    if (p >= n || b == 0.0) {
+      if (gt == 0) *status = 1;
+      return;                        // uniform across the grid
+    }
+    const T apc = ldcg(A + (int64_t)p * n + c);
+    const T inv = T(1.0) / apc;
+    // swap rows c <-> p and scale the pivot row (column c excluded: it is
+    // rewritten whole below); save column c as it reads after the swap
+    for (int64_t j = gt; j < n; j += nt) {
+      if (j == c) continue;
+      const T vp = ldcg(A + (int64_t)p * n + j);
+      const T vc = ldcg(A + (int64_t)c * n + j);
+      if (p != c) A[(int64_t)p * n + j] = vc;
+      A[(int64_t)c * n + j] = vp * inv;
+    }
+    for (int64_t r = gt; r < n; r += nt) {
+      T v = (r == p) ? ldcg(A + (int64_t)c * n + c) : ldcg(A + r * n + c);
+      if (r == c) v = apc;
+      colc[r] = v;
+    }
+    if (gt == 0) swaps[c] = p;
+    grid.sync();
+    // eliminate column c from every other row (in-place inverse columns)
+    const int64_t tot = (int64_t)n * n;
+    for (int64_t e = gt; e < tot; e += nt) {
+      const int64_t r = e / n, j = e - r * n;
+      if (r == c) {
+        if (j == c) A[e] = inv;
+        continue;
+      }
+      const T f = ldcg(colc + r);
+      if (j == c) A[e] = -(f * inv);
+      else A[e] = ldcg(A + e) - f * ldcg(A + (int64_t)c * n + j);
+    }
+    grid.sync();
+  }
+}
+
+// undo the row interchanges on the inverse's columns (reverse order)
+template <class T>
+__global__ void k_gj_unswap(T* A, int n, const int* swaps) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  T* row = A + r * n;
+  for (int c = n - 1; c >= 0; --c) {
+    const int p = swaps[c];
+    if (p != c) { T t = row[c]; row[c] = row[p]; row[p] = t; }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+template <class K>
+static int coop_grid(K kernel, int threads, size_t smem) {
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+  if (per < 1) per = 1;
+  if (per > 2) per = 2;
+  return per * skel_sm_count();
+}
+
+template <class T>
+static int cpqr_big_impl(void* W, int m, int n, int64_t ld, double eps, int min_rank, int resume,
+                         void* state, cudaStream_t st) {
+  if (!resume) {
+    int blocks = (n * 32 + 255) / 256;
+    if (blocks < 1) blocks = 1;
+    k_cpqr_big_init<T><<<blocks, 256, 0, st>>>((const T*)W, m, n, ld, state);
+    SKEL_TRY(cudaGetLastError());
+  }
+  if (m <= 0 || n <= 0) return 0;
+  int grid = coop_grid(k_cpqr_big<T>, 256, 0);
+  T* Wp = (T*)W;
+  void* args[] = {&Wp, &m, &n, &ld, &eps, &min_rank, &state};
+  SKEL_TRY(cudaLaunchCooperativeKernel((const void*)k_cpqr_big<T>, grid, 256, args, 0, st));
+  return 0;
+}
+
+template <class T>
+static int gj_impl(void* A, int n, double regularize, int32_t* status, void* scratch, cudaStream_t st) {
+  int grid = coop_grid(k_gj_coop<T>, 256, 0);
+  if (grid > 4096) grid = 4096;
+  unsigned char* p = (unsigned char*)scratch;
+  double* part_v = (double*)p;
+  int* part_i = (int*)(p + 4096 * sizeof(double));
+  T* colc = (T*)(p + 4096 * (sizeof(double) + sizeof(int)));
+  int* swaps = (int*)((unsigned char*)colc + (size_t)n * 16);
+  T* Ap = (T*)A;
+  void* args[] = {&Ap, &n, &regularize, &status, &part_v, &part_i, &colc, &swaps};
+  SKEL_TRY(cudaLaunchCooperativeKernel((const void*)k_gj_coop<T>, grid, 256, args, 0, st));
+  k_gj_unswap<T><<<(n + 127) / 128, 128, 0, st>>>(Ap, n, swaps);
+  return skel_last_error();
+}
+
+extern "C" {
+
+int64_t skel_big_state_bytes(int32_t n) {
+  return 256 + (int64_t)n * (3 * sizeof(double) + sizeof(int)) + 64;
+}
+
+int skel_big_target(const SkelSource* src, const SkelLevel* lv, int32_t box, int32_t side,
+                    const int32_t* nbr_box, const int32_t* nbr_pref, int32_t nnb, int32_t m,
+                    int32_t n, void* W, int64_t ld, int32_t field, void* stream) {
+  if (m <= 0 || n <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid((m + 127) / 128, (n + 63) / 64);
+  if (field == 0)
+    k_big_target<double><<<grid, 128, 0, st>>>(*src, *lv, box, side, nbr_box, nbr_pref, nnb, m,
+                                                (double*)W, ld);
+  else
+    k_big_target<zc><<<grid, 128, 0, st>>>(*src, *lv, box, side, nbr_box, nbr_pref, nnb, m, (zc*)W, ld);
+  return skel_last_error();
+}
+
+int skel_cpqr_big(void* W, int32_t m, int32_t n, int64_t ld, double eps, int32_t min_rank,
+                  int32_t resume, void* state, int32_t field, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  return field == 0 ? cpqr_big_impl<double>(W, m, n, ld, eps, min_rank, resume, state, st)
+                    : cpqr_big_impl<zc>(W, m, n, ld, eps, min_rank, resume, state, st);
+}
+
+int skel_big_interp(void* W, int32_t n, int64_t ld, void* state, int32_t min_rank, int32_t field,
+                    void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int blocks = (n + 63) / 64;
+  if (blocks < 1) blocks = 1;
+  if (field == 0) k_big_interp<double><<<blocks, 64, 0, st>>>((double*)W, n, ld, state, min_rank);
+  else k_big_interp<zc><<<blocks, 64, 0, st>>>((zc*)W, n, ld, state, min_rank);
+  return skel_last_error();
+}
+
+int skel_big_output(const SkelLevel* lv, int32_t box, int32_t side, const void* W, int64_t ld,
+                    const void* state, int32_t n, int32_t field, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = sizeof(int) * (size_t)(n > 0 ? n : 1);
+  const int blocks = 2 * skel_sm_count();
+  if (field == 0) {
+    SKEL_TRY(cudaFuncSetAttribute(k_big_output<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_big_output<double><<<blocks, 256, smem, st>>>(*lv, box, side, (const double*)W, ld, state, n);
+  } else {
+    SKEL_TRY(cudaFuncSetAttribute(k_big_output<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_big_output<zc><<<blocks, 256, smem, st>>>(*lv, box, side, (const zc*)W, ld, state, n);
+  }
+  return skel_last_error();
+}
+
+int skel_gemm_tn(int32_t m, int32_t n, int32_t k, const void* X, int64_t ldx, const void* A,
+                 int64_t lda, void* Y, int64_t ldy, int32_t field, void* stream) {
+  if (m <= 0 || n <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid((m + 63) / 64, (n + 63) / 64);
+  if (field == 0)
+    k_gemm_tn<double><<<grid, 256, 0, st>>>(m, n, k, (const double*)X, ldx, (const double*)A, lda,
+                                            (double*)Y, ldy);
+  else
+    k_gemm_tn<zc><<<grid, 256, 0, st>>>(m, n, k, (const zc*)X, ldx, (const zc*)A, lda, (zc*)Y, ldy);
+  return skel_last_error();
+}
+
+int skel_gemv(int32_t trans, int32_t m, int32_t n, const void* A, int64_t lda, const void* x, void* y,
+              int32_t field, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int rows = trans == 0 ? m : n * 32;
+  const int blocks = (rows + 255) / 256;
+  if (blocks <= 0) return 0;
+  if (field == 0)
+    k_gemv<double><<<blocks, 256, 0, st>>>(trans, m, n, (const double*)A, lda, (const double*)x, (double*)y);
+  else
+    k_gemv<zc><<<blocks, 256, 0, st>>>(trans, m, n, (const zc*)A, lda, (const zc*)x, (zc*)y);
+  return skel_last_error();
+}
+
+int skel_big_probe(int32_t m, int32_t n, const void* A, int64_t lda, const void* Ysk, int64_t ldy,
+                   const void* state, const void* v, void* u, void* z, int32_t field, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int bu = (n + 127) / 128, bz = (m + 127) / 128;
+  if (field == 0) {
+    k_probe_pv<double><<<bu, 128, 0, st>>>((const double*)Ysk, n, ldy, state, (const double*)v, (double*)u);
+    k_probe_z<double><<<bz, 128, 0, st>>>(m, n, (const double*)A, lda, state, (const double*)v,
+                                          (const double*)u, (double*)z);
+  } else {
+    k_probe_pv<zc><<<bu, 128, 0, st>>>((const zc*)Ysk, n, ldy, state, (const zc*)v, (zc*)u);
+    k_probe_z<zc><<<bz, 128, 0, st>>>(m, n, (const zc*)A, lda, state, (const zc*)v, (const zc*)u, (zc*)z);
+  }
+  return skel_last_error();
+}
+
+int64_t skel_gj_scratch_bytes(int32_t n) {
+  return 4096 * (int64_t)(sizeof(double) + sizeof(int)) + (int64_t)n * (16 + sizeof(int)) + 256;
+}
+
+// Shat^-1 in place for big K (status 1: exact zero pivot).  The caller zeroes
+// *status first.
+int skel_dense_inverse_big(void* A, int32_t n, double regularize, int32_t* status, int32_t field,
+                           void* scratch, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  return field == 0 ? gj_impl<double>(A, n, regularize, status, scratch, st)
+                    : gj_impl<zc>(A, n, regularize, status, scratch, st);
+}
+
+}  // extern "C"

@@ -340,14 +340,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
   }
 }
 
-// D = A(rd, cd) with the children's diagonal blocks zeroed (skel.py:344-348),
-// one CTA per box, both point sets staged in shared memory (SoA).
+// D = A(rd, cd) with the children's diagonal blocks zeroed (skel.py:344-348).
+// One CTA (or, for few big boxes, gridDim.y CTAs splitting the rows) per box;
+// column points staged in shared memory in chunks of `chunk`, each warp owns
+// a row and reads its point once from global memory.
 template <class T>
-__global__ void __launch_bounds__(128) k_assemble_D(const SkelSource S, const SkelLevel L, int max_n,
+__global__ void __launch_bounds__(128) k_assemble_D(const SkelSource S, const SkelLevel L, int chunk,
                                                     const int32_t* __restrict__ order) {
   extern __shared__ __align__(16) unsigned char smem[];
-  Pt* rp = reinterpret_cast<Pt*>(smem);
-  Pt* cpp = rp + max_n;
+  Pt* cpp = reinterpret_cast<Pt*>(smem);
   __shared__ int rsplit[SKEL_MAX_CHILD + 1], csplit[SKEL_MAX_CHILD + 1], nch_s;
   const int a = order ? order[blockIdx.x] : (int)blockIdx.x;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -368,35 +369,40 @@ __global__ void __launch_bounds__(128) k_assemble_D(const SkelSource S, const Sk
     }
     nch_s = nch;
   }
-  for (int i = tid; i < nr; i += nt) rp[i] = load_pt(S, L.rdofs[r0 + i]);
-  for (int j = tid; j < nc; j += nt) cpp[j] = load_pt(S, L.cdofs[c0 + j]);
-  __syncthreads();
-  const int nch = nch_s;
   T* D = reinterpret_cast<T*>(L.D) + L.d_off[a];
   const bool fast = sizeof(T) == sizeof(double) && S.kind == SKEL_SRC_BIE &&
                     S.equation == SKEL_EQ_LAPLACE && S.dim == 2 && !S.kr10 && S.curvature_limit;
   const double inv2pi = 1.0 / SKEL_TWO_PI, inv4pi = 1.0 / SKEL_FOUR_PI;
   const double tol2 = S.coincide_tol * S.coincide_tol;
-  for (int i = tid / 32; i < nr; i += nt / 32) {
-    const int ci = nch > 0 ? find_run(rsplit, nch + 1, i) : -1;
-    const Pt tp = rp[i];
-    for (int j = tid & 31; j < nc; j += 32) {
-      T v = T(0.0);
-      const bool zero = nch > 0 && ci == find_run(csplit, nch + 1, j);
-      if (!zero) {
-        if (fast) {
-          const Pt& sp = cpp[j];
-          const double dx = tp.x - sp.x, dy = tp.y - sp.y;
-          const double r2 = dx * dx + dy * dy;
-          double e = (dx * (sp.nx * sp.w * inv2pi) + dy * (sp.ny * sp.w * inv2pi)) / r2;
-          if (r2 < tol2) e = (-sp.kap * inv4pi) * sp.w;
-          if (tp.o == sp.o) e += S.identity_coef;
-          v = as_T<T>(e);
-        } else {
-          v = entry_A<T>(S, tp, cpp[j]);
+  const int nw = nt / 32, wid = tid / 32, lane = tid & 31;
+  for (int j0 = 0; j0 < nc; j0 += chunk) {
+    const int jn = min(chunk, nc - j0);
+    __syncthreads();
+    for (int j = tid; j < jn; j += nt) cpp[j] = load_pt(S, L.cdofs[c0 + j0 + j]);
+    __syncthreads();
+    const int nch = nch_s;
+    for (int i = blockIdx.y * nw + wid; i < nr; i += nw * gridDim.y) {
+      const int ci = nch > 0 ? find_run(rsplit, nch + 1, i) : -1;
+      const Pt tp = load_pt(S, L.rdofs[r0 + i]);
+      for (int jj = lane; jj < jn; jj += 32) {
+        const int j = j0 + jj;
+        T v = T(0.0);
+        const bool zero = nch > 0 && ci == find_run(csplit, nch + 1, j);
+        if (!zero) {
+          const Pt& sp = cpp[jj];
+          if (fast) {
+            const double dx = tp.x - sp.x, dy = tp.y - sp.y;
+            const double r2 = dx * dx + dy * dy;
+            double e = (dx * (sp.nx * sp.w * inv2pi) + dy * (sp.ny * sp.w * inv2pi)) / r2;
+            if (r2 < tol2) e = (-sp.kap * inv4pi) * sp.w;
+            if (tp.o == sp.o) e += S.identity_coef;
+            v = as_T<T>(e);
+          } else {
+            v = entry_A<T>(S, tp, sp);
+          }
         }
+        D[(int64_t)i * nc + j] = v;
       }
-      D[(int64_t)i * nc + j] = v;
     }
   }
 }
@@ -620,13 +626,23 @@ int skel_assemble_D(const SkelSource* src, const SkelLevel* lv, const int32_t* o
   if (nb <= 0) return 0;
   if (max_n < 1) max_n = 1;
   cudaStream_t st = (cudaStream_t)stream;
-  size_t smem = 2 * sizeof(Pt) * (size_t)max_n;
+  const int chunk = max_n < 512 ? max_n : 512;
+  size_t smem = sizeof(Pt) * (size_t)chunk;
+  // few big boxes (3D coarse levels): split each box's rows over CTAs
+  const int sms = skel_sm_count();
+  int gy = 1;
+  if (nb < 2 * sms && max_n > 64) {
+    gy = (2 * sms + nb - 1) / nb;
+    const int cap = (max_n + 31) / 32;
+    if (gy > cap) gy = cap;
+  }
+  dim3 grid(nb, gy);
   if (field == 0) {
     SKEL_TRY(cudaFuncSetAttribute(k_assemble_D<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_assemble_D<double><<<nb, 128, smem, st>>>(*src, *lv, max_n, order);
+    k_assemble_D<double><<<grid, 128, smem, st>>>(*src, *lv, chunk, order);
   } else {
     SKEL_TRY(cudaFuncSetAttribute(k_assemble_D<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_assemble_D<zc><<<nb, 128, smem, st>>>(*src, *lv, max_n, order);
+    k_assemble_D<zc><<<grid, 128, smem, st>>>(*src, *lv, chunk, order);
   }
   return skel_last_error();
 }

@@ -92,3 +92,82 @@ def id_fixed_precision(A, eps, min_rank=0) -> InterpDecomp:
 def id_rows(A, eps, min_rank=0) -> InterpDecomp:
     """Row ID: A ~ proj.T @ A[skel, :] (plain transpose, lowrank.py:164-166)."""
     return id_fixed_precision(np.asarray(A).T, eps, min_rank=min_rank)
+
+
+def _big_side(A):
+    """Upload an explicit matrix as a big-box side (column-major target)."""
+    from . import _bigbox
+    torch = _native.require_cuda()
+    A = _as_matrix(A)
+    m, n = A.shape
+    field = int(A.dtype.kind == "c")
+    tdt = _native.torch_dtype(field)
+    sd = _bigbox._Side(torch, m, n, tdt)
+    sd.W.copy_(torch.from_numpy(np.ascontiguousarray(A.T, dtype=np.complex128 if field else np.float64)
+                                ).reshape(-1).to("cuda"))
+    return torch, sd, field, tdt
+
+
+def _big_result(sd, field, min_rank):
+    """InterpDecomp from a big-box CPQR state (interp already applied)."""
+    from . import _bigbox
+    n = sd.n
+    st = sd.state_out
+    hdr = st[:4].cpu().view(_i32()).numpy()
+    r, pad = int(hdr[0]), int(hdr[2])
+    nb = st.numel() * 8
+    raw = st.cpu().numpy().view(np.uint8)
+    piv = raw[256 + 24 * n:256 + 28 * n].view(np.int32).astype(np.int64)
+    bigP = float(raw[32:40].view(np.float64)[0])       # BigState.bigP
+    W = sd.W_out.cpu().numpy().reshape(n, sd.ld_out)          # row q = column q of the target
+    dt = np.complex128 if field else np.float64
+    K = r + pad
+    P = np.zeros((K, n), dtype=dt)
+    for s in range(K):
+        P[s, piv[s]] = 1.0
+    for q in range(K, n):
+        P[:r, piv[q]] = W[piv[q], :r]
+    if bigP > 2.0:
+        warnings.warn(f"interpolation matrix entries reach {bigP:.3g} (> 2); "
+                      "pivoting quality degraded on this block", stacklevel=3)
+    del nb, _bigbox
+    return InterpDecomp(skel=piv[:K].copy(), proj=P, rank=K, achieved_error=float("nan"))
+
+
+def _i32():
+    import torch
+    return torch.int32
+
+
+def id_fixed_precision_large(A, eps, min_rank=0) -> InterpDecomp:
+    """id_fixed_precision for matrices too large for one CTA: the whole-GPU
+    cooperative CPQR of csrc/big.cu (same pivot / stop rules)."""
+    from . import _bigbox
+    if not 0 < eps < 1:
+        raise InvalidInput("eps must lie in (0, 1)")
+    torch, sd, field, _ = _big_side(A)
+    L = _native.lib()
+    st = _native.stream_ptr()
+    _bigbox._cpqr(L, sd.W, sd.m, sd.n, sd.m, eps, min_rank, 0, sd.state, field, st)
+    _native.check(L.skel_big_interp(_native.ptr(sd.W), sd.n, sd.m, _native.ptr(sd.state), min_rank,
+                                    field, st), "skel_big_interp")
+    return _big_result(sd, field, min_rank)
+
+
+def id_randomized(A, eps, oversampling=10, seed=0) -> InterpDecomp:
+    """Randomized ID (lowrank.py:186-231): Gaussian sketch with doubling,
+    5-probe check and deterministic fallback, on the GPU; the random numbers
+    are drawn from numpy's default_rng(seed) in the reference's order."""
+    from . import _bigbox
+    if not 0 < eps < 1:
+        raise InvalidInput("eps must lie in (0, 1)")
+    if oversampling != _bigbox.OVERSAMPLING:
+        raise InvalidInput("only the reference's oversampling (10) is supported")
+    torch, sd, field, tdt = _big_side(A)
+    L = _native.lib()
+    st = _native.stream_ptr()
+    _bigbox._randomized(torch, L, sd, eps, seed, field, tdt, st)
+    if sd.kind == "fixed":
+        _native.check(L.skel_big_interp(_native.ptr(sd.W), sd.n, sd.m, _native.ptr(sd.state), 0,
+                                        field, st), "skel_big_interp")
+    return _big_result(sd, field, 0)

@@ -500,7 +500,12 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         cls = (np.searchsorted(np.asarray(_W_CLASSES), wb, side="left") * 16
                + np.searchsorted(np.asarray(_M_CLASSES), need_m, side="left"))
         buckets = []
-        cls = np.where(own > 0, cls, -1)
+        # big boxes: targets the reference hands to id_randomized, or too
+        # large for one CTA -> one box at a time over the whole GPU (big.cu)
+        big = own > 0
+        big &= (_bigbox_randomized(m0, nr) | _bigbox_randomized(m1, nc)
+                | (need_n > _BIG_N) | (_level_smem_fixed_vec(need_n, field) > optin))
+        cls = np.where((own > 0) & ~big, cls, -1)
         for c in np.unique(cls[cls >= 0]):
             sel = np.nonzero(cls == c)[0]
             sel = sel[np.argsort(-wb[sel], kind="stable")].astype(np.int32)
@@ -573,6 +578,12 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
                                   f"skel_id_level (level {li})")
             if rec is not None:
                 recs.append(rec)
+        big_boxes = np.nonzero(big)[0]
+        if big_boxes.size:
+            from . import _bigbox
+            with _profile.timed("id_big", level=li):
+                _bigbox.run_boxes(desc, lvd, big_boxes, li, noff, nidx, nr, nc, neff, eps,
+                                  bool(equalize_ranks), seed, field)
         join(streams)
         if mine is not None:
             shard.all_reduce(kk)          # non-owned entries are zero on each rank
@@ -679,6 +690,17 @@ def _smem_optin():
                       "skel_device_query")
         _OPTIN = b.value
     return _OPTIN
+
+
+_BIG_N = 512                 # boxes wider than this take the whole-GPU path
+
+
+def _bigbox_randomized(m, n):
+    return m > np.maximum(4096, 4 * n + 256)        # skel.py:419-421
+
+
+def _level_smem_fixed_vec(n, field):
+    return _level_smem_fixed(np.asarray(n, dtype=np.int64), field)
 
 
 def _level_smem_fixed(max_n, field):

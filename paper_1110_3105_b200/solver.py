@@ -185,11 +185,23 @@ class FactoredInverse:
         return tot
 
 
+_BIG_TOP = 768          # top matrices above this size use the cooperative inverse
+
+
 def _invert_top(Sh, regularize, field):
     """Shat^-1 on the device (single CTA Gauss-Jordan); status 1 -> singular."""
     torch = _native.require_cuda()
     K = Sh.shape[0]
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    if K > _BIG_TOP:
+        # whole-GPU cooperative Gauss-Jordan (csrc/big.cu)
+        L = _native.lib()
+        scratch = torch.empty(int(L.skel_gj_scratch_bytes(K)) // 8 + 1, dtype=torch.float64,
+                              device="cuda")
+        _native.check(L.skel_dense_inverse_big(_native.ptr(Sh), K, float(regularize), _native.ptr(st),
+                                               field, _native.ptr(scratch), _native.stream_ptr()),
+                      "skel_dense_inverse_big")
+        return int(st.item()), 1.0
     rc = torch.zeros(1, dtype=torch.float64, device="cuda")
     scratch = torch.empty((K * K + 3 * K) * (2 if field else 1) + 1, dtype=torch.float64, device="cuda")
     _native.check(_native.lib().skel_dense_inverse(_native.ptr(Sh), None, None, K, float(regularize),

@@ -257,6 +257,8 @@ def main():
         "ellipse_16384_1e-12": lambda: ellipse_case(16384, 1e-12, 2),
         "cfie_2048_1e-9": lambda: cfie_case(2048, 1e-9, 2),
         "sphere_2000_1e-6": lambda: sphere_case(2000, 1e-6, 1),
+        # randomized IDs (m > max(4096, 4n + 256)) at the coarse levels
+        "sphere_10000_1e-6": lambda: sphere_case(10000, 1e-6, 1),
     }
     only = sys.argv[1:]
     for name, fn in jobs.items():

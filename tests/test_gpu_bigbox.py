@@ -1,0 +1,148 @@
+"""The whole-GPU big-box path (csrc/big.cu): cooperative CPQR against the
+oracle's pivoted QR, the randomized ID against the oracle's id_randomized on
+the same numpy generator, the cooperative top inverse, and the full 3D
+pipeline with every box forced through the big path (config-4 geometry,
+golden vectors from the live reference)."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+gpu = pytest.mark.gpu
+
+
+def _sk():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_1110_3105_b200 as sk
+    return sk
+
+
+def _decaying(m, n, seed, decay=0.7, cplx=False):
+    rng = np.random.default_rng(seed)
+    k = min(m, n)
+    U, _ = np.linalg.qr(rng.standard_normal((m, k)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, k)))
+    s = decay ** np.arange(k)
+    A = (U * s) @ V.T
+    if cplx:
+        A = A + 1j * ((U * s) @ np.roll(V, 1, axis=1).T)
+    return A
+
+
+def _id_err(A, skel, P):
+    return np.linalg.norm(A - A[:, skel] @ P) / np.linalg.norm(A)
+
+
+@gpu
+@pytest.mark.parametrize("m,n,eps,cplx", [(700, 300, 1e-9, False), (2000, 900, 1e-12, False),
+                                          (500, 200, 1e-9, True)])
+def test_big_cpqr_matches_oracle(m, n, eps, cplx):
+    sk = _sk()
+    A = _decaying(m, n, 3, cplx=cplx)
+    got = sk.id_fixed_precision_large(A, eps)
+    skel, P, k, _ = oracle.id_fixed(A, eps)
+    assert got.rank == k
+    np.testing.assert_array_equal(got.skel, skel)
+    # P = R11^-1 R12 with cond(R11) ~ 1/eps: entries agree to ~ u/eps
+    tol = max(1e-7, 50 * 2.2e-16 / eps) * max(1.0, np.abs(P).max())
+    np.testing.assert_allclose(got.proj, P, atol=tol)
+    assert _id_err(A, got.skel, got.proj) <= 10 * eps * np.sqrt(n)
+
+
+@gpu
+def test_big_cpqr_min_rank_padding():
+    sk = _sk()
+    A = _decaying(300, 120, 5, decay=0.3)
+    got = sk.id_fixed_precision_large(A, 1e-9, min_rank=60)
+    skel, P, k, _ = oracle.id_fixed(A, 1e-9, min_rank=60)
+    assert got.rank == k == 60
+    np.testing.assert_array_equal(np.sort(got.proj[:, got.skel], axis=None),
+                                  np.sort(np.eye(60), axis=None))
+
+
+@gpu
+@pytest.mark.parametrize("m,n,seed", [(5000, 300, 1), (6000, 400, 12345)])
+def test_randomized_id_matches_oracle(m, n, seed):
+    sk = _sk()
+    A = _decaying(m, n, seed, decay=0.8)
+    eps = 1e-9
+    got = sk.id_randomized(A, eps, seed=seed)
+    skel, P, k, _ = oracle.id_randomized(A, eps, seed=seed)
+    # same sketches (host generator), GEMM rounding only: same rank and set
+    assert abs(got.rank - k) <= 1
+    assert _id_err(A, got.skel, got.proj) <= 100 * eps
+
+
+@gpu
+@pytest.mark.parametrize("K,cplx", [(1000, False), (1500, False), (800, True)])
+def test_cooperative_top_inverse(K, cplx):
+    sk = _sk()
+    import torch
+    from paper_1110_3105_b200 import solver
+    rng = np.random.default_rng(K)
+    A = rng.standard_normal((K, K)) + (1j * rng.standard_normal((K, K)) if cplx else 0)
+    A = A + 4 * np.sqrt(K) * np.eye(K)
+    T = torch.from_numpy(np.ascontiguousarray(A)).to("cuda")
+    st, _ = solver._invert_top(T, 0.0, int(cplx))
+    assert st == 0 and K > solver._BIG_TOP
+    Ai = T.cpu().numpy()
+    err = np.linalg.norm(Ai @ A - np.eye(K)) / np.sqrt(K)
+    assert err < 1e-12, err
+    # exact singularity is reported, not inverted
+    Z = torch.zeros((K, K), dtype=T.dtype, device="cuda")
+    st, _ = solver._invert_top(Z, 0.0, int(cplx))
+    assert st == 1
+    assert sk is not None
+
+
+@gpu
+def test_sphere_all_boxes_through_big_path(golden, monkeypatch):
+    sk = _sk()
+    from paper_1110_3105_b200 import skel as skmod
+    monkeypatch.setattr(skmod, "_BIG_N", 0)
+    g = golden("sphere_2000_1e-6")
+    n = 2000
+    pts = sk.PointSet(oracle.fib_sphere(n), None, np.full(n, 4 * np.pi / n))
+    tree = sk.build_tree(pts, 64)
+    src = sk.KernelSource(sk.KernelSpec("laplace", 3), pts, tree.perm, diag=1.0)
+    cm = sk.compress_source(src, tree, 1e-6)
+    worst = max(int(np.abs(cm.levels[li].kr_counts - g[f"L{li}_kr"]).max())
+                for li in range(int(g["nlevels"])))
+    assert worst <= 2
+    fi = sk.factor(cm)
+    B = np.random.default_rng(0).standard_normal((n, 1))
+    X = sk.solve(fi, B)
+    err = np.linalg.norm(X - g["X"]) / np.linalg.norm(g["X"])
+    assert err <= 1e-5, err
+    res = np.linalg.norm(sk.bie.dense_matvec(src, X) - B) / np.linalg.norm(B)
+    assert res <= 1e-5, res
+
+
+@gpu
+def test_sphere_10000_randomized_levels(golden):
+    """Config-4 geometry at N = 10000: the coarse levels use the randomized
+    ID in the reference (m > max(4096, 4n + 256)) and here."""
+    sk = _sk()
+    try:
+        g = golden("sphere_10000_1e-6")
+    except FileNotFoundError:
+        pytest.skip("fixture not generated")
+    n = 10000
+    pts = sk.PointSet(oracle.fib_sphere(n), None, np.full(n, 4 * np.pi / n))
+    tree = sk.build_tree(pts, 64)
+    np.testing.assert_array_equal(tree.perm, g["perm"])
+    src = sk.KernelSource(sk.KernelSpec("laplace", 3), pts, tree.perm, diag=1.0)
+    cm = sk.compress_source(src, tree, 1e-6)
+    worst = max(int(np.abs(cm.levels[li].kr_counts - g[f"L{li}_kr"]).max())
+                for li in range(int(g["nlevels"])))
+    assert worst <= 2
+    fi = sk.factor(cm)
+    B = np.random.default_rng(0).standard_normal((n, 1))
+    X = sk.solve(fi, B)
+    err = np.linalg.norm(X - g["X"]) / np.linalg.norm(g["X"])
+    assert err <= 1e-5, err
+    res = np.linalg.norm(sk.bie.dense_matvec(src, X) - B) / np.linalg.norm(B)
+    assert res <= 1e-5, res
