@@ -255,6 +255,15 @@ int skel_big_probe(int32_t m, int32_t n, const void* A, int64_t lda, const void*
  * row-major matrix in place; *status (zeroed by the caller) = 1 on an exact
  * zero pivot.  scratch: skel_gj_scratch_bytes(n). */
 int64_t skel_gj_scratch_bytes(int32_t n);
+
+/* factor_node of ONE big box (n = nr = nc, k) over the whole GPU: cooperative
+ * inverses of D_eff and M = R D^-1 L, GEMMs for X, Rd, Ld, Dd
+ * (solver.py:224-262); status / rcond / outputs exactly as skel_factor_level.
+ * dd_off .. lam_off: the box's output offsets; work: skel_factor_big_bytes. */
+int64_t skel_factor_big_bytes(int32_t n, int32_t k, int32_t field);
+int skel_factor_big(const SkelFactorLevel* F, int32_t box, int32_t n, int32_t k, int64_t dd_off,
+                    int64_t ld_off, int64_t rd_off, int64_t lam_off, void* work, int64_t work_bytes,
+                    int32_t field, void* stream);
 int skel_dense_inverse_big(void* A, int32_t n, double regularize, int32_t* status, int32_t field,
                            void* scratch, void* stream);
 

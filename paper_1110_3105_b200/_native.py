@@ -104,9 +104,12 @@ _SIGS = {
     "skel_gemv": [c_i32, c_i32, c_i32, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp],
     "skel_big_probe": [c_i32, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp],
     "skel_gj_scratch_bytes": [c_i32],
+    "skel_factor_big_bytes": [c_i32, c_i32, c_i32],
+    "skel_factor_big": [_P(SkelFactorLevel), c_i32, c_i32, c_i32, c_i64, c_i64, c_i64, c_i64, c_vp,
+                        c_i64, c_i32, c_vp],
     "skel_dense_inverse_big": [c_vp, c_i32, c_f64, c_vp, c_i32, c_vp, c_vp],
 }
-_RESTYPE_I64 = {"skel_big_state_bytes", "skel_gj_scratch_bytes"}
+_RESTYPE_I64 = {"skel_big_state_bytes", "skel_gj_scratch_bytes", "skel_factor_big_bytes"}
 
 _lib = None
 
@@ -116,7 +119,7 @@ _LAUNCHING = {"skel_id_level", "skel_assemble_D", "skel_assemble_S", "skel_eval_
               "skel_sweep_down_ex", "skel_dense_apply", "skel_permute_rows",
               "skel_compact_i32", "skel_dense_matvec", "skel_fp64_probe", "skel_big_target",
               "skel_cpqr_big", "skel_big_interp", "skel_big_output", "skel_gemm_tn", "skel_gemv",
-              "skel_big_probe", "skel_dense_inverse_big"}
+              "skel_big_probe", "skel_dense_inverse_big", "skel_factor_big"}
 launch_count = [0]
 
 

@@ -438,8 +438,9 @@ __global__ void k_probe_z(int m, int n, const T* __restrict__ A, int64_t lda, co
 template <class T>
 __global__ void __launch_bounds__(256)
     k_gj_coop(T* A, int n, double regularize, int32_t* status, double* part_v, int* part_i,
-              T* colc, int* swaps) {
+              T* colc, int* swaps, const int32_t* skip) {
   cg::grid_group grid = cg::this_grid();
+  if (skip && *skip) return;           // an earlier step of the same box failed
   __shared__ double sv[8];
   __shared__ int si[8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -513,14 +514,159 @@ __global__ void __launch_bounds__(256)
 
 // undo the row interchanges on the inverse's columns (reverse order)
 template <class T>
-__global__ void k_gj_unswap(T* A, int n, const int* swaps) {
+__global__ void k_gj_unswap(T* A, int n, const int* swaps, const int32_t* status) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
+  if (r >= n || *status) return;
   T* row = A + r * n;
   for (int c = n - 1; c >= 0; --c) {
     const int p = swaps[c];
     if (p != c) { T t = row[c]; row[c] = row[p]; row[p] = t; }
   }
+}
+
+// ---------------------------------------------------------------------------
+// big-box factor_node (solver.py:224-262) over the whole GPU: D_eff gather,
+// cooperative inverses of D and M = R D^-1 L, row-major GEMMs for the rest
+
+// C (m x n) = alpha A (m x k) B (k x n) + beta Cin, row-major; skipped when *flag
+template <class T>
+__global__ void __launch_bounds__(256)
+    k_gemm_rm(int m, int n, int k, double alpha, const T* __restrict__ A, int64_t lda,
+              const T* __restrict__ B, int64_t ldb, double beta, const T* Cin, int64_t ldcin, T* C,
+              int64_t ldc, const int32_t* flag, int nflag) {
+  if (flag) {
+    for (int q = 0; q < nflag; ++q)
+      if (flag[q]) return;
+  }
+  __shared__ T as[16][65];
+  __shared__ T bs[16][65];
+  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  T acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int w = 0; w < 4; ++w) acc[u][w] = T(0.0);
+  for (int k0 = 0; k0 < k; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int kk = e & 15, rr = e >> 4;         // A: 64 rows x 16 k (k fastest)
+      const int i = r0 + rr, kq = k0 + kk;
+      as[kk][rr] = (i < m && kq < k) ? A[(int64_t)i * lda + kq] : T(0.0);
+      const int cc = e & 63, kb = e >> 6;         // B: 16 k x 64 cols (cols fastest)
+      const int j = c0 + cc, kr = k0 + kb;
+      bs[kb][cc] = (j < n && kr < k) ? B[(int64_t)kr * ldb + j] : T(0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      T ar[4], br[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { ar[u] = as[kk][ty * 4 + u]; br[u] = bs[kk][tx * 4 + u]; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) acc[u][w] += ar[u] * br[w];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int i = r0 + ty * 4 + u, j = c0 + tx * 4 + w;
+      if (i < m && j < n) {
+        T v = acc[u][w] * alpha;
+        if (beta != 0.0) v += Cin[(int64_t)i * ldcin + j] * beta;
+        C[(int64_t)i * ldc + j] = v;
+      }
+    }
+}
+
+// A = D (+ children Lambda on the diagonal blocks) (+ regularize I); also
+// copies L, R of the box into the workspace
+template <class T>
+__global__ void k_fb_gather(const SkelFactorLevel F, int a, int n, int k, T* A, T* Lw, T* Rw) {
+  const T* D = reinterpret_cast<const T*>(F.D) + F.d_off[a];
+  const T* Lg = reinterpret_cast<const T*>(F.L) + F.l_off[a];
+  const T* Rg = reinterpret_cast<const T*>(F.R) + F.r_off[a];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = tid; e < (int64_t)n * n; e += nt) A[e] = D[e];
+  for (int64_t e = tid; e < (int64_t)n * k; e += nt) { Lw[e] = Lg[e]; Rw[e] = Rg[e]; }
+}
+
+template <class T>
+__global__ void k_fb_diag(const SkelFactorLevel F, int a, int n, T* A) {
+  // children Lambda blocks (solver.py:226-233) and regularize; one block per child
+  if (F.child_off) {
+    const int64_t c0 = F.child_off[a], c1 = F.child_off[a + 1];
+    int ro = 0;
+    for (int64_t c = c0; c < c1; ++c) {
+      const int kc = F.prev_k[c];
+      if (c - c0 == blockIdx.x) {
+        const T* lam = reinterpret_cast<const T*>(F.prev_lam) + F.prev_lam_off[c];
+        for (int e = threadIdx.x; e < kc * kc; e += blockDim.x) {
+          const int i = e / kc, j = e - i * kc;
+          A[(int64_t)(ro + i) * n + ro + j] = lam[e];
+        }
+      }
+      ro += kc;
+    }
+  }
+}
+
+template <class T>
+__global__ void k_add_diag(T* A, int n, double reg, const int32_t* flag) {
+  if (flag && *flag) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) A[(int64_t)i * n + i] += T(reg);
+}
+
+// column abs sums of a row-major m x n matrix (atomic partial sums per 64 rows)
+template <class T>
+__global__ void k_colabs(const T* A, int m, int n, double* colsum, const int32_t* flag) {
+  if (flag && *flag) return;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int i0 = blockIdx.y * 64, i1 = min(m, i0 + 64);
+  double s = 0.0;
+  for (int i = i0; i < i1; ++i) s += sk_abs(A[(int64_t)i * n + j]);
+  atomicAdd(colsum + j, s);
+}
+
+// status / rcond of the box from the column sums (slots: 0 nA, 1 nAi, 2 nM, 3 nMi)
+__global__ void k_fb_finish(const SkelFactorLevel F, int a, int n, int k, const double* cs,
+                            const int32_t* stD, const int32_t* stM) {
+  __shared__ double mx[4];
+  if (threadIdx.x < 4) mx[threadIdx.x] = 0.0;
+  __syncthreads();
+  const int len[4] = {n, n, k, k};
+  for (int q = 0; q < 4; ++q) {
+    double v = 0.0;
+    for (int j = threadIdx.x; j < len[q]; j += blockDim.x) v = fmax(v, cs[(int64_t)q * n + j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0)
+      atomicMax(reinterpret_cast<unsigned long long*>(mx + q), (unsigned long long)__double_as_longlong(v));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double nA = mx[0], nAi = mx[1], nM = mx[2], nMi = mx[3];
+    if (*stD) { F.status[a] = 1; F.rcond_d[a] = 0.0; F.rcond_m[a] = 0.0; return; }
+    const double rcd = (nA * nAi > 0.0) ? 1.0 / (nA * nAi) : 0.0;
+    if (*stM) { F.status[a] = 2; F.rcond_d[a] = rcd; F.rcond_m[a] = 0.0; return; }
+    F.status[a] = 0;
+    F.rcond_d[a] = rcd;
+    F.rcond_m[a] = k == 0 ? 1.0 : ((nM * nMi > 0.0) ? 1.0 / (nM * nMi) : 0.0);
+  }
+}
+
+template <class T>
+__global__ void k_copy_flag(T* dst, const T* src, int64_t cnt, const int32_t* flag) {
+  if (flag && (flag[0] || flag[1])) return;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = tid; e < cnt; e += nt) dst[e] = src[e];
 }
 
 // ---------------------------------------------------------------------------
@@ -553,7 +699,8 @@ static int cpqr_big_impl(void* W, int m, int n, int64_t ld, double eps, int min_
 }
 
 template <class T>
-static int gj_impl(void* A, int n, double regularize, int32_t* status, void* scratch, cudaStream_t st) {
+static int gj_impl(void* A, int n, double regularize, int32_t* status, void* scratch, cudaStream_t st,
+                   const int32_t* skip = nullptr) {
   int grid = coop_grid(k_gj_coop<T>, 256, 0);
   if (grid > 4096) grid = 4096;
   unsigned char* p = (unsigned char*)scratch;
@@ -562,9 +709,72 @@ static int gj_impl(void* A, int n, double regularize, int32_t* status, void* scr
   T* colc = (T*)(p + 4096 * (sizeof(double) + sizeof(int)));
   int* swaps = (int*)((unsigned char*)colc + (size_t)n * 16);
   T* Ap = (T*)A;
-  void* args[] = {&Ap, &n, &regularize, &status, &part_v, &part_i, &colc, &swaps};
+  void* args[] = {&Ap, &n, &regularize, &status, &part_v, &part_i, &colc, &swaps, &skip};
   SKEL_TRY(cudaLaunchCooperativeKernel((const void*)k_gj_coop<T>, grid, 256, args, 0, st));
-  k_gj_unswap<T><<<(n + 127) / 128, 128, 0, st>>>(Ap, n, swaps);
+  k_gj_unswap<T><<<(n + 127) / 128, 128, 0, st>>>(Ap, n, swaps, status);
+  return skel_last_error();
+}
+
+template <class T>
+static int gemm_rm(int m, int n, int k, double alpha, const T* A, int64_t lda, const T* B, int64_t ldb,
+                   double beta, const T* Cin, int64_t ldcin, T* C, int64_t ldc, const int32_t* flag,
+                   int nflag, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return 0;
+  dim3 grid((n + 63) / 64, (m + 63) / 64);
+  k_gemm_rm<T><<<grid, 256, 0, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, Cin, ldcin, C, ldc, flag,
+                                     nflag);
+  return skel_last_error();
+}
+
+template <class T>
+static int factor_big_impl(const SkelFactorLevel* F, int a, int n, int k, int64_t dd_off,
+                           int64_t ld_off, int64_t rd_off, int64_t lam_off, void* work, int64_t wbytes,
+                           cudaStream_t st) {
+  // workspace: flags(2 int, padded) | colsums 4n doubles | gj scratch | A n^2 | L nk | R kn | X nk | Y kn | M k^2
+  unsigned char* p = (unsigned char*)work;
+  int32_t* flags = (int32_t*)p;                        // [0] D singular, [1] Lambda singular
+  double* cs = (double*)(p + 64);
+  unsigned char* gjs = p + 64 + 4 * (size_t)n * sizeof(double);
+  const size_t gjb = ((size_t)skel_gj_scratch_bytes(n) + 255) / 256 * 256;
+  T* A = (T*)(gjs + gjb);
+  T* Lw = A + (size_t)n * n;
+  T* Rw = Lw + (size_t)n * k;
+  T* X = Rw + (size_t)k * n;
+  T* Y = X + (size_t)n * k;
+  T* M = Y + (size_t)k * n;
+  const size_t need = (size_t)((unsigned char*)(M + (size_t)k * k) - p);
+  if ((size_t)wbytes < need) return -2;
+  SKEL_TRY(cudaMemsetAsync(work, 0, 64 + 4 * (size_t)n * sizeof(double), st));
+  const int sms = skel_sm_count();
+  k_fb_gather<T><<<2 * sms, 256, 0, st>>>(*F, a, n, k, A, Lw, Rw);
+  if (F->child_off) k_fb_diag<T><<<8, 256, 0, st>>>(*F, a, n, A);
+  if (F->regularize != 0.0) k_add_diag<T><<<(n + 255) / 256, 256, 0, st>>>(A, n, F->regularize, nullptr);
+  dim3 gcs((n + 127) / 128, (n + 63) / 64);
+  k_colabs<T><<<gcs, 128, 0, st>>>(A, n, n, cs, nullptr);
+  int rc = gj_impl<T>(A, n, 0.0, flags, gjs, st);
+  if (rc) return rc;
+  k_colabs<T><<<gcs, 128, 0, st>>>(A, n, n, cs + n, flags);
+  T* Dd = reinterpret_cast<T*>(F->Dd);
+  if (k > 0) {
+    if ((rc = gemm_rm<T>(n, k, n, 1.0, A, n, Lw, k, 0.0, nullptr, 0, X, k, flags, 1, st))) return rc;   // X = D^-1 L
+    if ((rc = gemm_rm<T>(k, n, n, 1.0, Rw, n, A, n, 0.0, nullptr, 0, Y, n, flags, 1, st))) return rc;   // Y = R D^-1
+    if ((rc = gemm_rm<T>(k, k, n, 1.0, Rw, n, X, k, 0.0, nullptr, 0, M, k, flags, 1, st))) return rc;   // M = R X
+    dim3 gm((k + 127) / 128, (k + 63) / 64);
+    k_colabs<T><<<gm, 128, 0, st>>>(M, k, k, cs + 2 * n, flags);
+    if (F->regularize != 0.0) k_add_diag<T><<<(k + 255) / 256, 256, 0, st>>>(M, k, F->regularize, flags);
+    if ((rc = gj_impl<T>(M, k, 0.0, flags + 1, gjs, st, flags))) return rc;
+    k_colabs<T><<<gm, 128, 0, st>>>(M, k, k, cs + 3 * n, flags);
+    T* Rd = reinterpret_cast<T*>(F->Rd) + rd_off;
+    T* Ld = reinterpret_cast<T*>(F->Ld) + ld_off;
+    // Rd = Lam Y, Ld = X Lam, Dd = D^-1 - X Rd (the flag covers both singular cases)
+    if ((rc = gemm_rm<T>(k, n, k, 1.0, M, k, Y, n, 0.0, nullptr, 0, Rd, n, flags, 2, st))) return rc;
+    if ((rc = gemm_rm<T>(n, k, k, 1.0, X, k, M, k, 0.0, nullptr, 0, Ld, k, flags, 2, st))) return rc;
+    if ((rc = gemm_rm<T>(n, n, k, -1.0, X, k, Rd, n, 1.0, A, n, Dd + dd_off, n, flags, 2, st))) return rc;
+    k_copy_flag<T><<<sms, 256, 0, st>>>(reinterpret_cast<T*>(F->Lam) + lam_off, M, (int64_t)k * k, flags);
+  } else {
+    k_copy_flag<T><<<sms, 256, 0, st>>>(Dd + dd_off, A, (int64_t)n * n, flags);
+  }
+  k_fb_finish<<<1, 256, 0, st>>>(*F, a, n, k, cs, flags, flags + 1);
   return skel_last_error();
 }
 
@@ -673,6 +883,24 @@ int skel_dense_inverse_big(void* A, int32_t n, double regularize, int32_t* statu
   cudaStream_t st = (cudaStream_t)stream;
   return field == 0 ? gj_impl<double>(A, n, regularize, status, scratch, st)
                     : gj_impl<zc>(A, n, regularize, status, scratch, st);
+}
+
+int64_t skel_factor_big_bytes(int32_t n, int32_t k, int32_t field) {
+  const int64_t el = field ? 16 : 8;
+  const int64_t gjb = (skel_gj_scratch_bytes(n) + 255) / 256 * 256;
+  return 64 + 4 * (int64_t)n * 8 + gjb + el * ((int64_t)n * n + 4 * (int64_t)n * k + (int64_t)k * k) + 256;
+}
+
+// factor_node of ONE big box over the whole GPU (status / rcond / outputs as
+// skel_factor_level); the box's output offsets are passed by the host.
+int skel_factor_big(const SkelFactorLevel* F, int32_t box, int32_t n, int32_t k, int64_t dd_off,
+                    int64_t ld_off, int64_t rd_off, int64_t lam_off, void* work, int64_t work_bytes,
+                    int32_t field, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  return field == 0 ? factor_big_impl<double>(F, box, n, k, dd_off, ld_off, rd_off, lam_off, work,
+                                              work_bytes, st)
+                    : factor_big_impl<zc>(F, box, n, k, dd_off, ld_off, rd_off, lam_off, work,
+                                          work_bytes, st);
 }
 
 }  // extern "C"

@@ -20,6 +20,7 @@ from ._staging import Packer, fork, join
 from .skel import CompressedMatrix, _dense_apply, _nullctx, _off
 
 _RCOND_WARN = 1e-14
+_BIG_FAC_N = 768          # boxes at least this wide are factored over the whole GPU
 # per-box shared-memory need classes (bytes) -> one launch each
 _FAC_CLASSES = (24 << 10, 48 << 10, 80 << 10, 112 << 10, 160 << 10, 224 << 10)
 
@@ -248,9 +249,11 @@ class FactorRun:
         dd_off, ld_off, lam_off = _off(n_own * n_own), _off(n_own * k), _off(k * k)
         need = (n * n + 4 * n * k + k * k + 3 * n) * elem
         cls = np.searchsorted(np.asarray(_FAC_CLASSES), need, side="left")
+        # big boxes (3D coarse levels): one box at a time over the whole GPU
+        big = n_own >= _BIG_FAC_N
         buckets = []
-        for c in np.unique(cls[n_own > 0]):
-            sel = np.nonzero((cls == c) & (n_own > 0))[0]
+        for c in np.unique(cls[(n_own > 0) & ~big]):
+            sel = np.nonzero((cls == c) & (n_own > 0) & ~big)[0]
             buckets.append(sel[np.argsort(-need[sel], kind="stable")].astype(np.int32))
         p = dl.p
         outer = torch.cuda.stream(self.stream) if self.stream is not None else _nullctx()
@@ -310,6 +313,15 @@ class FactorRun:
                     rec.flops = float((2 * nf[b_] ** 3 + 6 * nf[b_] ** 2 * kf[b_]
                                        + 6 * kf[b_] ** 2 * nf[b_] + 2 * kf[b_] ** 3).sum())
                     rec.nbytes = float(((nf[b_] ** 2 + 2 * nf[b_] * kf[b_]) * 2 + kf[b_] ** 2).sum()) * elem
+            for a in np.nonzero(big)[0]:
+                na, ka = int(n[a]), int(k[a])
+                wb = int(L.skel_factor_big_bytes(na, ka, field))
+                # allocated on this (the launching) stream: reuse is stream-ordered
+                work = torch.empty(wb // 8 + 1, dtype=torch.float64, device=dev)
+                with _profile.timed("factor_big", level=li):
+                    _native.check(L.skel_factor_big(F, int(a), na, ka, int(dd_off[a]), int(ld_off[a]),
+                                                    int(ld_off[a]), int(lam_off[a]), p_(work), wb, field,
+                                                    _native.stream_ptr()), f"skel_factor_big ({li})")
             if streams:
                 join(streams)
             if gather_lam:

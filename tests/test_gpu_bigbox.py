@@ -102,7 +102,9 @@ def test_cooperative_top_inverse(K, cplx):
 def test_sphere_all_boxes_through_big_path(golden, monkeypatch):
     sk = _sk()
     from paper_1110_3105_b200 import skel as skmod
+    from paper_1110_3105_b200 import solver
     monkeypatch.setattr(skmod, "_BIG_N", 0)
+    monkeypatch.setattr(solver, "_BIG_FAC_N", 1)
     g = golden("sphere_2000_1e-6")
     n = 2000
     pts = sk.PointSet(oracle.fib_sphere(n), None, np.full(n, 4 * np.pi / n))
@@ -146,3 +148,45 @@ def test_sphere_10000_randomized_levels(golden):
     assert err <= 1e-5, err
     res = np.linalg.norm(sk.bie.dense_matvec(src, X) - B) / np.linalg.norm(B)
     assert res <= 1e-5, res
+
+
+@gpu
+def test_big_factor_synthetic_and_singular(monkeypatch):
+    """skel_factor_big (whole-GPU factor_node) on every box: inverse of the
+    one-level synthetic system, SingularBlock for a zero D, regularize."""
+    sk = _sk()
+    from paper_1110_3105_b200 import solver
+    import test_gpu_parity as tp
+    monkeypatch.setattr(solver, "_BIG_FAC_N", 1)
+    cm, A = tp._one_level_synthetic(sk, seed=3, sizes=(40, 35, 45), k=4)
+    fi = sk.factor(cm)
+    b = np.random.default_rng(5).standard_normal(A.shape[0])
+    x = sk.solve(fi, b)
+    xd = np.linalg.solve(A, b)
+    assert np.linalg.norm(x - xd) / np.linalg.norm(xd) <= 1e-10
+    cm, _ = tp._one_level_synthetic(sk, seed=1, sizes=(8, 8), k=2)
+    cm.levels[0].nodes[1].D[:] = 0.0
+    with pytest.raises(sk.SingularBlock) as exc:
+        sk.factor(cm)
+    assert exc.value.level == 1 and exc.value.node == 1 and exc.value.what == "D"
+    cm2, _ = tp._one_level_synthetic(sk, seed=1, sizes=(8, 8), k=2)
+    cm2.levels[0].nodes[1].D[:] = 0.0
+    assert sk.factor(cm2, regularize=1e-8) is not None
+
+
+@gpu
+def test_big_factor_matches_per_box_kernel(monkeypatch):
+    """Ellipse N = 1024 (golden blocks from the reference): factor blocks of
+    the whole-GPU path against the reference's Dd / Ld / Rd / Lambda."""
+    sk = _sk()
+    from paper_1110_3105_b200 import solver
+    import test_gpu_parity as tp
+    monkeypatch.setattr(solver, "_BIG_FAC_N", 1)
+    from conftest import GOLDEN
+    g = dict(np.load(GOLDEN + "/ellipse_1024_1e-9_full.npz"))
+    system, tree, cm, fi, B, X = tp._ellipse_gpu(sk, 1024, 1e-9, 3)
+    err = np.linalg.norm(X - g["X"]) / np.linalg.norm(g["X"])
+    assert err <= 1e-8, err
+    for li, lv in enumerate(fi.levels):
+        Lam = np.concatenate([nd.Lam.ravel() for nd in lv.nodes])
+        np.testing.assert_allclose(Lam, g[f"L{li}_Lam"], atol=1e-7 * np.abs(g[f"L{li}_Lam"]).max())

@@ -48,6 +48,62 @@ def config4(n=40000):
     report(f"config4 N={n}", tree, src, cm, fi, B, tc, tf)
 
 
+def profile_big(n=40000):
+    """Attribute config-4 compress time to the big-box pieces (synchronising)."""
+    import collections
+    from paper_1110_3105_b200 import _bigbox, skel as skmod
+    acc = collections.defaultdict(float)
+    cnt = collections.Counter()
+
+    def wrap(name, fn):
+        def f(*a, **k):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            r = fn(*a, **k)
+            torch.cuda.synchronize()
+            acc[name] += time.perf_counter() - t
+            cnt[name] += 1
+            return r
+        return f
+    _bigbox._cpqr = wrap("cpqr", _bigbox._cpqr)
+    _bigbox._norm_estimate = wrap("norm_est", _bigbox._norm_estimate)
+    _bigbox._randomized = wrap("randomized(total)", _bigbox._randomized)
+    _bigbox.run_boxes = wrap("run_boxes(total)", _bigbox.run_boxes)
+    orig_rng = np.random.default_rng
+
+    class R:
+        def __init__(self, s):
+            self.g = orig_rng(s)
+
+        def standard_normal(self, *a):
+            t = time.perf_counter()
+            r = self.g.standard_normal(*a)
+            acc["rng"] += time.perf_counter() - t
+            return r
+    _bigbox.np = type("npshim", (), {"random": type("r", (), {"default_rng": R}),
+                                      "__getattr__": lambda s, k: getattr(np, k)})()
+    for k in dir(np):
+        if not k.startswith("_") and k != "random":
+            try:
+                setattr(_bigbox.np, k, getattr(np, k))
+            except Exception:
+                pass
+    _profile.reset()
+    _profile.enabled = True
+    config4(n)
+    _profile.enabled = False
+    for r in _profile.records:
+        if r.kind in ("level", "id_level", "assemble_D", "id_big", "factor_level"):
+            m = {k: (v.size if hasattr(v, "size") else v) for k, v in r.meta.items()}
+            print(f"  {r.kind:12s} {r.ms():9.2f} ms  {m}")
+    for k in sorted(acc, key=lambda k: -acc[k]):
+        print(f"  {k:20s} {acc[k]:8.3f} s  x{cnt[k]}")
+
+
+if __name__ == "__main__" and sys.argv[1] == "prof":
+    profile_big(int(sys.argv[2]) if len(sys.argv) > 2 else 40000)
+    sys.exit(0)
+
 if __name__ == "__main__":
     which = sys.argv[1]
     n = int(sys.argv[2]) if len(sys.argv) > 2 else None
