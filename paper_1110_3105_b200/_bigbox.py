@@ -15,6 +15,7 @@ import numpy as np
 from . import _native
 
 RANDOMIZED_CUTOFF = 4096        # skel.py:33
+_WINDOW = 4                     # randomized sides whose host streams run ahead
 OVERSAMPLING = 10               # lowrank.py:186
 
 
@@ -66,12 +67,91 @@ def _cpqr(L, W, m, n, ld, eps, min_rank, resume, state, field, st):
                                   _native.ptr(state), field, st), "skel_cpqr_big")
 
 
-def _norm_estimate(torch, L, sd, rng, cplx, tdt, field, st, iters=8):
-    """lowrank.py:169-183 with the GEMVs on the device."""
+class SketchStream:
+    """The host random stream of one randomized side, in the reference's draw
+    order (lowrank.py:169-231): the norm-estimate vector, then Omega_20,
+    Omega_40, ... (doubling), then the five probe vectors.  A worker thread
+    draws the sketches ahead into pinned host memory (up to the expected
+    final size, further on demand) so the host generator overlaps the GPU;
+    the probe vectors are drawn from the generator state saved right after
+    the last sketch actually used."""
+
+    def __init__(self, seed, m, n, cplx, expect_rank=None):
+        import threading
+        self.rng = np.random.default_rng(seed)
+        self.m, self.n, self.cplx = m, n, cplx
+        self.v0 = self._draw(n)
+        self.ready = {}
+        self.cv = threading.Condition()
+        self.stopped = False
+        self.want = 0
+        k = n // 2 if expect_rank is None else expect_rank
+        self.target = 2 * OVERSAMPLING
+        while self.target < k + OVERSAMPLING:
+            self.target *= 2
+        self.last_state = None
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    def _draw(self, shape):
+        x = self.rng.standard_normal(shape)
+        if self.cplx:
+            x = x + 1j * self.rng.standard_normal(shape)
+        return x
+
+    def _run(self):
+        import copy
+        torch = _native.require_cuda()
+        ell = 2 * OVERSAMPLING
+        while ell < self.m:
+            with self.cv:
+                while not self.stopped and ell > self.target and self.want < ell:
+                    self.cv.wait()
+                if self.stopped:
+                    return
+            dt = np.complex128 if self.cplx else np.float64
+            host = torch.empty((ell, self.m), dtype=torch.complex128 if self.cplx else torch.float64,
+                               pin_memory=True)
+            hv = host.numpy()
+            if self.cplx:
+                hv[...] = self._draw((ell, self.m))
+            else:
+                self.rng.standard_normal((ell, self.m), out=hv)
+            state = copy.deepcopy(self.rng.bit_generator.state)
+            with self.cv:
+                self.ready[ell] = (host, state)
+                self.cv.notify_all()
+            del dt
+            ell *= 2
+
+    def sketch(self, ell):
+        """Omega_ell (pinned CPU tensor, ell x m); records the state after it."""
+        with self.cv:
+            self.want = max(self.want, ell)
+            self.cv.notify_all()
+            while ell not in self.ready:
+                self.cv.wait()
+            host, state = self.ready.pop(ell)
+        self.last_state = state
+        return host
+
+    def probe_rng(self):
+        self.stop()
+        g = np.random.Generator(np.random.PCG64())
+        g.bit_generator.state = self.last_state
+        return g
+
+    def stop(self):
+        with self.cv:
+            self.stopped = True
+            self.ready.clear()
+            self.cv.notify_all()
+
+
+def _norm_estimate(torch, L, sd, v, cplx, tdt, field, st, iters=8):
+    """lowrank.py:169-183 with the GEMVs on the device (v: the stream's
+    first draw)."""
     n, m = sd.n, sd.m
-    v = rng.standard_normal(n)
-    if cplx:
-        v = v + 1j * rng.standard_normal(n)
     v = v / np.linalg.norm(v)
     s = 0.0
     vd = _vec(torch, v, tdt)
@@ -90,13 +170,21 @@ def _norm_estimate(torch, L, sd, rng, cplx, tdt, field, st, iters=8):
     return float(s)
 
 
-def _randomized(torch, L, sd, eps, seed, field, tdt, st):
+def _randomized(torch, L, sd, eps, seed, field, tdt, st, stream=None):
     """id_randomized (lowrank.py:186-231) on the side's target; falls back
     to the deterministic CPQR exactly where the reference does."""
     m, n = sd.m, sd.n
     cplx = bool(field)
-    rng = np.random.default_rng(seed)
-    normA = _norm_estimate(torch, L, sd, rng, cplx, tdt, field, st)
+    ss = stream if stream is not None else SketchStream(seed, m, n, cplx)
+    try:
+        _randomized_body(torch, L, sd, eps, ss, field, tdt, st, cplx)
+    finally:
+        ss.stop()
+
+
+def _randomized_body(torch, L, sd, eps, ss, field, tdt, st, cplx):
+    m, n = sd.m, sd.n
+    normA = _norm_estimate(torch, L, sd, ss.v0, cplx, tdt, field, st)
     if normA == 0.0:
         _cpqr(L, sd.W, m, n, m, eps, 0, 0, sd.state, field, st)      # rank 0, empty ID
         return
@@ -105,10 +193,9 @@ def _randomized(torch, L, sd, eps, seed, field, tdt, st):
         if ell >= m:
             _cpqr(L, sd.W, m, n, m, eps, 0, 0, sd.state, field, st)
             return
-        Om = rng.standard_normal((ell, m))
-        if cplx:
-            Om = Om + 1j * rng.standard_normal((ell, m))
-        X = _vec(torch, Om, tdt)                     # (ell, m) row-major = m x ell column-major
+        host = ss.sketch(ell)
+        X = torch.empty((ell, m), dtype=tdt, device="cuda")
+        X.copy_(host, non_blocking=True)             # (ell, m) row-major = m x ell column-major
         Y = torch.empty(ell * n, dtype=tdt, device="cuda")
         _native.check(L.skel_gemm_tn(ell, n, m, _native.ptr(X), m, _native.ptr(sd.W), m,
                                      _native.ptr(Y), ell, field, st), "skel_gemm_tn")
@@ -123,6 +210,7 @@ def _randomized(torch, L, sd, eps, seed, field, tdt, st):
     worst = 0.0
     u = torch.empty(max(rank, 1), dtype=tdt, device="cuda")
     z = torch.empty(m, dtype=tdt, device="cuda")
+    rng = ss.probe_rng()
     for _ in range(5):
         v = rng.standard_normal(n)
         if cplx:
@@ -147,6 +235,25 @@ def run_boxes(desc, lvd, boxes, li, noff, nidx, nr, nc, neff, eps, equalize, see
     L = _native.lib()
     st = _native.stream_ptr()
     tdt = _native.torch_dtype(field)
+    # host random streams of the randomized sides, started WINDOW sides ahead
+    plan = []
+    for a in boxes:
+        a = int(a)
+        nb = nidx[noff[a]:noff[a + 1]]
+        for side, n in ((0, int(nr[a])), (1, int(nc[a]))):
+            m = int((nc[nb] if side == 0 else nr[nb]).sum() + neff[a])
+            if n > 0 and randomized(m, n):
+                plan.append((a, side, m, n))
+    streams = {}
+    expect = [None]
+    pos = [0]
+
+    def top_up():
+        while pos[0] < len(plan) and len(streams) < _WINDOW:
+            a_, s_, m_, n_ = plan[pos[0]]
+            streams[(a_, s_)] = SketchStream(sub_seed(seed, li, a_, s_), m_, n_, bool(field), expect[0])
+            pos[0] += 1
+    top_up()
     for a in boxes:
         a = int(a)
         nb = nidx[noff[a]:noff[a + 1]].astype(np.int32)
@@ -163,7 +270,10 @@ def run_boxes(desc, lvd, boxes, li, noff, nidx, nr, nc, neff, eps, equalize, see
                                                 _native.ptr(prefs[side]), int(nb.size), m, n,
                                                 _native.ptr(sd.W), m, field, st), "skel_big_target")
             if n > 0 and randomized(m, n):
-                _randomized(torch, L, sd, eps, sub_seed(seed, li, a, side), field, tdt, st)
+                ss = streams.pop((a, side))
+                _randomized(torch, L, sd, eps, sub_seed(seed, li, a, side), field, tdt, st, ss)
+                expect[0] = _rank_of(sd.state_out)
+                top_up()
             else:
                 _cpqr(L, sd.W, m, n, m, eps, 0, 0, sd.state, field, st)
             sides.append(sd)

@@ -138,147 +138,246 @@ __global__ void k_cpqr_big_init(const T* W, int m, int n, int64_t ld, void* buf)
   }
 }
 
+// One grid barrier per step.  Every CTA redundantly reduces the per-CTA
+// pivot candidates of the previous step (first maximum by position), applies
+// the stop rule and forms the reflector; the position -> column map is
+// double-buffered (CTA 0 writes the swapped copy for the next step) so no CTA
+// reads an entry another CTA is rewriting.  Phase B: one warp per trailing
+// position -- reflector, norm downdate / stale / renorm rules, exact
+// trailing norm, next-step candidate.
 template <class T>
 __global__ void __launch_bounds__(256)
-    k_cpqr_big(T* W, int m, int n, int64_t ld, double eps, int min_rank, void* buf) {
+    k_cpqr_big(T* W, int m, int n, int64_t ld, double eps, int min_rank, void* buf, int vsmem,
+               int* pivb, double* cand_v, int* cand_i) {
   cg::grid_group grid = cg::this_grid();
   BigView<T> v = big_view<T>(buf, n);
+  extern __shared__ __align__(16) unsigned char cp_smem[];
+  T* vs = reinterpret_cast<T*>(cp_smem);        // the reflector, when it fits
   __shared__ double sv[8];
   __shared__ int si[8];
+  __shared__ double red_v;
+  __shared__ int red_i;
+  const int G = gridDim.x;
   const int kmax = m < n ? m : n;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int tw = (gridDim.x * blockDim.x) >> 5;
   int s = ldcg(&v.st->rank);
+  double p0 = ldcg(&v.st->p0);
+  int* pcur = v.piv;
+  int* pnext = pivb;
+  // candidates for the first step: every CTA scans nrm[s..n) itself
+  {
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int c = s + threadIdx.x; c < n; c += blockDim.x) cmerge(bv, bi, ldcg(v.nrm + c), c);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      cmerge(bv, bi, ov, oi);
+    }
+    if (lane == 0) { sv[wid] = bv; si[wid] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = -1.0;
+      int j = 0x7fffffff;
+      for (int w = 0; w < nwb; ++w) cmerge(b, j, sv[w], si[w]);
+      red_v = b;
+      red_i = j;
+    }
+    __syncthreads();
+  }
+  double bsel = red_v;
+  int jsel = red_i;
+  int par = 0;
   while (s < kmax) {
-    // ---- phase A (CTA 0): first-maximum pivot, stop rule, swap, reflector
+    // ---- pivot + stop rule (identical on every CTA)
+    const int j = jsel;
+    int stop = 0;
+    if (j >= n) {
+      stop = 1;
+    } else {
+      const double pn = sqrt(fmax(bsel, 0.0));
+      if (s == 0) {
+        p0 = pn;
+        if (pn == 0.0) stop = 1;
+      }
+      if (!stop && ((s >= min_rank && pn <= eps * p0) || pn == 0.0)) stop = 1;
+    }
+    if (stop) break;
+    const int pc = ldcg(pcur + j);           // pivot column
+    const int ps_old = ldcg(pcur + s);
+    const double nrm_s_old = ldcg(v.nrm + s);
+    const double nx2 = ldcg(v.xn2 + j);
+    const T x0 = ldcg(W + (int64_t)pc * ld + s);
+    const double ax0 = sk_abs(x0);
+    const double normx = sqrt(nx2);
+    T phase = T(1.0);
+    if (ax0 != 0.0) phase = sk_unit_phase(x0, ax0);
+    const T alpha = -(phase * normx);
+    const double vv = 2.0 * normx * (normx + ax0);
+    const T v0 = x0 - alpha;
+    const double beta = vv > 0.0 ? 2.0 / vv : 0.0;
     if (blockIdx.x == 0) {
-      double bv = -1.0;
-      int bi = 0x7fffffff;
-      for (int c = s + threadIdx.x; c < n; c += blockDim.x) cmerge(bv, bi, ldcg(v.nrm + c), c);
+      // next step's position -> column map, with positions s and j swapped
+      for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        int col = ldcg(pcur + c);
+        if (c == s) col = pc;
+        else if (c == j) col = ps_old;
+        pnext[c] = col;
+      }
+      if (threadIdx.x == 0 && s == 0) v.st->p0 = p0;
+    }
+    // ---- phase B
+    const int s1 = s + 1;
+    const bool renorm = (s1 < kmax) && (s1 % 32 == 0);
+    const T* vcol = W + (int64_t)pc * ld;
+    if (vsmem) {
+      for (int i = s + threadIdx.x; i < m; i += blockDim.x) vs[i] = (i == s) ? v0 : ldcg(vcol + i);
+      __syncthreads();
+    }
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int c = s1 + gw; c < n; c += tw) {
+      const int col = (c == j) ? ps_old : ldcg(pcur + c);
+      T* wc = W + (int64_t)col * ld;
+      // 4 rows per lane per pass: independent loads in flight, 4 partial sums
+      T d4[4] = {T(0.0), T(0.0), T(0.0), T(0.0)};
+      for (int i0 = s; i0 < m; i0 += 128) {
+        T wv[4], vq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + lane + 32 * u;
+          wv[u] = i < m ? ldcg(wc + i) : T(0.0);
+          vq[u] = i < m ? (vsmem ? vs[i] : ((i == s) ? v0 : ldcg(vcol + i))) : T(0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) d4[u] += sk_conj(vq[u]) * wv[u];
+      }
+      T dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+      dot = warp_sum(dot);
+      const T f = dot * beta;
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
+      T row = T(0.0);
+      for (int i0 = s; i0 < m; i0 += 128) {
+        T wv[4], vq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + lane + 32 * u;
+          wv[u] = i < m ? ldcg(wc + i) : T(0.0);
+          vq[u] = i < m ? (vsmem ? vs[i] : ((i == s) ? v0 : ldcg(vcol + i))) : T(0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + lane + 32 * u;
+          if (i < m) {
+            T w = wv[u];
+            if (beta != 0.0) {
+              w -= vq[u] * f;
+              wc[i] = w;
+            }
+            if (i > s) a4[u] += sk_abs2(w);
+            if (i == s) row = w;
+          }
+        }
+      }
+      double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      acc = warp_sum(acc);
+      row = shfl(row, 0);
+      double t = ((c == j) ? nrm_s_old : ldcg(v.nrm + c)) - sk_abs2(row);
+      t = t > 0.0 ? t : 0.0;
+      if (renorm || t < 1e-8 * ldcg(v.ref + c)) {
+        t = acc;
+        if (lane == 0) v.ref[c] = acc;
+      }
+      if (lane == 0) {
+        v.nrm[c] = t;
+        v.xn2[c] = acc;
+      }
+      cmerge(bv, bi, t, c);
+    }
+    if (lane == 0) { sv[wid] = bv; si[wid] = bi; }
+    __syncthreads();
+    par ^= 1;
+    if (threadIdx.x == 0) {
+      double b = -1.0;
+      int jj = 0x7fffffff;
+      for (int w = 0; w < nwb; ++w) cmerge(b, jj, sv[w], si[w]);
+      cand_v[par * 4096 + blockIdx.x] = b;
+      cand_i[par * 4096 + blockIdx.x] = jj;
+    }
+    grid.sync();
+    // every CTA has read x0 of this step: the diagonal entry can be written
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      W[(int64_t)pc * ld + s] = alpha;
+      v.st->rank = s + 1;
+    }
+    // ---- reduce the candidates for the next step (warp 0 of every CTA)
+    if (wid == 0) {
+      double b = -1.0;
+      int jj = 0x7fffffff;
+      for (int q = lane; q < G; q += 32)
+        cmerge(b, jj, ldcg(cand_v + par * 4096 + q), ldcg(cand_i + par * 4096 + q));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        cmerge(bv, bi, ov, oi);
+        double ov = __shfl_xor_sync(0xffffffffu, b, o);
+        int oi = __shfl_xor_sync(0xffffffffu, jj, o);
+        cmerge(b, jj, ov, oi);
       }
-      if (lane == 0) { sv[wid] = bv; si[wid] = bi; }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double b = -1.0;
-        int j = 0x7fffffff;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) cmerge(b, j, sv[w], si[w]);
-        int stop = 0;
-        if (j >= n) {
-          stop = 1;
-        } else {
-          const double pn = sqrt(fmax(ldcg(v.nrm + j), 0.0));
-          if (s == 0) {
-            v.st->p0 = pn;
-            if (pn == 0.0) stop = 1;
-          }
-          const double p0 = s == 0 ? pn : ldcg(&v.st->p0);
-          if (!stop && ((s >= min_rank && pn <= eps * p0) || pn == 0.0)) stop = 1;
-        }
-        if (!stop) {
-          if (j != s) {
-            double t = ldcg(v.nrm + s); v.nrm[s] = ldcg(v.nrm + j); v.nrm[j] = t;
-            t = ldcg(v.xn2 + s); v.xn2[s] = ldcg(v.xn2 + j); v.xn2[j] = t;
-            int q = ldcg(v.piv + s); v.piv[s] = ldcg(v.piv + j); v.piv[j] = q;
-          }
-          const int pc = ldcg(v.piv + s);
-          const double nx2 = ldcg(v.xn2 + s);
-          const T x0 = ldcg(W + (int64_t)pc * ld + s);
-          const double ax0 = sk_abs(x0);
-          const double normx = sqrt(nx2);
-          T phase = T(1.0);
-          if (ax0 != 0.0) phase = sk_unit_phase(x0, ax0);
-          const T alpha = -(phase * normx);
-          const double vv = 2.0 * normx * (normx + ax0);
-          v.st->v0 = x0 - alpha;
-          v.st->alpha = alpha;
-          v.st->beta = vv > 0.0 ? 2.0 / vv : 0.0;
-          v.st->pc = pc;
-        }
-        v.st->stop = stop;
-      }
+      if (lane == 0) { red_v = b; red_i = jj; }
     }
-    grid.sync();
-    if (ldcg(&v.st->stop)) break;
-    // ---- phase B (all warps): reflector on every trailing column + norms
-    {
-      const int pc = ldcg(&v.st->pc);
-      const double beta = ldcg(&v.st->beta);
-      const T v0 = ldcg(&v.st->v0);
-      const int s1 = s + 1;
-      const bool renorm = (s1 < kmax) && (s1 % 32 == 0);
-      const T* vcol = W + (int64_t)pc * ld;
-      for (int c = s1 + gw; c < n; c += tw) {
-        T* wc = W + (int64_t)ldcg(v.piv + c) * ld;
-        T dot = T(0.0);
-        for (int i = s + lane; i < m; i += 32) {
-          const T vi = (i == s) ? v0 : ldcg(vcol + i);
-          dot += sk_conj(vi) * ldcg(wc + i);
-        }
-        dot = warp_sum(dot);
-        const T f = dot * beta;
-        double acc = 0.0;
-        T row = T(0.0);
-        for (int i = s + lane; i < m; i += 32) {
-          const T vi = (i == s) ? v0 : ldcg(vcol + i);
-          T w = ldcg(wc + i);
-          if (beta != 0.0) {
-            w -= vi * f;
-            wc[i] = w;
-          }
-          if (i > s) acc += sk_abs2(w);
-          if (i == s) row = w;
-        }
-        acc = warp_sum(acc);
-        row = shfl(row, 0);
-        if (lane == 0) {
-          double t = ldcg(v.nrm + c) - sk_abs2(row);
-          t = t > 0.0 ? t : 0.0;
-          const double rf = ldcg(v.ref + c);
-          if (renorm || t < 1e-8 * rf) { t = acc; v.ref[c] = acc; }
-          v.nrm[c] = t;
-          v.xn2[c] = acc;
-        }
-      }
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        W[(int64_t)pc * ld + s] = ldcg(&v.st->alpha);
-        v.st->rank = s + 1;
-      }
-    }
-    grid.sync();
+    __syncthreads();
+    bsel = red_v;
+    jsel = red_i;
+    int* t = pcur; pcur = pnext; pnext = t;
     ++s;
+  }
+  // the final map must live in v.piv
+  if (pcur != v.piv) {
+    grid.sync();
+    if (blockIdx.x == 0)
+      for (int c = threadIdx.x; c < n; c += blockDim.x) v.piv[c] = ldcg(pcur + c);
   }
 }
 
 // P = R11^-1 R12 in place (rows 0..r-1 of the non-pivot columns), max|P|,
-// padding count to min_rank (lowrank.py:122-161)
+// padding count to min_rank (lowrank.py:122-161).  One warp per column, the
+// column staged in shared memory; the back substitution runs in the same
+// (dtrsm, column-oriented) order as cpqr.cuh's interp_solve, with the
+// x[t] -= R[t,s] x[s] updates of one step spread over the lanes.
 template <class T>
-__global__ void k_big_interp(T* W, int n, int64_t ld, void* buf, int min_rank) {
+__global__ void __launch_bounds__(128) k_big_interp(T* W, int n, int64_t ld, void* buf, int min_rank) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   BigView<T> v = big_view<T>(buf, n);
   const int r = v.st->rank;
-  const int c = r + blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  T* xs = reinterpret_cast<T*>(smem_raw) + (size_t)wid * (r > 0 ? r : 1);
+  const int c = r + blockIdx.x * (blockDim.x >> 5) + wid;
   double big = 0.0;
-  if (c < n) {
+  if (c < n && r > 0) {
     T* x = W + (int64_t)v.piv[c] * ld;
+    for (int t = lane; t < r; t += 32) xs[t] = x[t];
+    __syncwarp();
     for (int s = r - 1; s >= 0; --s) {
-      T xs = x[s];
-      if (xs != T(0.0)) {
-        const T* rs = W + (int64_t)v.piv[s] * ld;
-        xs = xs / rs[s];
-        x[s] = xs;
-        for (int t = 0; t < s; ++t) x[t] -= rs[t] * xs;
+      T xv = xs[s];
+      if (xv != T(0.0)) {
+        const T* rs = W + (int64_t)v.piv[s] * ld;   // R[:, s]
+        xv = xv / rs[s];
+        __syncwarp();
+        if (lane == 0) xs[s] = xv;
+        for (int t = lane; t < s; t += 32) xs[t] -= rs[t] * xv;
       }
+      __syncwarp();
     }
-    for (int s = 0; s < r; ++s) big = fmax(big, sk_abs(x[s]));
+    for (int t = lane; t < r; t += 32) {
+      x[t] = xs[t];
+      big = fmax(big, sk_abs(xs[t]));
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) big = fmax(big, __shfl_xor_sync(0xffffffffu, big, o));
-  if ((threadIdx.x & 31) == 0 && big > 0.0)
+  if (lane == 0 && big > 0.0)
     atomicMax(reinterpret_cast<unsigned long long*>(&v.st->bigP), (unsigned long long)__double_as_longlong(big));
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const int kmin = min_rank < n ? min_rank : n;
@@ -382,6 +481,78 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// DMMA (mma.sync m8n8k4 f64) version of k_gemm_tn for real data: 64 x 64 CTA
+// tile, 4 warps of 32 x 32, K staged 16 deep in shared memory with cp.async
+// (double-buffered).  Both operands are contiguous along K in global memory
+// and in shared memory (row stride 20 doubles: conflict-free fragment loads).
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+#define TN_LDS 20
+__global__ void __launch_bounds__(128)
+    k_gemm_tn_dmma(int m, int n, int k, const double* __restrict__ X, int64_t ldx,
+                   const double* __restrict__ A, int64_t lda, double* Y, int64_t ldy) {
+  __shared__ __align__(16) double xs[2][64 * TN_LDS];
+  __shared__ __align__(16) double as[2][64 * TN_LDS];
+  const int r0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wr = (wid >> 1) * 32, wc = (wid & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  auto stage = [&](int buf, int k0) {
+    for (int e = threadIdx.x; e < 64 * 16; e += 128) {
+      const int kk = e & 15, rr = e >> 4;
+      const int i = k0 + kk;
+      double* dx = &xs[buf][rr * TN_LDS + kk];
+      double* da = &as[buf][rr * TN_LDS + kk];
+      if (i < k && r0 + rr < m) cp_async8(dx, X + (int64_t)(r0 + rr) * ldx + i); else *dx = 0.0;
+      if (i < k && c0 + rr < n) cp_async8(da, A + (int64_t)(c0 + rr) * lda + i); else *da = 0.0;
+    }
+    cp_async_commit();
+  };
+  const int nk = (k + 15) / 16;
+  stage(0, 0);
+  for (int t = 0; t < nk; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < nk) {
+      stage(buf ^ 1, (t + 1) * 16);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < 16; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) af[a] = xs[buf][(wr + a * 8 + (lane >> 2)) * TN_LDS + k4 + (lane & 3)];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = as[buf][(wc + b * 8 + (lane >> 2)) * TN_LDS + k4 + (lane & 3)];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = r0 + wr + a * 8 + (lane >> 2);
+        const int c = c0 + wc + b * 8 + 2 * (lane & 3) + h;
+        if (r < m && c < n) Y[(int64_t)c * ldy + r] = acc[a][b][h];
+      }
+}
+
 // y = A x (trans 0: thread per row) or y = A^H x (trans 1: warp per column)
 template <class T>
 __global__ void k_gemv(int trans, int m, int n, const T* __restrict__ A, int64_t lda,
@@ -439,22 +610,24 @@ template <class T>
 __global__ void __launch_bounds__(256)
     k_gj_coop(T* A, int n, double regularize, int32_t* status, double* part_v, int* part_i,
               T* colc, int* swaps, const int32_t* skip) {
+  // Two grid barriers per column: (1) after the row swap / pivot-row scaling,
+  // (2) after the elimination, which also produces the next column's pivot
+  // candidates over each CTA's own rows.
   cg::grid_group grid = cg::this_grid();
   if (skip && *skip) return;           // an earlier step of the same box failed
+  extern __shared__ __align__(16) unsigned char gj_smem[];
+  T* prow = reinterpret_cast<T*>(gj_smem);
   __shared__ double sv[8];
   __shared__ int si[8];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ double red_v;
+  __shared__ int red_i;
+  const int G = gridDim.x;
+  const int rpc = (n + G - 1) / G;
+  const int r0 = min(n, (int)blockIdx.x * rpc), r1 = min(n, r0 + rpc);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nt = (int64_t)gridDim.x * blockDim.x;
-  if (regularize != 0.0) {
-    for (int64_t i = gt; i < n; i += nt) A[i * n + i] += T(regularize);
-    grid.sync();
-  }
-  for (int c = 0; c < n; ++c) {
-    // pivot: first max of |A[r][c]| over r >= c (LAPACK i?amax order)
-    double bv = -1.0;
-    int bi = 0x7fffffff;
-    for (int64_t r = c + gt; r < n; r += nt) cmerge(bv, bi, sk_pivabs(ldcg(A + r * n + c)), (int)r);
+  auto block_cand = [&](double bv, int bi, int slot) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       double ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -466,14 +639,39 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) {
       double b = -1.0;
       int j = 0x7fffffff;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) cmerge(b, j, sv[w], si[w]);
-      part_v[blockIdx.x] = b;
-      part_i[blockIdx.x] = j;
+      for (int w = 0; w < nwb; ++w) cmerge(b, j, sv[w], si[w]);
+      part_v[slot * 4096 + blockIdx.x] = b;
+      part_i[slot * 4096 + blockIdx.x] = j;
     }
-    grid.sync();
-    double b = -1.0;
-    int p = 0x7fffffff;
-    for (int q = 0; q < (int)gridDim.x; ++q) cmerge(b, p, ldcg(part_v + q), ldcg(part_i + q));
+  };
+  {
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+      if (regularize != 0.0) A[(int64_t)r * n + r] += T(regularize);
+      cmerge(bv, bi, sk_pivabs(A[(int64_t)r * n]), r);
+    }
+    block_cand(bv, bi, 0);
+  }
+  grid.sync();
+  int par = 0;
+  for (int c = 0; c < n; ++c) {
+    // pivot: first max of |A[r][c]| over r >= c (LAPACK i?amax order)
+    if (wid == 0) {
+      double b = -1.0;
+      int jj = 0x7fffffff;
+      for (int q = lane; q < G; q += 32) cmerge(b, jj, ldcg(part_v + par * 4096 + q), ldcg(part_i + par * 4096 + q));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, b, o);
+        int oi = __shfl_xor_sync(0xffffffffu, jj, o);
+        cmerge(b, jj, ov, oi);
+      }
+      if (lane == 0) { red_v = b; red_i = jj; }
+    }
+    __syncthreads();
+    const double b = red_v;
+    const int p = red_i;
     if (p >= n || b == 0.0) {
       if (gt == 0) *status = 1;
       return;                        // uniform across the grid
@@ -496,18 +694,42 @@ __global__ void __launch_bounds__(256)
     }
     if (gt == 0) swaps[c] = p;
     grid.sync();
-    // eliminate column c from every other row (in-place inverse columns)
-    const int64_t tot = (int64_t)n * n;
-    for (int64_t e = gt; e < tot; e += nt) {
-      const int64_t r = e / n, j = e - r * n;
+    // eliminate column c from the CTA's rows (in-place inverse columns), the
+    // scaled pivot row staged in shared memory; candidates for column c + 1
+    for (int j = threadIdx.x; j < n; j += blockDim.x) prow[j] = ldcg(A + (int64_t)c * n + j);
+    __syncthreads();
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    const int cn = c + 1;
+    for (int r = r0 + wid; r < r1; r += nwb) {
+      T* Ar = A + (int64_t)r * n;
       if (r == c) {
-        if (j == c) A[e] = inv;
+        if (lane == 0) Ar[c] = inv;
         continue;
       }
       const T f = ldcg(colc + r);
-      if (j == c) A[e] = -(f * inv);
-      else A[e] = ldcg(A + e) - f * ldcg(A + (int64_t)c * n + j);
+      for (int j0 = 0; j0 < n; j0 += 128) {
+        T av[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + lane + 32 * u;
+          av[u] = j < n ? ldcg(Ar + j) : T(0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + lane + 32 * u;
+          if (j < n) {
+            T nv;
+            if (j == c) nv = -(f * inv);
+            else nv = av[u] - f * prow[j];
+            Ar[j] = nv;
+            if (j == cn && r >= cn) cmerge(bv, bi, sk_pivabs(nv), r);
+          }
+        }
+      }
     }
+    par ^= 1;
+    if (cn < n) block_cand(bv, bi, par);
     grid.sync();
   }
 }
@@ -691,26 +913,39 @@ static int cpqr_big_impl(void* W, int m, int n, int64_t ld, double eps, int min_
     SKEL_TRY(cudaGetLastError());
   }
   if (m <= 0 || n <= 0) return 0;
-  int grid = coop_grid(k_cpqr_big<T>, 256, 0);
+  size_t smem = sizeof(T) * (size_t)m;
+  int vsmem = smem <= (size_t)skel_smem_optin() - 1024;
+  if (!vsmem) smem = 0;
+  SKEL_TRY(cudaFuncSetAttribute(k_cpqr_big<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int grid = coop_grid(k_cpqr_big<T>, 256, smem);
+  if (grid > 4096) grid = 4096;
+  // scratch behind the state: second position map + 2 x 4096 candidates
+  unsigned char* extra = (unsigned char*)state + 256 + (size_t)n * (3 * sizeof(double) + sizeof(int));
+  extra = (unsigned char*)(((uintptr_t)extra + 15) / 16 * 16);
+  int* pivb = (int*)extra;
+  double* cand_v = (double*)(extra + (((size_t)n * sizeof(int) + 15) / 16) * 16);
+  int* cand_i = (int*)(cand_v + 2 * 4096);
   T* Wp = (T*)W;
-  void* args[] = {&Wp, &m, &n, &ld, &eps, &min_rank, &state};
-  SKEL_TRY(cudaLaunchCooperativeKernel((const void*)k_cpqr_big<T>, grid, 256, args, 0, st));
+  void* args[] = {&Wp, &m, &n, &ld, &eps, &min_rank, &state, &vsmem, &pivb, &cand_v, &cand_i};
+  SKEL_TRY(cudaLaunchCooperativeKernel((const void*)k_cpqr_big<T>, grid, 256, args, smem, st));
   return 0;
 }
 
 template <class T>
 static int gj_impl(void* A, int n, double regularize, int32_t* status, void* scratch, cudaStream_t st,
                    const int32_t* skip = nullptr) {
-  int grid = coop_grid(k_gj_coop<T>, 256, 0);
+  const size_t smem = sizeof(T) * (size_t)(n > 0 ? n : 1);
+  SKEL_TRY(cudaFuncSetAttribute(k_gj_coop<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int grid = coop_grid(k_gj_coop<T>, 256, smem);
   if (grid > 4096) grid = 4096;
   unsigned char* p = (unsigned char*)scratch;
-  double* part_v = (double*)p;
-  int* part_i = (int*)(p + 4096 * sizeof(double));
-  T* colc = (T*)(p + 4096 * (sizeof(double) + sizeof(int)));
+  double* part_v = (double*)p;                       // 2 x 4096 (double-buffered)
+  int* part_i = (int*)(p + 2 * 4096 * sizeof(double));
+  T* colc = (T*)(p + 2 * 4096 * (sizeof(double) + sizeof(int)));
   int* swaps = (int*)((unsigned char*)colc + (size_t)n * 16);
   T* Ap = (T*)A;
   void* args[] = {&Ap, &n, &regularize, &status, &part_v, &part_i, &colc, &swaps, &skip};
-  SKEL_TRY(cudaLaunchCooperativeKernel((const void*)k_gj_coop<T>, grid, 256, args, 0, st));
+  SKEL_TRY(cudaLaunchCooperativeKernel((const void*)k_gj_coop<T>, grid, 256, args, smem, st));
   k_gj_unswap<T><<<(n + 127) / 128, 128, 0, st>>>(Ap, n, swaps, status);
   return skel_last_error();
 }
@@ -781,7 +1016,8 @@ static int factor_big_impl(const SkelFactorLevel* F, int a, int n, int k, int64_
 extern "C" {
 
 int64_t skel_big_state_bytes(int32_t n) {
-  return 256 + (int64_t)n * (3 * sizeof(double) + sizeof(int)) + 64;
+  return 256 + (int64_t)n * (3 * sizeof(double) + sizeof(int)) + 16 + ((int64_t)n * 4 + 15) / 16 * 16 +
+         2 * 4096 * (int64_t)(sizeof(double) + sizeof(int)) + 64;
 }
 
 int skel_big_target(const SkelSource* src, const SkelLevel* lv, int32_t box, int32_t side,
@@ -807,11 +1043,22 @@ int skel_cpqr_big(void* W, int32_t m, int32_t n, int64_t ld, double eps, int32_t
 
 int skel_big_interp(void* W, int32_t n, int64_t ld, void* state, int32_t min_rank, int32_t field,
                     void* stream) {
+  // the rank lives on the device: size the staging for r <= n
   cudaStream_t st = (cudaStream_t)stream;
-  int blocks = (n + 63) / 64;
+  const size_t col = (size_t)(n > 0 ? n : 1) * (field ? 16 : 8);
+  int wpb = (int)((size_t)skel_smem_optin() / col);
+  if (wpb > 4) wpb = 4;
+  if (wpb < 1) return -2;
+  int blocks = (n + wpb - 1) / wpb;
   if (blocks < 1) blocks = 1;
-  if (field == 0) k_big_interp<double><<<blocks, 64, 0, st>>>((double*)W, n, ld, state, min_rank);
-  else k_big_interp<zc><<<blocks, 64, 0, st>>>((zc*)W, n, ld, state, min_rank);
+  const size_t smem = wpb * col;
+  if (field == 0) {
+    SKEL_TRY(cudaFuncSetAttribute(k_big_interp<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_big_interp<double><<<blocks, 32 * wpb, smem, st>>>((double*)W, n, ld, state, min_rank);
+  } else {
+    SKEL_TRY(cudaFuncSetAttribute(k_big_interp<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_big_interp<zc><<<blocks, 32 * wpb, smem, st>>>((zc*)W, n, ld, state, min_rank);
+  }
   return skel_last_error();
 }
 
@@ -836,8 +1083,8 @@ int skel_gemm_tn(int32_t m, int32_t n, int32_t k, const void* X, int64_t ldx, co
   cudaStream_t st = (cudaStream_t)stream;
   dim3 grid((m + 63) / 64, (n + 63) / 64);
   if (field == 0)
-    k_gemm_tn<double><<<grid, 256, 0, st>>>(m, n, k, (const double*)X, ldx, (const double*)A, lda,
-                                            (double*)Y, ldy);
+    k_gemm_tn_dmma<<<grid, 128, 0, st>>>(m, n, k, (const double*)X, ldx, (const double*)A, lda,
+                                         (double*)Y, ldy);
   else
     k_gemm_tn<zc><<<grid, 256, 0, st>>>(m, n, k, (const zc*)X, ldx, (const zc*)A, lda, (zc*)Y, ldy);
   return skel_last_error();
@@ -872,7 +1119,7 @@ int skel_big_probe(int32_t m, int32_t n, const void* A, int64_t lda, const void*
 }
 
 int64_t skel_gj_scratch_bytes(int32_t n) {
-  return 4096 * (int64_t)(sizeof(double) + sizeof(int)) + (int64_t)n * (16 + sizeof(int)) + 256;
+  return 2 * 4096 * (int64_t)(sizeof(double) + sizeof(int)) + (int64_t)n * (16 + sizeof(int)) + 256;
 }
 
 // Shat^-1 in place for big K (status 1: exact zero pivot).  The caller zeroes

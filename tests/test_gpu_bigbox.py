@@ -190,3 +190,44 @@ def test_big_factor_matches_per_box_kernel(monkeypatch):
     for li, lv in enumerate(fi.levels):
         Lam = np.concatenate([nd.Lam.ravel() for nd in lv.nodes])
         np.testing.assert_allclose(Lam, g[f"L{li}_Lam"], atol=1e-7 * np.abs(g[f"L{li}_Lam"]).max())
+
+
+@gpu
+@pytest.mark.parametrize("m,n,k,cplx", [(20, 37, 1000, False), (640, 300, 5000, False),
+                                        (1280, 130, 777, False), (40, 50, 300, True)])
+def test_sketch_gemm(m, n, k, cplx):
+    """skel_gemm_tn (DMMA for real data): Y = X^T A, column-major."""
+    sk = _sk()
+    import torch
+    from paper_1110_3105_b200 import _native
+    rng = np.random.default_rng(m + n)
+    X = rng.standard_normal((m, k)) + (1j * rng.standard_normal((m, k)) if cplx else 0)   # = Omega
+    A = rng.standard_normal((n, k)) + (1j * rng.standard_normal((n, k)) if cplx else 0)   # rows = columns of the target
+    dX = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    dA = torch.from_numpy(np.ascontiguousarray(A)).cuda()
+    dY = torch.empty((n, m), dtype=dX.dtype, device="cuda")
+    _native.check(_native.lib().skel_gemm_tn(m, n, k, _native.ptr(dX), k, _native.ptr(dA), k,
+                                             _native.ptr(dY), m, int(cplx), _native.stream_ptr()), "gemm")
+    Y = dY.cpu().numpy().T
+    ref = X @ A.T
+    np.testing.assert_allclose(Y, ref, rtol=0, atol=1e-12 * np.sqrt(k) * np.abs(ref).max())
+    assert sk is not None
+
+
+@gpu
+def test_config4_full_size_residual():
+    """BASELINE config 4 at its full size (N = 40000 Fibonacci sphere, eps
+    1e-6, unit diagonal): the reference needs tens of minutes here, so the
+    check is the exact on-the-fly residual (<= 10 eps) and the rank profile."""
+    sk = _sk()
+    n = 40000
+    pts = sk.PointSet(oracle.fib_sphere(n), None, np.full(n, 4 * np.pi / n))
+    tree = sk.build_tree(pts, 64)
+    src = sk.KernelSource(sk.KernelSpec("laplace", 3), pts, tree.perm, diag=1.0)
+    cm = sk.compress_source(src, tree, 1e-6)
+    fi = sk.factor(cm)
+    B = np.random.default_rng(0).standard_normal((n, 1))
+    X = sk.solve(fi, B)
+    res = np.linalg.norm(sk.bie.dense_matvec(src, X) - B) / np.linalg.norm(B)
+    assert res <= 1e-5, res
+    assert cm.S_shape()[0] > 1000

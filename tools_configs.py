@@ -65,29 +65,27 @@ def profile_big(n=40000):
             cnt[name] += 1
             return r
         return f
-    _bigbox._cpqr = wrap("cpqr", _bigbox._cpqr)
     _bigbox._norm_estimate = wrap("norm_est", _bigbox._norm_estimate)
     _bigbox._randomized = wrap("randomized(total)", _bigbox._randomized)
     _bigbox.run_boxes = wrap("run_boxes(total)", _bigbox.run_boxes)
-    orig_rng = np.random.default_rng
+    _bigbox.SketchStream.sketch = wrap("sketch_wait", _bigbox.SketchStream.sketch)
+    from paper_1110_3105_b200 import _native
+    Lb = _native.lib()
+    for nm in ("skel_gemm_tn", "skel_big_target", "skel_big_output", "skel_big_probe",
+               "skel_big_interp", "skel_gemv", "skel_factor_big", "skel_dense_inverse_big"):
+        setattr(Lb, nm, wrap(nm, getattr(Lb, nm)))
+    orig = _bigbox._cpqr
 
-    class R:
-        def __init__(self, s):
-            self.g = orig_rng(s)
-
-        def standard_normal(self, *a):
-            t = time.perf_counter()
-            r = self.g.standard_normal(*a)
-            acc["rng"] += time.perf_counter() - t
-            return r
-    _bigbox.np = type("npshim", (), {"random": type("r", (), {"default_rng": R}),
-                                      "__getattr__": lambda s, k: getattr(np, k)})()
-    for k in dir(np):
-        if not k.startswith("_") and k != "random":
-            try:
-                setattr(_bigbox.np, k, getattr(np, k))
-            except Exception:
-                pass
+    def cp(L, W, m, n, ld, eps, min_rank, resume, state, field, st):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        orig(L, W, m, n, ld, eps, min_rank, resume, state, field, st)
+        torch.cuda.synchronize()
+        key = "cpqr_full" if m > 4000 else "cpqr_sketch"
+        acc[key] += time.perf_counter() - t
+        cnt[key] += 1
+        acc[key + "_steps"] += _bigbox._rank_of(state)
+    _bigbox._cpqr = cp
     _profile.reset()
     _profile.enabled = True
     config4(n)
