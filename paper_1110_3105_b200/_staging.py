@@ -131,3 +131,39 @@ def join(streams):
 def eager_stream():
     """The side stream of the eager (overlapped) factorization."""
     return side_streams(1, "eager")[0]
+
+
+def size_buckets(cls, key):
+    """Group positions by class (cls >= 0; negative = excluded), each group
+    ordered by descending key with ties by position: one lexsort instead of
+    a nonzero / argsort per class.  Returns a list of int32 index arrays in
+    ascending class order."""
+    cls = np.asarray(cls)
+    keep = np.flatnonzero(cls >= 0)
+    if keep.size == 0:
+        return []
+    c = cls[keep].astype(np.int64)
+    k = np.asarray(key)[keep].astype(np.int64)
+    # one stable argsort of (class, -key) packed into an int64
+    span = int(k.max()) - int(k.min()) + 1
+    order = np.argsort(c * span + (int(k.max()) - k), kind="stable")
+    idx = keep[order].astype(np.int32)
+    cs = c[order]
+    cuts = np.flatnonzero(cs[1:] != cs[:-1]) + 1
+    return np.split(idx, cuts)
+
+
+def on_stream(s, fn, kind=None, **meta):
+    """Run ``fn(stream_handle)`` for a launch on side stream ``s``.  Without
+    profiling the raw handle is passed directly (no torch stream context:
+    those cost ~10 us of host time per launch); with profiling the launch is
+    bracketed by CUDA events on ``s``.  Returns the profiling record."""
+    from . import _profile
+    if not _profile.enabled:
+        fn(_native.c_vp(s.cuda_stream))
+        return None
+    torch = _native.require_cuda()
+    with torch.cuda.stream(s):
+        with _profile.timed(kind, **meta) as rec:
+            fn(_native.stream_ptr())
+    return rec

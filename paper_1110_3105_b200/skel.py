@@ -24,7 +24,7 @@ from ._device import DeviceGeometry
 from .errors import InvalidInput, RefusedTooLarge
 from .geom import OrthTree, PointSet
 from .kernels import KernelSpec
-from ._staging import Packer, eager_stream, fork, join
+from ._staging import Packer, eager_stream, fork, join, on_stream, size_buckets
 
 DEFAULT_N_PROXY = {2: 64, 3: 512}        # skel.py:29
 _RANDOMIZED_CUTOFF = 4096                # skel.py:33
@@ -383,6 +383,34 @@ def id_level_flops(m0, m1, nr, nc, kr, kc, c_entry=10.0):
     return one(m0, nr, kr) + one(m1, nc, kc) + asm
 
 
+def _level_geometry(tree, li, cfg, dim, k_wave):
+    """Rank-independent per-level inputs (neighbour lists, proxy circles /
+    spheres, children ranges), uploaded in one async copy; computed for
+    level l+1 while level l's ID kernels run."""
+    from types import SimpleNamespace
+    ids = tree.levels[li]
+    p = ids.size
+    noff, nidx = tree.cover_neighbors(li)
+    rad = cfg.radius_factor * 3.0 * tree.hw[ids] * np.sqrt(dim)
+    neff = np.full(p, cfg.n_proxy, dtype=np.int64)
+    if k_wave > 0:
+        neff += np.ceil(4.0 * k_wave * rad).astype(np.int64)
+    uniq = np.unique(neff)
+    tables = [unit_proxy(int(u), dim) for u in uniq]
+    tstart = _off([t.shape[0] for t in tables])[:-1]
+    pxy_begin = tstart[np.searchsorted(uniq, neff)].astype(np.int32)
+    unit = np.concatenate(tables, axis=0)
+    child_off = tree.cover_children(li) if li > 0 else None
+    pk = Packer()
+    pk.add("nbr_off", noff).add("nbr", nidx.astype(np.int32))
+    pk.add("box_c", np.ascontiguousarray(tree.center[ids]).ravel()).add("box_r", rad)
+    pk.add("pxy_begin", pxy_begin).add("pxy_count", neff.astype(np.int32)).add("pxy_unit", unit.ravel())
+    if child_off is not None:
+        pk.add("child_off", child_off)
+    return SimpleNamespace(ids=ids, p=p, noff=noff, nidx=nidx, rad=rad, neff=neff,
+                           n_unit=unit.shape[0], child_off=child_off, t=pk.upload())
+
+
 def _segment_sum(vals, off):
     cs = np.concatenate([[0], np.cumsum(vals)])
     return cs[off[1:]] - cs[off[:-1]]
@@ -457,36 +485,31 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         from .solver import FactorRun
         run = FactorRun(field, 0.0, stream=eager_stream(), shard=shard)
     nvtx = _NVTX
+    geo_next = _level_geometry(tree, 0, cfg, dim, k_wave)
+    pending = None          # (level, DevLevel, event): factor launch deferred into the next level
     for li in range(top_run):
+        _ht = _HostTimer(li) if _HOST_TIMING else None
         lev_ctx = _profile.timed("level", level=li)
         lev_rec = lev_ctx.__enter__()
         if nvtx:
             torch.cuda.nvtx.range_push(f"level{li}")
-        ids = covers[li]
-        p = ids.size
+        geo = geo_next
+        ids, p = geo.ids, geo.p
         mine = shard.mine(li) if shard is not None else None
         own = np.ones(p, dtype=np.int64) if mine is None else mine.astype(np.int64)
-        noff, nidx = tree.cover_neighbors(li)
+        noff, nidx = geo.noff, geo.nidx
         if li == 0:
             nr = (tree.hi[ids] - tree.lo[ids]).astype(np.int64)
             nc = nr.copy()
             rdofs = cdofs = allpos
             child_off = None
         else:
-            child_off = tree.cover_children(li)
+            child_off = geo.child_off
             nr = _segment_sum(prev.kr, child_off)
             nc = _segment_sum(prev.kc, child_off)
             rdofs, cdofs = prev.rskel, prev.cskel
         rdof_off, cdof_off = _off(nr), _off(nc)
-        rad = cfg.radius_factor * 3.0 * tree.hw[ids] * np.sqrt(dim)
-        neff = np.full(p, cfg.n_proxy, dtype=np.int64)
-        if k_wave > 0:
-            neff += np.ceil(4.0 * k_wave * rad).astype(np.int64)
-        uniq = np.unique(neff)
-        tables = [unit_proxy(int(u), dim) for u in uniq]
-        tstart = _off([t.shape[0] for t in tables])[:-1]
-        pxy_begin = tstart[np.searchsorted(uniq, neff)].astype(np.int32)
-        unit = np.concatenate(tables, axis=0)
+        neff = geo.neff
         m0 = _segment_sum(nc[nidx], noff) + neff
         m1 = _segment_sum(nr[nidx], noff) + neff
         # slab slots only for this rank's boxes (all boxes when unsharded)
@@ -506,18 +529,12 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         big &= (_bigbox_randomized(m0, nr) | _bigbox_randomized(m1, nc)
                 | (need_n > _BIG_N) | (_level_smem_fixed_vec(need_n, field) > optin))
         cls = np.where((own > 0) & ~big, cls, -1)
-        for c in np.unique(cls[cls >= 0]):
-            sel = np.nonzero(cls == c)[0]
-            sel = sel[np.argsort(-wb[sel], kind="stable")].astype(np.int32)
-            buckets.append(sel)
+        buckets = size_buckets(cls, wb)
+        _ht and _ht.mark("prep")
         pk = Packer()
-        pk.add("rdof_off", rdof_off).add("cdof_off", cdof_off).add("nbr_off", noff)
-        pk.add("nbr", nidx.astype(np.int32)).add("box_c", np.ascontiguousarray(tree.center[ids]).ravel())
-        pk.add("box_r", rad).add("pxy_begin", pxy_begin).add("pxy_count", neff.astype(np.int32))
-        pk.add("pxy_unit", unit.ravel()).add("d_off", d_off).add("l_off", l_off).add("r_off", r_off)
+        pk.add("rdof_off", rdof_off).add("cdof_off", cdof_off)
+        pk.add("d_off", d_off).add("l_off", l_off).add("r_off", r_off)
         pk.add("nr", nr.astype(np.int32))
-        if li > 0:
-            pk.add("child_off", child_off)
         for bi, sel in enumerate(buckets):
             pk.add(f"order{bi}", sel)
         own_idx = None
@@ -525,6 +542,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             own_idx = np.nonzero(mine)[0].astype(np.int32)
             pk.add("own", own_idx)
         t = pk.upload()
+        tg = geo.t
         Dt = torch.empty(max(int(d_off[-1]), 1), dtype=tdt, device=dev)
         Lt = torch.empty(max(int(l_off[-1]), 1), dtype=tdt, device=dev)
         Rt = torch.empty(max(int(r_off[-1]), 1), dtype=tdt, device=dev)
@@ -532,32 +550,33 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         cskel = torch.empty(max(int(cdof_off[-1]), 1), dtype=torch.int32, device=dev)
         kk = torch.zeros(3 * p, dtype=torch.int32, device=dev)     # kr | kc | flags
         lvd = _native.SkelLevel()
-        lvd.nbox, lvd.level, lvd.equalize, lvd.n_unit = p, li, int(bool(equalize_ranks)), unit.shape[0]
+        lvd.nbox, lvd.level, lvd.equalize, lvd.n_unit = p, li, int(bool(equalize_ranks)), geo.n_unit
         lvd.eps = float(eps)
         lvd.debug_skip = _DEBUG_SKIP[0]
         lvd.rdof_off, lvd.rdofs = p_(t["rdof_off"]), p_(rdofs)
         lvd.cdof_off, lvd.cdofs = p_(t["cdof_off"]), p_(cdofs)
         if li > 0:
-            lvd.child_off = p_(t["child_off"])
+            lvd.child_off = p_(tg["child_off"])
             lvd.prev_kr, lvd.prev_kc = p_(prev.t_kr), p_(prev.t_kc)
-        lvd.nbr_off, lvd.nbr = p_(t["nbr_off"]), p_(t["nbr"])
-        lvd.box_c, lvd.box_r = p_(t["box_c"]), p_(t["box_r"])
-        lvd.pxy_begin, lvd.pxy_count, lvd.pxy_unit = (p_(t["pxy_begin"]), p_(t["pxy_count"]),
-                                                      p_(t["pxy_unit"]))
+        lvd.nbr_off, lvd.nbr = p_(tg["nbr_off"]), p_(tg["nbr"])
+        lvd.box_c, lvd.box_r = p_(tg["box_c"]), p_(tg["box_r"])
+        lvd.pxy_begin, lvd.pxy_count, lvd.pxy_unit = (p_(tg["pxy_begin"]), p_(tg["pxy_count"]),
+                                                      p_(tg["pxy_unit"]))
         lvd.d_off, lvd.l_off, lvd.r_off = p_(t["d_off"]), p_(t["l_off"]), p_(t["r_off"])
         lvd.D, lvd.L, lvd.R = p_(Dt), p_(Lt), p_(Rt)
         lvd.rskel, lvd.cskel = p_(rskel), p_(cskel)
         lvd.kr, lvd.kc, lvd.flags = p_(kk[:p]), p_(kk[p:2 * p]), p_(kk[2 * p:])
         scratch_keep = []
         recs = []
+        _ht and _ht.mark("pack+upload+alloc")
         streams = fork(len(buckets) + 1)
         # D blocks on their own stream, concurrent with the ID buckets
-        with torch.cuda.stream(streams[-1]):
-            with _profile.timed("assemble_D", level=li):
-                _native.check(L.skel_assemble_D(desc, lvd, p_(t["own"]) if own_idx is not None else None,
-                                                0 if own_idx is None else own_idx.size,
-                                                int(max(nr.max(initial=0), nc.max(initial=0), 1)),
-                                                field, _native.stream_ptr()), "skel_assemble_D")
+        d_order = p_(t["own"]) if own_idx is not None else None
+        d_nrun = 0 if own_idx is None else own_idx.size
+        d_maxn = int(max(nr.max(initial=0), nc.max(initial=0), 1))
+        on_stream(streams[-1], lambda sp: _native.check(
+            L.skel_assemble_D(desc, lvd, d_order, d_nrun, d_maxn, field, sp), "skel_assemble_D"),
+            "assemble_D", level=li)
         for bi, sel in enumerate(buckets):
             max_m, max_n = int(need_m[sel].max()), int(need_n[sel].max())
             max_w = int((need_m[sel] * need_n[sel]).max())
@@ -569,13 +588,11 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
                 lvd.scratch, lvd.scratch_bytes = p_(scr), sb
             else:
                 lvd.scratch, lvd.scratch_bytes = None, 0
-            ctx = torch.cuda.stream(streams[bi]) if streams else _nullctx()
-            with ctx:
-                with _profile.timed("id_level", level=li, sel=sel, max_m=max_m, max_n=max_n,
-                                    max_w=max_w) as rec:
-                    _native.check(L.skel_id_level(desc, lvd, p_(t[f"order{bi}"]), sel.size, max_m,
-                                                  max_n, max_w, field, _native.stream_ptr()),
-                                  f"skel_id_level (level {li})")
+            order_p = p_(t[f"order{bi}"])
+            rec = on_stream(streams[bi], lambda sp: _native.check(
+                L.skel_id_level(desc, lvd, order_p, sel.size, max_m, max_n, max_w, field, sp),
+                f"skel_id_level (level {li})"),
+                "id_level", level=li, sel=sel, max_m=max_m, max_n=max_n, max_w=max_w)
             if rec is not None:
                 recs.append(rec)
         big_boxes = np.nonzero(big)[0]
@@ -584,10 +601,21 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             with _profile.timed("id_big", level=li):
                 _bigbox.run_boxes(desc, lvd, big_boxes, li, noff, nidx, nr, nc, neff, eps,
                                   bool(equalize_ranks), seed, field)
+        # host work overlapped with this level's ID kernels: the next level's
+        # geometry and the deferred factor launch of the previous level
+        if li + 1 < top_run:
+            geo_next = _level_geometry(tree, li + 1, cfg, dim, k_wave)
+        if pending is not None:
+            run.stream.wait_event(pending[2])
+            run.add_level(pending[0], pending[1])
+            pending = None
+        _ht and _ht.mark("launch")
         join(streams)
         if mine is not None:
             shard.all_reduce(kk)          # non-owned entries are zero on each rank
+        _ht and _ht.mark("big+join")
         kk_h = kk.cpu().numpy()
+        _ht and _ht.mark("kk-wait")
         kr = kk_h[:p].astype(np.int64)
         kc = kk_h[p:2 * p].astype(np.int64)
         fl = kk_h[2 * p:]
@@ -605,16 +633,17 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         # the sorted skeletons, compacted, are the next level's dof lists
         kro, kco = _off(kr), _off(kc)
         pk2 = Packer()
-        pk2.add("d_off", d_off).add("l_off", l_off).add("r_off", r_off)
-        pk2.add("kr", kr.astype(np.int32)).add("kc", kc.astype(np.int32))
         pk2.add("kr_off", kro).add("kc_off", kco)
         t2 = pk2.upload()
-        t2.update({k: t[k] for k in ("rdof_off", "cdof_off", "nr")})
+        t2.update({k: t[k] for k in ("rdof_off", "cdof_off", "nr", "d_off", "l_off", "r_off")})
+        t2["kr"], t2["kc"] = kk[:p], kk[p:2 * p]      # the device ranks (full after the all-reduce)
         if own_idx is not None:
             t2["own"] = t["own"]
         if li > 0:
-            t2["child_off"] = t["child_off"]
+            t2["child_off"] = tg["child_off"]
         t2["_buffer0"] = t["_buffer"]
+        t2["_buffer_geo"] = tg["_buffer"]
+        t2["_kk"] = kk
         if mine is None:
             rsk = torch.empty(max(int(kro[-1]), 1), dtype=torch.int32, device=dev)
             csk = torch.empty(max(int(kco[-1]), 1), dtype=torch.int32, device=dev)
@@ -641,15 +670,20 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
                       dtype, t=t2, mine=mine)
         levels.append(CompressedLevel(dev=dl))
         prev = dl
+        _ht and _ht.mark("post")
         if run is not None:
             ev = torch.cuda.Event()
             ev.record()
-            run.stream.wait_event(ev)
-            run.add_level(li, dl)
+            pending = (li, dl, ev)
+        _ht and _ht.mark("factor-launch")
+        _ht and _ht.done()
         lev_ctx.__exit__(None, None, None)
         if nvtx:
             torch.cuda.nvtx.range_pop()
 
+    if pending is not None:
+        run.stream.wait_event(pending[2])
+        run.add_level(pending[0], pending[1])
     if top_run < top:      # developer benchmarking only: partial sweep
         return levels
     last = prev
@@ -667,6 +701,24 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
 
 
 _OPTIN = None
+_HOST_TIMING = bool(__import__("os").environ.get("SKEL_HOST_TIMING"))   # developer: host phases per level
+
+
+class _HostTimer:
+    def __init__(self, li):
+        import time
+        self.li, self.t, self.parts = li, time.perf_counter(), []
+
+    def mark(self, name):
+        import time
+        now = time.perf_counter()
+        self.parts.append((name, now - self.t))
+        self.t = now
+
+    def done(self):
+        print(f"  L{self.li:2d} host: " + "  ".join(f"{k} {1e3 * v:.2f}" for k, v in self.parts), flush=True)
+
+
 _DEBUG_MAX_LEVELS = [0]      # developer benchmarking: stop the sweep after this many levels
 _DEBUG_SKIP = [0]            # developer benchmarking: 1 = assembly only, 2 = + column norms
 _NVTX = bool(__import__("os").environ.get("SKEL_NVTX"))   # per-level NVTX ranges (profiling)

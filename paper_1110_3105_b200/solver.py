@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _native, _profile
 from .errors import InvalidInput, SingularBlock
-from ._staging import Packer, fork, join
+from ._staging import Packer, fork, join, on_stream, size_buckets
 from .skel import CompressedMatrix, _dense_apply, _nullctx, _off
 
 _RCOND_WARN = 1e-14
@@ -64,11 +64,7 @@ def _solve_buckets(n):
     """Boxes grouped by size so each sweep launch sizes its shared memory for
     its own boxes (more CTAs per SM for the many small ones)."""
     cls = np.searchsorted(np.asarray(_SOLVE_CLASSES), n, side="left")
-    out = []
-    for c in np.unique(cls[n > 0]):
-        sel = np.nonzero((cls == c) & (n > 0))[0]
-        out.append(sel[np.argsort(-n[sel], kind="stable")].astype(np.int32))
-    return out
+    return size_buckets(np.where(n > 0, cls, -1), n)
 
 
 class FactoredLevel:
@@ -251,10 +247,7 @@ class FactorRun:
         cls = np.searchsorted(np.asarray(_FAC_CLASSES), need, side="left")
         # big boxes (3D coarse levels): one box at a time over the whole GPU
         big = n_own >= _BIG_FAC_N
-        buckets = []
-        for c in np.unique(cls[(n_own > 0) & ~big]):
-            sel = np.nonzero((cls == c) & (n_own > 0) & ~big)[0]
-            buckets.append(sel[np.argsort(-need[sel], kind="stable")].astype(np.int32))
+        buckets = size_buckets(np.where((n_own > 0) & ~big, cls, -1), need)
         p = dl.p
         outer = torch.cuda.stream(self.stream) if self.stream is not None else _nullctx()
         with outer:
@@ -303,11 +296,10 @@ class FactorRun:
                     scr = torch.empty(sel.size * nd // 8 + 1, dtype=torch.float64, device=dev)
                     self.keep.append(scr)
                     F.scratch, F.scratch_bytes = p_(scr), sel.size * nd
-                ctx = torch.cuda.stream(streams[bi]) if streams else _nullctx()
-                with ctx:
-                    with _profile.timed("factor_level", level=li) as rec:
-                        _native.check(L.skel_factor_level(F, max_n, max_k, field, _native.stream_ptr()),
-                                      f"skel_factor_level ({li})")
+                rec = on_stream(streams[bi] if streams else torch.cuda.current_stream(),
+                                lambda sp: _native.check(L.skel_factor_level(F, max_n, max_k, field, sp),
+                                                         f"skel_factor_level ({li})"),
+                                "factor_level", level=li)
                 if rec is not None:
                     b_ = sel
                     rec.flops = float((2 * nf[b_] ** 3 + 6 * nf[b_] ** 2 * kf[b_]
@@ -461,21 +453,20 @@ def _sweep_launch(L, d, direction, u, v, out, Rn, field):
     if not bks:
         return
     streams = fork(len(bks), tag="solve") if len(bks) > 1 else None
+    main = _native.stream_ptr()
     for bi, (order, cnt, mn, mk) in enumerate(bks):
-        ctx = torch.cuda.stream(streams[bi]) if streams else _nullctx()
-        with ctx:
-            st = _native.stream_ptr()
-            if direction == "up":
-                if mk == 0:
-                    continue
-                _native.check(L.skel_sweep_up_ex(cnt, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
-                                                 p_(d.t_ld_off), p_(d.Rd), p_(u), p_(out), Rn, field,
-                                                 mn, mk, p_(order), st), "sweep_up")
-            else:
-                _native.check(L.skel_sweep_down_ex(cnt, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
-                                                   p_(d.t_dd_off), p_(d.Dd), p_(d.t_ld_off), p_(d.Ld),
-                                                   p_(u), p_(v), p_(out), Rn, field, mn, mk, p_(order),
-                                                   st), "sweep_down")
+        st = _native.c_vp(streams[bi].cuda_stream) if streams else main
+        if direction == "up":
+            if mk == 0:
+                continue
+            _native.check(L.skel_sweep_up_ex(cnt, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
+                                             p_(d.t_ld_off), p_(d.Rd), p_(u), p_(out), Rn, field,
+                                             mn, mk, p_(order), st), "sweep_up")
+        else:
+            _native.check(L.skel_sweep_down_ex(cnt, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
+                                               p_(d.t_dd_off), p_(d.Dd), p_(d.t_ld_off), p_(d.Ld),
+                                               p_(u), p_(v), p_(out), Rn, field, mn, mk, p_(order),
+                                               st), "sweep_down")
     if streams:
         join(streams)
 

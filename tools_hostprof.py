@@ -15,4 +15,4 @@ def step():
 for _ in range(2): step()
 t = time.perf_counter(); step(); print("step", time.perf_counter() - t)
 pr = cProfile.Profile(); pr.enable(); step(); pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+pstats.Stats(pr).sort_stats("tottime").print_stats(40)
