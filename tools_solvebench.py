@@ -20,3 +20,11 @@ for R in Rs:
     cnt, ms, fl, by = _profile.summary("sweep")
     print(f"R={R}: {t*1e3:.3f} ms  {n*R/t:.3e} N*RHS/s  sweeps {cnt} launches {ms:.3f} ms  "
           f"{fl/ms/1e9:.2f} TF/s  {by/ms/1e6:.1f} GB/s", flush=True)
+    # per level / direction
+    rs = [r for r in _profile.records if r.kind == "sweep"]
+    nl = len(fi.levels)
+    for i, r in enumerate(rs):
+        li = i if i < nl else 2 * nl - 1 - i
+        d = fi.levels[li].dev
+        print(f"   {r.meta['dir']:4s} L{li:2d} boxes {d.p:6d} {r.ms()*1e3:8.1f} us  {r.nbytes/1e6:8.2f} MB  "
+              f"{r.nbytes/max(r.ms(),1e-9)/1e6:8.1f} GB/s  buckets {len(d.solve_buckets)}", flush=True)
