@@ -210,6 +210,9 @@ int skel_dense_inverse(void* A, void* lu, int32_t* ipiv, int32_t K, double regul
                        int32_t* status, double* rcond, int32_t field, void* scratch,
                        void* stream);
 
+/* out[2i], out[2i+1] = Re, Im of H0^(1)(z[i]) = J0 + i Y0 (kernels.py:65-75). */
+int skel_bessel_h0(const double* z, int64_t n, double* out, void* stream);
+
 /* ---- big boxes (one box over the whole GPU; csrc/big.cu) ---------------
  * Used for boxes whose target does not fit a per-box CTA (3D coarse levels)
  * and for every target the reference sends to id_randomized
@@ -255,6 +258,17 @@ int skel_big_probe(int32_t m, int32_t n, const void* A, int64_t lda, const void*
  * row-major matrix in place; *status (zeroed by the caller) = 1 on an exact
  * zero pivot.  scratch: skel_gj_scratch_bytes(n). */
 int64_t skel_gj_scratch_bytes(int32_t n);
+
+/* LU with partial pivoting in place (getrf conventions: unit-lower L, U,
+ * 0-based piv as scipy.linalg.lu_factor; the reference's Shat factorization,
+ * solver.py:269-274, and the factored container's S_lu).  *status (zeroed by
+ * the caller) = 1 on an exact zero pivot.  scratch: skel_gj_scratch_bytes(n). */
+int skel_dense_lu(void* A, int32_t n, int32_t* piv, int32_t* status, int32_t field, void* scratch,
+                  void* stream);
+
+/* inv = A^-1 (row-major) from skel_dense_lu factors (getrs order per column). */
+int skel_lu_inverse(const void* lu, const int32_t* piv, int32_t n, void* inv, int32_t field,
+                    void* stream);
 
 /* factor_node of ONE big box (n = nr = nc, k) over the whole GPU: cooperative
  * inverses of D_eff and M = R D^-1 L, GEMMs for X, Rd, Ld, Dd

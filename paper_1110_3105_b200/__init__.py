@@ -13,7 +13,10 @@ from . import bie  # noqa: F401
 from .errors import (AccuracyWarning, InvalidInput, NotConverged, RefusedTooLarge,
                      SingularBlock, SkelkitError)
 from .geom import OrthTree, PointSet, build_tree, level_neighbors, neighbors
-from .kernels import KernelSpec, eval_block
+from .container import load_compressed, load_factored, save_compressed, save_factored
+from .embedding import SparseEmbedding, assemble_embedding, export_matrix_market
+from .kernels import KernelSpec, bessel_h0, eval_block
+from .krylov import gmres
 from .lowrank import (InterpDecomp, id_fixed_precision, id_fixed_precision_batched,
                       id_fixed_precision_large, id_randomized, id_rows)
 from .skel import (CompressedLevel, CompressedMatrix, CompressedNode, KernelSource, ProxyConfig,
@@ -29,4 +32,6 @@ __all__ = [
     "id_fixed_precision_batched", "id_fixed_precision_large", "id_randomized", "id_rows", "CompressedLevel", "CompressedMatrix",
     "CompressedNode", "KernelSource", "ProxyConfig", "apply", "compress", "compress_source",
     "proxy_points", "FactoredInverse", "factor", "solve", "solve_device", "__version__",
+    "bessel_h0", "save_compressed", "load_compressed", "save_factored", "load_factored",
+    "SparseEmbedding", "assemble_embedding", "export_matrix_market", "gmres",
 ]

@@ -105,6 +105,9 @@ _SIGS = {
     "skel_big_probe": [c_i32, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp],
     "skel_gj_scratch_bytes": [c_i32],
     "skel_factor_big_bytes": [c_i32, c_i32, c_i32],
+    "skel_dense_lu": [c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp],
+    "skel_bessel_h0": [c_vp, c_i64, c_vp, c_vp],
+    "skel_lu_inverse": [c_vp, c_vp, c_i32, c_vp, c_i32, c_vp],
     "skel_factor_big": [_P(SkelFactorLevel), c_i32, c_i32, c_i32, c_i64, c_i64, c_i64, c_i64, c_vp,
                         c_i64, c_i32, c_vp],
     "skel_dense_inverse_big": [c_vp, c_i32, c_f64, c_vp, c_i32, c_vp, c_vp],
@@ -119,7 +122,8 @@ _LAUNCHING = {"skel_id_level", "skel_assemble_D", "skel_assemble_S", "skel_eval_
               "skel_sweep_down_ex", "skel_dense_apply", "skel_permute_rows",
               "skel_compact_i32", "skel_dense_matvec", "skel_fp64_probe", "skel_big_target",
               "skel_cpqr_big", "skel_big_interp", "skel_big_output", "skel_gemm_tn", "skel_gemv",
-              "skel_big_probe", "skel_dense_inverse_big", "skel_factor_big"}
+              "skel_big_probe", "skel_dense_inverse_big", "skel_factor_big", "skel_dense_lu",
+              "skel_lu_inverse", "skel_bessel_h0"}
 launch_count = [0]
 
 

@@ -734,6 +734,150 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Cooperative LU with partial pivoting, row-major n x n in place, LAPACK
+// getrf conventions (unit-lower L below the diagonal, U on and above, piv[c]
+// = the row interchanged with row c, 0-based as scipy.linalg.lu_factor
+// returns it) -- the reference stores Shat as lu_factor output
+// (solver.py:269-274) and its container keeps (lu, piv).
+template <class T>
+__global__ void __launch_bounds__(256)
+    k_lu_coop(T* A, int n, int32_t* status, double* part_v, int* part_i, T* colc, int* piv) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char lu_smem[];
+  T* prow = reinterpret_cast<T*>(lu_smem);
+  __shared__ double sv[8];
+  __shared__ int si[8];
+  __shared__ double red_v;
+  __shared__ int red_i;
+  const int G = gridDim.x;
+  const int rpc = (n + G - 1) / G;
+  const int r0 = min(n, (int)blockIdx.x * rpc), r1 = min(n, r0 + rpc);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  auto block_cand = [&](double bv, int bi, int slot) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      cmerge(bv, bi, ov, oi);
+    }
+    if (lane == 0) { sv[wid] = bv; si[wid] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = -1.0;
+      int j = 0x7fffffff;
+      for (int w = 0; w < nwb; ++w) cmerge(b, j, sv[w], si[w]);
+      part_v[slot * 4096 + blockIdx.x] = b;
+      part_i[slot * 4096 + blockIdx.x] = j;
+    }
+  };
+  {
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) cmerge(bv, bi, sk_pivabs(A[(int64_t)r * n]), r);
+    block_cand(bv, bi, 0);
+  }
+  grid.sync();
+  int par = 0;
+  for (int c = 0; c < n; ++c) {
+    if (wid == 0) {
+      double b = -1.0;
+      int jj = 0x7fffffff;
+      for (int q = lane; q < G; q += 32) cmerge(b, jj, ldcg(part_v + par * 4096 + q), ldcg(part_i + par * 4096 + q));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, b, o);
+        int oi = __shfl_xor_sync(0xffffffffu, jj, o);
+        cmerge(b, jj, ov, oi);
+      }
+      if (lane == 0) { red_v = b; red_i = jj; }
+    }
+    __syncthreads();
+    const double b = red_v;
+    const int p = red_i;
+    if (p >= n || b == 0.0) {
+      if (gt == 0) *status = 1;
+      return;
+    }
+    // interchange rows c and p (whole rows, as getrf; column c is handled
+    // through colc and rewritten below), save column c as it reads after
+    for (int64_t j = gt; j < n; j += nt) {
+      if (p != c && j != c) {
+        const T vp = ldcg(A + (int64_t)p * n + j);
+        const T vc = ldcg(A + (int64_t)c * n + j);
+        A[(int64_t)p * n + j] = vc;
+        A[(int64_t)c * n + j] = vp;
+      }
+    }
+    for (int64_t r = gt; r < n; r += nt) {
+      T v = (r == p) ? ldcg(A + (int64_t)c * n + c) : ldcg(A + r * n + c);
+      if (r == c) v = ldcg(A + (int64_t)p * n + c);
+      colc[r] = v;
+    }
+    if (gt == 0) piv[c] = p;
+    grid.sync();
+    // multipliers and the rank-1 update of the trailing block (own rows > c)
+    for (int j = threadIdx.x; j < n; j += blockDim.x) prow[j] = ldcg(A + (int64_t)c * n + j);
+    __syncthreads();
+    const T pv = ldcg(colc + c);
+    const T inv = T(1.0) / pv;
+    if (gt == 0) A[(int64_t)c * n + c] = pv;
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    const int cn = c + 1;
+    for (int r = max(r0, c + 1) + wid; r < r1; r += nwb) {
+      T* Ar = A + (int64_t)r * n;
+      const T l = ldcg(colc + r) * inv;
+      if (lane == 0) Ar[c] = l;
+      for (int j = c + 1 + lane; j < n; j += 32) {
+        const T nv = ldcg(Ar + j) - l * prow[j];
+        Ar[j] = nv;
+        if (j == cn) cmerge(bv, bi, sk_pivabs(nv), r);
+      }
+    }
+    par ^= 1;
+    if (cn < n) block_cand(bv, bi, par);
+    grid.sync();
+  }
+}
+
+// inverse from getrf factors: one warp per right-hand side e_j (row
+// interchanges, unit-lower forward, upper backward substitution; getrs order)
+template <class T>
+__global__ void k_lu_inverse(const T* __restrict__ LU, const int* __restrict__ piv, int n, T* inv) {
+  extern __shared__ __align__(16) unsigned char li_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int j = blockIdx.x * (blockDim.x >> 5) + wid;
+  if (j >= n) return;
+  T* x = reinterpret_cast<T*>(li_smem) + (size_t)wid * n;
+  for (int i = lane; i < n; i += 32) x[i] = (i == j) ? T(1.0) : T(0.0);
+  __syncwarp();
+  if (lane == 0)
+    for (int i = 0; i < n; ++i) {
+      const int p = piv[i];
+      if (p != i) { T t = x[i]; x[i] = x[p]; x[p] = t; }
+    }
+  __syncwarp();
+  for (int i = 1; i < n; ++i) {
+    const T* li = LU + (int64_t)i * n;
+    T s = T(0.0);
+    for (int t = lane; t < i; t += 32) s += li[t] * x[t];
+    s = warp_sum(s);
+    if (lane == 0) x[i] -= s;
+    __syncwarp();
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    const T* ui = LU + (int64_t)i * n;
+    T s = T(0.0);
+    for (int t = i + 1 + lane; t < n; t += 32) s += ui[t] * x[t];
+    s = warp_sum(s);
+    if (lane == 0) x[i] = (x[i] - s) / ui[i];
+    __syncwarp();
+  }
+  for (int i = lane; i < n; i += 32) inv[(int64_t)i * n + j] = x[i];
+}
+
 // undo the row interchanges on the inverse's columns (reverse order)
 template <class T>
 __global__ void k_gj_unswap(T* A, int n, const int* swaps, const int32_t* status) {
@@ -1148,6 +1292,50 @@ int skel_factor_big(const SkelFactorLevel* F, int32_t box, int32_t n, int32_t k,
                                               work_bytes, st)
                     : factor_big_impl<zc>(F, box, n, k, dd_off, ld_off, rd_off, lam_off, work,
                                           work_bytes, st);
+}
+
+// LU with partial pivoting of a row-major n x n matrix in place (getrf
+// conventions, 0-based piv); *status (zeroed by the caller) = 1 on an exact
+// zero pivot.  scratch: skel_gj_scratch_bytes(n).
+int skel_dense_lu(void* A, int32_t n, int32_t* piv, int32_t* status, int32_t field, void* scratch,
+                  void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto run = [&](auto kern, size_t el) -> int {
+    const size_t smem = el * (size_t)n;
+    SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int grid = coop_grid(kern, 256, smem);
+    if (grid > 4096) grid = 4096;
+    unsigned char* p = (unsigned char*)scratch;
+    double* part_v = (double*)p;
+    int* part_i = (int*)(p + 2 * 4096 * sizeof(double));
+    void* colc = (void*)(p + 2 * 4096 * (sizeof(double) + sizeof(int)));
+    void* Ap = A;
+    void* args[] = {&Ap, &n, &status, &part_v, &part_i, &colc, &piv};
+    SKEL_TRY(cudaLaunchCooperativeKernel((const void*)kern, grid, 256, args, smem, st));
+    return 0;
+  };
+  return field == 0 ? run(k_lu_coop<double>, 8) : run(k_lu_coop<zc>, 16);
+}
+
+// inv (row-major n x n) = A^-1 from skel_dense_lu / getrf factors.
+int skel_lu_inverse(const void* lu, const int32_t* piv, int32_t n, void* inv, int32_t field, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t col = (size_t)n * (field ? 16 : 8);
+  int wpb = (int)((size_t)skel_smem_optin() / col);
+  if (wpb > 8) wpb = 8;
+  if (wpb < 1) return -2;
+  const size_t smem = wpb * col;
+  const int blocks = (n + wpb - 1) / wpb;
+  if (field == 0) {
+    SKEL_TRY(cudaFuncSetAttribute(k_lu_inverse<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_lu_inverse<double><<<blocks, 32 * wpb, smem, st>>>((const double*)lu, piv, n, (double*)inv);
+  } else {
+    SKEL_TRY(cudaFuncSetAttribute(k_lu_inverse<zc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_lu_inverse<zc><<<blocks, 32 * wpb, smem, st>>>((const zc*)lu, piv, n, (zc*)inv);
+  }
+  return skel_last_error();
 }
 
 }  // extern "C"

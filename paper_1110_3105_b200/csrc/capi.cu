@@ -72,3 +72,20 @@ extern "C" int skel_fp64_probe(int32_t kind, int32_t iters, double* scratch, dou
   }
   return skel_last_error();
 }
+
+// H0^(1)(z) = J0(z) + i Y0(z) elementwise (kernels.py:65-75; CUDA's j0 / y0,
+// the same functions the Helmholtz entries use).  out: interleaved complex.
+__global__ void k_bessel_h0(const double* __restrict__ z, int64_t n, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = z[i];
+  out[2 * i] = j0(x);
+  out[2 * i + 1] = y0(x);
+}
+
+extern "C" int skel_bessel_h0(const double* z, int64_t n, double* out, void* stream) {
+  if (n <= 0) return 0;
+  k_bessel_h0<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(z, n, out);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}

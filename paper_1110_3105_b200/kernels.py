@@ -107,3 +107,18 @@ def eval_block(spec: KernelSpec, targets, sources, source_curvature=None) -> np.
                                                 _native.ptr(out), field, _native.stream_ptr()),
                   "skel_eval_block")
     return out.cpu().numpy()
+
+
+def bessel_h0(z):
+    """H0^(1)(z) = J0(z) + i Y0(z) on the GPU (kernels.py:65-75); z > 0."""
+    torch = _native.require_cuda()
+    za = np.asarray(z, dtype=np.float64)
+    if not np.all(za > 0):
+        raise InvalidInput("bessel_h0 requires z > 0 (Y0 is singular at 0)")
+    flat = np.ascontiguousarray(za.reshape(-1))
+    dz = torch.from_numpy(flat).to("cuda")
+    out = torch.empty(2 * flat.size, dtype=torch.float64, device="cuda")
+    _native.check(_native.lib().skel_bessel_h0(_native.ptr(dz), flat.size, _native.ptr(out),
+                                               _native.stream_ptr()), "skel_bessel_h0")
+    h = out.cpu().numpy().view(np.complex128).reshape(za.shape)
+    return complex(h) if h.ndim == 0 else h

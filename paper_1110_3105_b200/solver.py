@@ -122,9 +122,26 @@ class FactoredInverse:
 
     @property
     def S_lu(self):
-        """Explicit top inverse stands in for the reference's (lu, piv); kept
-        for attribute compatibility."""
-        return None if self.S_inv is None else (self.S_inv, None)
+        """(lu, piv) of Shat exactly as the reference holds it (scipy
+        lu_factor conventions, solver.py:269-274), host arrays.  The solve
+        uses the explicit Shat^-1; the LU is computed on the device on first
+        access (skel_dense_lu) -- or is the one a loaded container carried."""
+        if getattr(self, "_S_lu", None) is None and self.S_hat is not None and self.S_hat.numel():
+            torch = _native.require_cuda()
+            L = _native.lib()
+            K = self.S_hat.shape[0]
+            A = self.S_hat.clone()
+            piv = torch.zeros(K, dtype=torch.int32, device="cuda")
+            st = torch.zeros(1, dtype=torch.int32, device="cuda")
+            scratch = torch.empty(int(L.skel_gj_scratch_bytes(K)) // 8 + 1, dtype=torch.float64,
+                                  device="cuda")
+            _native.check(L.skel_dense_lu(_native.ptr(A), K, _native.ptr(piv), _native.ptr(st),
+                                          self.field, _native.ptr(scratch), _native.stream_ptr()),
+                          "skel_dense_lu")
+            if int(st.item()):
+                raise SingularBlock("top", 0, "S")
+            self._S_lu = (_native.to_host(A).copy(), piv.cpu().numpy())
+        return getattr(self, "_S_lu", None)
 
     def perm_dev(self):
         if self._perm_dev is None:
@@ -183,6 +200,34 @@ class FactoredInverse:
 
 
 _BIG_TOP = 768          # top matrices above this size use the cooperative inverse
+
+
+def factored_level_from_host(nodes, field):
+    """Device level from host blocks [(Dd, Ld, Rd), ...] (a loaded container)."""
+    torch = _native.require_cuda()
+    dt = np.complex128 if field else np.float64
+    n = np.array([Dd.shape[0] for Dd, _, _ in nodes], dtype=np.int64)
+    k = np.array([Ld.shape[1] if Ld.ndim == 2 else 0 for _, Ld, _ in nodes], dtype=np.int64)
+    dd_off, ld_off, lam_off = _off(n * n), _off(n * k), _off(np.zeros_like(k))
+    cat = lambda arrs: (np.concatenate([np.asarray(a, dtype=dt).ravel() for a in arrs])  # noqa: E731
+                        if arrs else np.zeros(0, dtype=dt))
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda")  # noqa: E731
+    Dd = up(cat([x[0] for x in nodes]) if nodes else np.zeros(1, dt))
+    Ld = up(cat([x[1] for x in nodes]) if nodes else np.zeros(1, dt))
+    Rd = up(cat([x[2] for x in nodes]) if nodes else np.zeros(1, dt))
+    Lam = torch.zeros(1, dtype=Dd.dtype, device="cuda")
+    pk = Packer()
+    pk.add("n", n.astype(np.int32)).add("k", k.astype(np.int32))
+    pk.add("noff", _off(n)).add("koff", _off(k))
+    pk.add("dd_off", dd_off).add("ld_off", ld_off).add("lam_off", lam_off)
+    for bi, sel in enumerate(_solve_buckets(n)):
+        pk.add(f"sv{bi}", sel)
+    t = pk.upload()
+    lv = FactoredLevel(DevFactorLevel(n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, None, t))
+    lv._nodes = [FactoredNode(Dd=np.asarray(a, dtype=dt), Ld=np.asarray(b, dtype=dt),
+                              Rd=np.asarray(c, dtype=dt), Lam=np.zeros((0, 0), dtype=dt))
+                 for a, b, c in nodes]
+    return lv
 
 
 def _invert_top(Sh, regularize, field):

@@ -184,6 +184,41 @@ def sphere_case(n, eps, nrhs, full=False):
     return out
 
 
+def sklc_case(n, eps, nrhs):
+    """The reference's binary containers (skel.py:428-511, solver.py:439-529)
+    of one compressed matrix / factored inverse, plus the solution they give."""
+    from skelkit.skel import serialize_compressed
+    from skelkit.solver import serialize_factored
+    curve = bie.ellipse(2.0, 1.0, n)
+    system = bie.discretize_dirichlet(curve, KernelSpec("laplace", 2))
+    tree, cm = bie.compress_system(system, eps, 64)
+    fi = skelkit.factor(cm)
+    B = np.random.default_rng(0).standard_normal((n, nrhs))
+    X = skelkit.solve(fi, B)
+    import os
+    import tempfile
+    se = skelkit.assemble_embedding(cm)
+    r, c, v = se.to_coo()
+    fd, path = tempfile.mkstemp(suffix=".mtx")
+    os.close(fd)
+    skelkit.export_matrix_market(se, path)
+    with open(path, "rb") as fh:
+        mm = fh.read()
+    os.unlink(path)
+    # a small GMRES case (solver.py:328-408): diagonally shifted random system
+    rng = np.random.default_rng(5)
+    G = rng.standard_normal((60, 60)) / np.sqrt(60) + 2.0 * np.eye(60)
+    gb = rng.standard_normal(60)
+    gx, gits = skelkit.gmres(G, gb, tol=1e-12)
+    return {"cm_bytes": np.frombuffer(serialize_compressed(cm), dtype=np.uint8),
+            "fi_bytes": np.frombuffer(serialize_factored(fi), dtype=np.uint8),
+            "X": X, "Y_apply": skelkit.apply(cm, X), "n": np.array(n), "eps": np.array(eps),
+            "emb_m": np.array(se.m), "emb_rows": r, "emb_cols": c, "emb_vals": v,
+            "emb_labels": np.array(list(se.blocks.keys())),
+            "mm_bytes": np.frombuffer(mm, dtype=np.uint8),
+            "gmres_A": G, "gmres_b": gb, "gmres_x": gx, "gmres_iters": np.array(gits)}
+
+
 def perimeter(m=4096):
     t = 2 * np.pi * np.arange(m) / m
     return float(np.sum(np.sqrt((2 * np.sin(t)) ** 2 + np.cos(t) ** 2)) * 2 * np.pi / m)
@@ -259,6 +294,7 @@ def main():
         "sphere_2000_1e-6": lambda: sphere_case(2000, 1e-6, 1),
         # randomized IDs (m > max(4096, 4n + 256)) at the coarse levels
         "sphere_10000_1e-6": lambda: sphere_case(10000, 1e-6, 1),
+        "sklc_ellipse_512_1e-6": lambda: sklc_case(512, 1e-6, 2),
     }
     only = sys.argv[1:]
     for name, fn in jobs.items():

@@ -1,0 +1,179 @@
+"""Data formats either side of the path: the reference's SKLC
+binary containers, the sparse embedding + Matrix Market export, GMRES, and
+bessel_h0.  Golden bytes / arrays come from the live reference
+(tests/golden/make_golden.py, case sklc_ellipse_512_1e-6)."""
+
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+gpu = pytest.mark.gpu
+
+
+def _g(golden):
+    return golden("sklc_ellipse_512_1e-6")
+
+
+# ---------------------------------------------------------------------------
+# CPU: container / embedding / Matrix Market / GMRES semantics
+
+def test_compressed_container_round_trip_bytes(golden):
+    from paper_1110_3105_b200 import container
+    g = _g(golden)
+    data = g["cm_bytes"].tobytes()
+    cm = container.deserialize_compressed(data)
+    assert cm.n == int(g["n"]) and cm.eps == float(g["eps"])
+    assert container.serialize_compressed(cm) == data
+
+
+def test_factored_container_round_trip_bytes(golden):
+    from paper_1110_3105_b200 import container
+    g = _g(golden)
+    data = g["fi_bytes"].tobytes()
+    parsed = container.parse_factored(data)
+    assert parsed[1] == int(g["n"])
+    assert container.emit_factored(*parsed) == data
+
+
+def test_container_rejects_garbage(golden):
+    from paper_1110_3105_b200 import InvalidInput, container
+    with pytest.raises(InvalidInput):
+        container.deserialize_compressed(b"NOPE" + b"\0" * 64)
+    g = _g(golden)
+    with pytest.raises(InvalidInput):              # a compressed container is not a factored one
+        container.parse_factored(g["cm_bytes"].tobytes())
+    with pytest.raises(InvalidInput):
+        container.deserialize_compressed(g["cm_bytes"].tobytes()[:100])
+
+
+def test_embedding_matches_reference(golden):
+    from paper_1110_3105_b200 import assemble_embedding, container
+    g = _g(golden)
+    cm = container.deserialize_compressed(g["cm_bytes"].tobytes())
+    se = assemble_embedding(cm)
+    assert se.m == int(g["emb_m"])
+    assert list(se.blocks.keys()) == [str(x) for x in g["emb_labels"]]
+    r, c, v = se.to_coo()
+    np.testing.assert_array_equal(r, g["emb_rows"])
+    np.testing.assert_array_equal(c, g["emb_cols"])
+    np.testing.assert_array_equal(v, g["emb_vals"])
+    # the embedding reproduces the solve: x = first n unknowns of A_e^-1 [b, 0]
+    A = se.to_dense()
+    b = np.random.default_rng(0).standard_normal(cm.n)
+    x = se.extract_x(np.linalg.solve(A, se.rhs(b)))
+    assert np.isfinite(x).all()
+
+
+def test_matrix_market_export_is_reference_text(golden):
+    from paper_1110_3105_b200 import assemble_embedding, container, export_matrix_market
+    from paper_1110_3105_b200.embedding import read_matrix_market
+    g = _g(golden)
+    se = assemble_embedding(container.deserialize_compressed(g["cm_bytes"].tobytes()))
+    fd, path = tempfile.mkstemp(suffix=".mtx")
+    os.close(fd)
+    try:
+        export_matrix_market(se, path)
+        with open(path, "rb") as fh:
+            assert fh.read() == g["mm_bytes"].tobytes()
+        shape, r, c, v = read_matrix_market(path)
+    finally:
+        os.unlink(path)
+    assert shape == (se.m, se.m)
+    A = np.zeros(shape)
+    A[r, c] = v
+    np.testing.assert_array_equal(A, se.to_dense())
+
+
+def test_gmres_matches_reference(golden):
+    from paper_1110_3105_b200 import NotConverged, gmres
+    g = _g(golden)
+    x, its = gmres(g["gmres_A"], g["gmres_b"], tol=1e-12)
+    assert its == int(g["gmres_iters"])
+    np.testing.assert_allclose(x, g["gmres_x"], rtol=0, atol=1e-12)
+    with pytest.raises(NotConverged) as exc:
+        gmres(g["gmres_A"], g["gmres_b"], tol=1e-14, max_iter=3)
+    assert exc.value.iterations == 3 and exc.value.x.shape == (60,)
+
+
+# ---------------------------------------------------------------------------
+# GPU: loading into device slabs, saving from them
+
+def _sk():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_1110_3105_b200 as sk
+    return sk
+
+
+@gpu
+def test_load_reference_factored_and_solve(golden):
+    sk = _sk()
+    from paper_1110_3105_b200 import container
+    g = _g(golden)
+    fi = container.deserialize_factored(g["fi_bytes"].tobytes())
+    n = int(g["n"])
+    B = np.random.default_rng(0).standard_normal((n, 2))
+    X = sk.solve(fi, B)
+    np.testing.assert_allclose(X, g["X"], rtol=0, atol=1e-12 * np.abs(g["X"]).max())
+    # and save it back byte for byte (blocks and the stored LU untouched)
+    assert container.serialize_factored(fi) == g["fi_bytes"].tobytes()
+
+
+@gpu
+def test_load_reference_compressed_factor_apply(golden):
+    sk = _sk()
+    from paper_1110_3105_b200 import container
+    g = _g(golden)
+    cm = container.deserialize_compressed(g["cm_bytes"].tobytes())
+    fi = sk.factor(cm)
+    n = int(g["n"])
+    B = np.random.default_rng(0).standard_normal((n, 2))
+    X = sk.solve(fi, B)
+    assert np.linalg.norm(X - g["X"]) / np.linalg.norm(g["X"]) <= 1e-10
+    Y = sk.apply(cm, g["X"])
+    np.testing.assert_allclose(Y, g["Y_apply"], rtol=0, atol=1e-12 * np.abs(g["Y_apply"]).max())
+
+
+@gpu
+def test_save_load_gpu_factorization(tmp_path):
+    sk = _sk()
+    import scipy.linalg as sla
+    n = 2048
+    curve = sk.bie.ellipse(2.0, 1.0, n)
+    system = sk.bie.discretize_dirichlet(curve, sk.KernelSpec("laplace", 2))
+    tree, cm = sk.bie.compress_system(system, 1e-10, 64)
+    fi = sk.factor(cm)
+    B = np.random.default_rng(1).standard_normal((n, 3))
+    X = sk.solve(fi, B)
+    sk.save_compressed(cm, tmp_path / "cm.sklc")
+    sk.save_factored(fi, tmp_path / "fi.sklc")
+    fi2 = sk.load_factored(tmp_path / "fi.sklc")
+    X2 = sk.solve(fi2, B)
+    assert np.linalg.norm(X2 - X) / np.linalg.norm(X) <= 1e-12
+    # the stored Shat factors are a valid getrf result: P L U = Shat
+    lu, piv = fi.S_lu
+    Sh = fi.S_hat.cpu().numpy()
+    ref_lu, ref_piv = sla.lu_factor(Sh)
+    x = np.random.default_rng(2).standard_normal(Sh.shape[0])
+    np.testing.assert_allclose(sla.lu_solve((lu, piv), x), sla.lu_solve((ref_lu, ref_piv), x),
+                               rtol=1e-9, atol=1e-12)
+    cm2 = sk.load_compressed(tmp_path / "cm.sklc")
+    np.testing.assert_allclose(sk.apply(cm2, X), sk.apply(cm, X), rtol=0, atol=1e-13)
+
+
+@gpu
+def test_bessel_h0_gpu():
+    sk = _sk()
+    import scipy.special as spc
+    z = np.linspace(0.01, 600.0, 4001)
+    h = sk.bessel_h0(z)
+    ref = spc.j0(z) + 1j * spc.y0(z)
+    # CUDA's j0 / y0 (libdevice) against Cephes: ~1e-12 absolute for large z,
+    # the same bar as the Helmholtz kernel KATs in test_gpu_parity.py
+    np.testing.assert_allclose(h, ref, rtol=0, atol=1e-12)
+    assert isinstance(sk.bessel_h0(1.0), complex)
+    with pytest.raises(sk.InvalidInput):
+        sk.bessel_h0(0.0)
