@@ -40,7 +40,13 @@ enum {
   /* KernelSource (skel.py:100-124) + optional `diag` on coincident indices */
   SKEL_SRC_KERNEL = 1,
   /* combined field (D_k - i k S_k) * KR10 + identity_coef (BASELINE config 3) */
-  SKEL_SRC_CFIE = 2
+  SKEL_SRC_CFIE = 2,
+  /* sound-hard multiple scattering (bie.py:305-367): target-normal derivative
+     of the 2D Helmholtz single layer, -(ik/4) H1(kr) (x-y).nu_x / r * w_y,
+     KR10 within a scatterer, + identity_coef (-1/2) on the diagonal; row
+     proxies = the same Neumann trace of the proxy field (unweighted), column
+     proxies = single layer * w */
+  SKEL_SRC_NTRACE = 3
 };
 
 typedef struct {
@@ -66,6 +72,12 @@ typedef struct {
   double diag;            /* added where row == col (KERNEL) */
   double wscale;          /* row-proxy scale (bie.py:251); 1 otherwise */
   double coincide_tol;    /* r < coincide_tol counts as coincident */
+  /* optional point groups (several scatterers in one source): KR10 applies
+     only within a group, on local indices (orig - grp_start[g]) cyclic in
+     grp_size[g]; NULL = one group of size n */
+  const int32_t* grp;     /* per ORIGINAL index */
+  const int64_t* grp_start;
+  const int64_t* grp_size;
 } SkelSource;
 
 /* ---- one cover (tree level) of the compression sweep -------------------- */

@@ -20,7 +20,7 @@ c_i64 = ctypes.c_int64
 c_f64 = ctypes.c_double
 c_vp = ctypes.c_void_p
 
-SRC_BIE, SRC_KERNEL, SRC_CFIE = 0, 1, 2
+SRC_BIE, SRC_KERNEL, SRC_CFIE, SRC_NTRACE = 0, 1, 2, 3
 EQ_LAPLACE, EQ_HELMHOLTZ = 0, 1
 LAYER_SINGLE, LAYER_DOUBLE = 0, 1
 
@@ -34,6 +34,7 @@ class SkelSource(ctypes.Structure):
         ("layer", c_i32), ("curvature_limit", c_i32), ("kr10", c_i32),
         ("k", c_f64), ("identity_coef", c_f64), ("diag", c_f64), ("wscale", c_f64),
         ("coincide_tol", c_f64),
+        ("grp", c_vp), ("grp_start", c_vp), ("grp_size", c_vp),
     ]
 
 

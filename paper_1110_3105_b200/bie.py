@@ -240,3 +240,228 @@ def dense_matvec(source, x):
     y = np.empty_like(X)
     y[perm] = yt.cpu().numpy()
     return y[:, 0] if single else y
+
+
+# ---------------------------------------------------------------------------
+# more curves, post-processing and CSV output (bie.py:98-114, 216-230, 282-300)
+
+def trefoil(n, center=(0.0, 0.0), scale=1.0) -> Curve2D:
+    """Three-lobed curve r(theta) = (2 + cos 3 theta) / 6 (bie.py:98-114)."""
+    if n < 8:
+        raise InvalidInput("need n >= 8")
+    t = 2 * np.pi * np.arange(n) / n
+    r = (2 + np.cos(3 * t)) / 6
+    dr = -np.sin(3 * t) / 2
+    ddr = -1.5 * np.cos(3 * t)
+    c, s = np.cos(t), np.sin(t)
+    xy = np.asarray(center) + scale * r[:, None] * np.column_stack([c, s])
+    tx = scale * (dr * c - r * s)
+    ty = scale * (dr * s + r * c)
+    speed = np.hypot(tx, ty)
+    kap = (r * r + 2 * dr * dr - r * ddr) / (r * r + dr * dr) ** 1.5 / scale
+    return Curve2D(t, xy, np.column_stack([ty, -tx]) / speed[:, None], kap,
+                   speed * (2 * np.pi / n))
+
+
+def eval_interior(curve: Curve2D, density, spec: KernelSpec, targets) -> np.ndarray:
+    """Double-layer potential of ``density`` at interior targets (trapezoid
+    rule, bie.py:216-230); the kernel block is evaluated on the GPU."""
+    import warnings
+
+    from .errors import AccuracyWarning
+    targets = np.atleast_2d(np.asarray(targets, dtype=np.float64))
+    for p in targets:
+        if not contains(curve, p):
+            raise InvalidInput(f"target {p} is not interior")
+    d = np.min(np.linalg.norm(curve.xy[None, :, :] - targets[:, None, :], axis=2), axis=1)
+    if np.any(d < 2 * curve.node_spacing()):
+        warnings.warn("target within 2 node spacings of the boundary; quadrature accuracy "
+                      "degrades near the curve", AccuracyWarning, stacklevel=2)
+    blk = eval_block(KernelSpec(spec.equation, 2, "double", spec.wavenumber), PointSet(targets),
+                     curve.point_set())
+    return blk @ np.asarray(density)
+
+
+def write_density_csv(path, curve: Curve2D, density):
+    """t, x, y, re(sigma), im(sigma) per node (bie.py:282-289)."""
+    density = np.asarray(density)
+    with open(path, "w") as f:
+        f.write("t,x,y,sigma_re,sigma_im\n")
+        f.writelines(f"{curve.t[i]:.17g},{curve.xy[i, 0]:.17g},{curve.xy[i, 1]:.17g},"
+                     f"{np.real(density[i]):.17g},{np.imag(density[i]):.17g}\n" for i in range(curve.n))
+
+
+def write_field_csv(path, points, values):
+    """x, y, re(u), im(u) per sample (bie.py:292-299)."""
+    points = np.atleast_2d(np.asarray(points))
+    values = np.asarray(values)
+    with open(path, "w") as f:
+        f.write("x,y,u_re,u_im\n")
+        f.writelines(f"{p[0]:.17g},{p[1]:.17g},{np.real(v):.17g},{np.imag(v):.17g}\n"
+                     for p, v in zip(points, values))
+
+
+# ---------------------------------------------------------------------------
+# multiple scattering by sound-hard obstacles (bie.py:305-459): single-layer
+# representation, Neumann-trace system, block-diagonal skeletonized
+# preconditioner, GMRES (krylov.gmres)
+
+def _curves_resident(curves):
+    xy = np.concatenate([c.xy for c in curves])
+    nrm = np.concatenate([c.normals for c in curves])
+    w = np.concatenate([c.weights for c in curves])
+    kap = np.concatenate([c.curvature for c in curves])
+    return ResidentPoints(xy, nrm, w, kap)
+
+
+class ScattererSource(_DeviceSourceMixin):
+    """Self-block of one scatterer in tree order (bie.py:326-349): Neumann
+    trace of the Helmholtz single layer with KR10 and the -1/2 jump; row
+    proxies are the Neumann trace of the proxy field, column proxies the
+    weighted single layer (entries: csrc/entries.cuh, SKEL_SRC_NTRACE)."""
+
+    def __init__(self, scat, perm):
+        self.scat = scat
+        self.perm = np.asarray(perm)
+        self.n = scat.npts
+        self.dtype = np.complex128
+        self.wavenumber = scat.k
+        self.geo = DeviceGeometry(None, self.perm, resident=scat.resident())
+
+    def _desc(self):
+        return self.geo.source(_native.SRC_NTRACE, _native.EQ_HELMHOLTZ, _native.LAYER_SINGLE,
+                               self.scat.k, identity_coef=-0.5, kr10=True)
+
+
+class Scatterer:
+    def __init__(self, curve: Curve2D, k):
+        self.curve = curve
+        self.k = float(k)
+        self.points = curve.point_set()
+        self.npts = curve.n
+        self._res = None
+
+    def resident(self):
+        if self._res is None:
+            self._res = _curves_resident([self.curve])
+        return self._res
+
+    def self_block(self, rows, cols):
+        """Dense self-interaction block on ORIGINAL indices (bie.py:359-367)."""
+        src = ScattererSource(self, np.arange(self.npts))
+        return src.block(np.asarray(rows), np.asarray(cols))
+
+
+class _SystemSource(_DeviceSourceMixin):
+    """All scatterers as one source (original order): KR10 only inside a
+    scatterer (point groups), -1/2 on the diagonal, plain Neumann trace
+    between scatterers (bie.py:386-398)."""
+
+    def __init__(self, system):
+        torch = _native.require_cuda()
+        self.system = system
+        off = system.offsets()
+        self.n = int(off[-1])
+        self.dtype = np.complex128
+        self.wavenumber = system.k
+        self.perm = np.arange(self.n)
+        res = _curves_resident([s.curve for s in system.scatterers])
+        self.geo = DeviceGeometry(None, self.perm, resident=res)
+        grp = np.repeat(np.arange(len(system.scatterers)), np.diff(off)).astype(np.int32)
+        self._grp = torch.from_numpy(grp).to("cuda")
+        self._gstart = torch.from_numpy(off[:-1].astype(np.int64)).to("cuda")
+        self._gsize = torch.from_numpy(np.diff(off).astype(np.int64)).to("cuda")
+
+    def _desc(self):
+        s = self.geo.source(_native.SRC_NTRACE, _native.EQ_HELMHOLTZ, _native.LAYER_SINGLE,
+                            self.system.k, identity_coef=-0.5, kr10=True)
+        s.grp = _native.ptr(self._grp)
+        s.grp_start = _native.ptr(self._gstart)
+        s.grp_size = _native.ptr(self._gsize)
+        return s
+
+
+@dataclass
+class ScatteringSystem:
+    """A_ii = -I/2 + K_ii (KR10), A_ij = K_ij: K the target-normal derivative
+    of the Helmholtz single layer; incoming plane wave exp(i k x2)."""
+
+    scatterers: list
+    k: float
+
+    def __post_init__(self):
+        self._src = None
+
+    @property
+    def n(self):
+        return sum(s.npts for s in self.scatterers)
+
+    def offsets(self):
+        return np.concatenate([[0], np.cumsum([s.npts for s in self.scatterers])]).astype(np.int64)
+
+    def source(self):
+        if self._src is None:
+            self._src = _SystemSource(self)
+        return self._src
+
+    def matrix(self):
+        """Dense system matrix (evaluated on the GPU)."""
+        idx = np.arange(self.n)
+        return self.source().block(idx, idx)
+
+    def apply(self, x):
+        """y = A x with exact entries evaluated on the fly (no N x N storage)."""
+        return dense_matvec(self.source(), x)
+
+    def rhs_plane_wave(self):
+        """-d/dnu of u_inc = exp(i k x2) on every boundary (bie.py:400-406)."""
+        return np.concatenate([-1j * self.k * s.curve.normals[:, 1] * np.exp(1j * self.k * s.curve.xy[:, 1])
+                               for s in self.scatterers])
+
+    def precond_blocks(self, eps=1e-6, max_leaf_size=None):
+        """Skeletonized factorization of every isolated self-system (GPU)."""
+        facs = []
+        for s in self.scatterers:
+            tree = build_tree(s.points, max_leaf_size)
+            cm = compress_source(ScattererSource(s, tree.perm), tree, eps)
+            facs.append(factor(cm))
+        return facs
+
+    def precond_apply(self, facs):
+        off = self.offsets()
+
+        def apply_pinv(x):
+            x = np.asarray(x, dtype=np.complex128)
+            out = np.empty_like(x)
+            for i, fi in enumerate(facs):
+                out[off[i]:off[i + 1]] = solve(fi, x[off[i]:off[i + 1]])
+            return out
+
+        return apply_pinv
+
+    def scattered_field(self, densities, targets):
+        """Single-layer field of the densities at exterior points (bie.py:429-438)."""
+        targets = np.atleast_2d(np.asarray(targets, dtype=np.float64))
+        off = self.offsets()
+        spec = KernelSpec("helmholtz", 2, "single", self.k)
+        out = np.zeros(targets.shape[0], dtype=np.complex128)
+        for i, s in enumerate(self.scatterers):
+            out += eval_block(spec, PointSet(targets), s.points) @ np.asarray(densities)[off[i]:off[i + 1]]
+        return out
+
+
+def scattering_system(scatterers, k) -> ScatteringSystem:
+    """Validate the geometry (pairwise disjoint, bie.py:441-459) and build the system."""
+    if k <= 0:
+        raise InvalidInput("wavenumber must be positive")
+    curves = list(scatterers)
+    for i in range(len(curves)):
+        for j in range(i + 1, len(curves)):
+            a, b = curves[i], curves[j]
+            la, ha = a.xy.min(0), a.xy.max(0)
+            lb, hb = b.xy.min(0), b.xy.max(0)
+            if (np.all(la <= hb) and np.all(lb <= ha)
+                    and (contains(a, b.xy.mean(0)) or contains(b, a.xy.mean(0))
+                         or contains(a, b.xy[0]) or contains(b, a.xy[0]))):
+                raise InvalidInput(f"scatterers {i} and {j} overlap")
+    return ScatteringSystem([Scatterer(c, k) for c in curves], k)

@@ -54,8 +54,17 @@ __device__ __forceinline__ double sk_ndot_neg(const SkelSource& S, double dx, do
 }
 
 __device__ __forceinline__ double kr10_factor(const SkelSource& S, int64_t oi, int64_t oj) {
+  int64_t nn = S.n;
+  if (S.grp) {
+    const int g = __ldg(S.grp + oi);
+    if (g != __ldg(S.grp + oj)) return 1.0;
+    const int64_t b = __ldg(S.grp_start + g);
+    oi -= b;
+    oj -= b;
+    nn = __ldg(S.grp_size + g);
+  }
   int64_t d = oi > oj ? oi - oj : oj - oi;
-  int64_t d2 = S.n - d;
+  int64_t d2 = nn - d;
   if (d2 < d) d = d2;
   if (d >= 1 && d <= 10) return __dadd_rn(1.0, c_kr10[d - 1]);
   return 1.0;
@@ -116,7 +125,12 @@ __device__ __forceinline__ T entry_A(const SkelSource& S, const Pt& t, const Pt&
   bool same = r < S.coincide_tol;
   bool helm = S.equation == SKEL_EQ_HELMHOLTZ;
   T g;
-  if (S.kind == SKEL_SRC_CFIE) {
+  if (S.kind == SKEL_SRC_NTRACE) {
+    // -(ik/4) H1(kr) (x - y).nu_x / r * w_y  (bie.py:305-323)
+    zc v(0.0);
+    if (!same) v = helm_dl(S, -__dadd_rn(__dmul_rn(dx, t.nx), __dmul_rn(dy, t.ny)), r);
+    g = from_zc<T>(zc(v.re * s.w, v.im * s.w));
+  } else if (S.kind == SKEL_SRC_CFIE) {
     zc v(0.0);
     if (!same) {
       double e = sk_ndot_neg(S, dx, dy, dz, s);
@@ -167,7 +181,14 @@ __device__ __forceinline__ T proxy_G(const SkelSource& S, double dx, double dy, 
 template <class T>
 __device__ __forceinline__ T entry_proxy_row(const SkelSource& S, const Pt& t, double px,
                                              double py, double pz) {
-  T g = proxy_G<T>(S, __dsub_rn(t.x, px), __dsub_rn(t.y, py), __dsub_rn(t.z, pz));
+  const double dx = __dsub_rn(t.x, px), dy = __dsub_rn(t.y, py), dz = __dsub_rn(t.z, pz);
+  if (S.kind == SKEL_SRC_NTRACE) {
+    // Neumann trace of the proxy's single-layer field, unweighted (bie.py:342-344)
+    const double r = sk_dist(S, dx, dy, dz);
+    if (r < S.coincide_tol) return as_T<T>(0.0);
+    return from_zc<T>(helm_dl(S, -__dadd_rn(__dmul_rn(dx, t.nx), __dmul_rn(dy, t.ny)), r));
+  }
+  T g = proxy_G<T>(S, dx, dy, dz);
   return g * S.wscale;
 }
 

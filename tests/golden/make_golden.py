@@ -219,6 +219,27 @@ def sklc_case(n, eps, nrhs):
             "gmres_A": G, "gmres_b": gb, "gmres_x": gx, "gmres_iters": np.array(gits)}
 
 
+def scattering_case(n, k):
+    """Two sound-hard trefoils (bie.py:305-459): system entries (a sample),
+    plane-wave data, block-preconditioned GMRES, scattered field."""
+    curves = [bie.trefoil(n, center=(-0.6, 0.0), scale=1.0), bie.trefoil(n, center=(0.6, 0.1), scale=0.8)]
+    sysm = bie.scattering_system(curves, k)
+    A = sysm.matrix()
+    rng = np.random.default_rng(9)
+    ii = rng.integers(0, A.shape[0], 3000)
+    jj = rng.integers(0, A.shape[0], 3000)
+    diag = np.arange(A.shape[0])
+    b = sysm.rhs_plane_wave()
+    facs = sysm.precond_blocks(1e-8, 32)
+    x, its = skelkit.gmres(A, b, tol=1e-10, precond=sysm.precond_apply(facs))
+    tg = np.array([[3.0, 0.5], [-2.5, -1.0], [0.0, 2.5]])
+    return {"ii": ii, "jj": jj, "A_sample": A[ii, jj], "A_diag": A[diag, diag],
+            "A_row0": A[0], "A_row_last": A[-1], "rhs": b, "x": x, "iters": np.array(its),
+            "field_targets": tg, "field": sysm.scattered_field(x, tg), "n": np.array(n),
+            "k": np.array(k), "ranks": np.array([f_.levels[0].nodes[0].Ld.shape[1] if f_.levels else 0
+                                                  for f_ in facs])}
+
+
 def perimeter(m=4096):
     t = 2 * np.pi * np.arange(m) / m
     return float(np.sum(np.sqrt((2 * np.sin(t)) ** 2 + np.cos(t) ** 2)) * 2 * np.pi / m)
@@ -295,6 +316,7 @@ def main():
         # randomized IDs (m > max(4096, 4n + 256)) at the coarse levels
         "sphere_10000_1e-6": lambda: sphere_case(10000, 1e-6, 1),
         "sklc_ellipse_512_1e-6": lambda: sklc_case(512, 1e-6, 2),
+        "scattering_2x256_k3": lambda: scattering_case(256, 3.0),
     }
     only = sys.argv[1:]
     for name, fn in jobs.items():
