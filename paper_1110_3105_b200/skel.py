@@ -529,6 +529,21 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         big &= (_bigbox_randomized(m0, nr) | _bigbox_randomized(m1, nc)
                 | (need_n > _BIG_N) | (_level_smem_fixed_vec(need_n, field) > optin))
         cls = np.where((own > 0) & ~big, cls, -1)
+        merged = None
+        if p <= _SMALL_LEVEL:
+            # few boxes: they all run at once anyway -- one launch for every
+            # box whose target fits shared memory.  Decided and sized over ALL
+            # boxes of the level (not just this rank's), so the kernel
+            # configuration -- hence every rounding -- is the same for any
+            # number of ranks
+            fits_all = (~big | (own == 0)) & (_level_smem_fixed_vec(need_n, field) + wb <= optin)
+            if fits_all.any():
+                mm = (int(need_m[fits_all].max()), int(need_n[fits_all].max()),
+                      int((need_m[fits_all] * need_n[fits_all]).max()))
+                if _level_smem_fixed(mm[1], field) + mm[2] * elem <= optin:
+                    fits = fits_all & (cls >= 0)
+                    cls = np.where(fits, 0, np.where(cls >= 0, cls + 1, -1))
+                    merged = mm
         buckets = size_buckets(cls, wb)
         _ht and _ht.mark("prep")
         pk = Packer()
@@ -580,6 +595,8 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         for bi, sel in enumerate(buckets):
             max_m, max_n = int(need_m[sel].max()), int(need_n[sel].max())
             max_w = int((need_m[sel] * need_n[sel]).max())
+            if merged is not None and cls[sel[0]] == 0:
+                max_m, max_n, max_w = merged
             fixed = _level_smem_fixed(max_n, field)
             if fixed + max_w * elem > optin:
                 sb = 2 * sel.size * max_w * elem
@@ -745,6 +762,7 @@ def _smem_optin():
 
 
 _BIG_N = 512                 # boxes wider than this take the whole-GPU path
+_SMALL_LEVEL = 400           # levels with at most this many boxes: one ID launch
 
 
 def _bigbox_randomized(m, n):

@@ -292,7 +292,19 @@ class FactorRun:
         cls = np.searchsorted(np.asarray(_FAC_CLASSES), need, side="left")
         # big boxes (3D coarse levels): one box at a time over the whole GPU
         big = n_own >= _BIG_FAC_N
-        buckets = size_buckets(np.where((n_own > 0) & ~big, cls, -1), need)
+        fcls = np.where((n_own > 0) & ~big, cls, -1)
+        merged = None
+        if n.size <= 400:
+            # few boxes: one launch for all that fit shared memory (decided
+            # and sized over all boxes of the level, for any number of ranks)
+            fits_all = (n > 0) & (n < _BIG_FAC_N) & (need + 1024 + 4 * n <= optin)
+            if fits_all.any():
+                mn, mk = int(n[fits_all].max()), int(k[fits_all].max())
+                if (mn * mn + 4 * mn * mk + mk * mk + 3 * mn) * elem + 1024 + 4 * mn <= optin:
+                    fits = fits_all & (fcls >= 0)
+                    fcls = np.where(fits, 0, np.where(fcls >= 0, fcls + 1, -1))
+                    merged = (mn, mk)
+        buckets = size_buckets(fcls, need)
         p = dl.p
         outer = torch.cuda.stream(self.stream) if self.stream is not None else _nullctx()
         with outer:
@@ -334,6 +346,8 @@ class FactorRun:
             for bi, sel in enumerate(buckets):
                 max_n = int(n[sel].max())
                 max_k = int(k[sel].max())
+                if merged is not None and fcls[sel[0]] == 0:
+                    max_n, max_k = merged
                 nd = (max_n * max_n + 4 * max_n * max_k + max_k * max_k + 3 * max_n) * elem
                 F.order, F.nrun = p_(t[f"order{bi}"]), sel.size
                 F.scratch, F.scratch_bytes = None, 0
