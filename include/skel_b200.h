@@ -225,6 +225,31 @@ int skel_dense_inverse(void* A, void* lu, int32_t* ipiv, int32_t K, double regul
 /* out[2i], out[2i+1] = Re, Im of H0^(1)(z[i]) = J0 + i Y0 (kernels.py:65-75). */
 int skel_bessel_h0(const double* z, int64_t n, double* out, void* stream);
 
+/* ---- host planning of one level (csrc/plan.cpp) --------------------------
+ * The index bookkeeping of compress_source / factor per level in one native
+ * pass: dof / slab offsets, target heights (sum of neighbour dofs + proxies),
+ * size classes, big-box selection (randomized-ID selector skel.py:419-421,
+ * width, shared-memory fit), size-bucketed launch orders (class ascending,
+ * size descending).  `merged` = {flag, max_m, max_n, max_w} (ID) or
+ * {flag, max_n, max_k} (factor): levels with <= small_level boxes launch
+ * every fitting box at once, configured over the whole level. */
+int skel_plan_id_level(int64_t p, const int64_t* nr, const int64_t* nc, const int64_t* noff,
+                       const int64_t* nidx, const int64_t* neff, const uint8_t* own, int32_t elem,
+                       int64_t optin, const int64_t* wcls, int32_t n_wcls, const int64_t* mcls,
+                       int32_t n_mcls, int64_t big_n, int64_t rand_cut, int64_t small_level,
+                       int64_t* rdof_off, int64_t* cdof_off, int64_t* m0, int64_t* m1,
+                       int64_t* d_off, int64_t* l_off, int64_t* r_off, int64_t* need_m,
+                       int64_t* need_n, uint8_t* big, int32_t* order, int32_t* bstart,
+                       int32_t* nbuckets, int64_t* merged);
+int skel_plan_factor_level(int64_t p, const int64_t* nr, const int64_t* nc, const int64_t* kr,
+                           const int64_t* kc, const uint8_t* own, int32_t elem, int64_t optin,
+                           const int64_t* fcls, int32_t n_fcls, int64_t big_n, int64_t small_level,
+                           const int64_t* scls, int32_t n_scls, int64_t* n, int64_t* k,
+                           uint8_t* sq_bad, uint8_t* lam_bad, int64_t* dd_off, int64_t* ld_off,
+                           int64_t* lam_off, int64_t* noff, int64_t* koff, uint8_t* big,
+                           int32_t* order, int32_t* bstart, int32_t* nbuckets, int32_t* sorder,
+                           int32_t* sstart, int32_t* nsbuckets, int64_t* merged);
+
 /* ---- big boxes (one box over the whole GPU; csrc/big.cu) ---------------
  * Used for boxes whose target does not fit a per-box CTA (3D coarse levels)
  * and for every target the reference sends to id_randomized

@@ -108,6 +108,10 @@ _SIGS = {
     "skel_factor_big_bytes": [c_i32, c_i32, c_i32],
     "skel_dense_lu": [c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp],
     "skel_bessel_h0": [c_vp, c_i64, c_vp, c_vp],
+    "skel_plan_id_level": [c_i64] + [c_vp] * 6 + [c_i32, c_i64, c_vp, c_i32, c_vp, c_i32, c_i64, c_i64,
+                                                  c_i64] + [c_vp] * 14,
+    "skel_plan_factor_level": [c_i64] + [c_vp] * 5 + [c_i32, c_i64, c_vp, c_i32, c_i64, c_i64, c_vp,
+                                                      c_i32] + [c_vp] * 17,
     "skel_lu_inverse": [c_vp, c_vp, c_i32, c_vp, c_i32, c_vp],
     "skel_factor_big": [_P(SkelFactorLevel), c_i32, c_i32, c_i32, c_i64, c_i64, c_i64, c_i64, c_vp,
                         c_i64, c_i32, c_vp],

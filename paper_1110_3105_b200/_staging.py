@@ -133,7 +133,7 @@ def eager_stream():
     return side_streams(1, "eager")[0]
 
 
-def size_buckets(cls, key):
+def size_buckets(cls, key=None):
     """Group positions by class (cls >= 0; negative = excluded), each group
     ordered by descending key with ties by position: one lexsort instead of
     a nonzero / argsort per class.  Returns a list of int32 index arrays in
@@ -142,6 +142,13 @@ def size_buckets(cls, key):
     keep = np.flatnonzero(cls >= 0)
     if keep.size == 0:
         return []
+    if key is None:
+        # grouping only: a stable radix sort of the (small) class ids
+        c = cls[keep].astype(np.int16)
+        order = np.argsort(c, kind="stable")
+        idx = keep[order].astype(np.int32)
+        cs = c[order]
+        return np.split(idx, np.flatnonzero(cs[1:] != cs[:-1]) + 1)
     c = cls[keep].astype(np.int64)
     k = np.asarray(key)[keep].astype(np.int64)
     # one stable argsort of (class, -key) packed into an int64

@@ -24,6 +24,7 @@ from ._device import DeviceGeometry
 from .errors import InvalidInput, RefusedTooLarge
 from .geom import OrthTree, PointSet
 from .kernels import KernelSpec
+from ._plan import plan_id_level
 from ._staging import Packer, eager_stream, fork, join, on_stream, size_buckets
 
 DEFAULT_N_PROXY = {2: 64, 3: 512}        # skel.py:29
@@ -508,43 +509,18 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             nr = _segment_sum(prev.kr, child_off)
             nc = _segment_sum(prev.kc, child_off)
             rdofs, cdofs = prev.rskel, prev.cskel
-        rdof_off, cdof_off = _off(nr), _off(nc)
         neff = geo.neff
-        m0 = _segment_sum(nc[nidx], noff) + neff
-        m1 = _segment_sum(nr[nidx], noff) + neff
-        # slab slots only for this rank's boxes (all boxes when unsharded)
-        d_off, l_off, r_off = _off(nr * nc * own), _off(nr * nr * own), _off(nc * nc * own)
-        # size buckets: each launch gets a tight shared-memory footprint (so
-        # small boxes run several CTAs per SM) and a register tile matched to
-        # its tallest target; buckets run concurrently on side streams
-        need_m = np.maximum(m0, m1)
-        need_n = np.maximum(np.maximum(nr, nc), 1)
-        wb = need_m * need_n * elem
-        cls = (np.searchsorted(np.asarray(_W_CLASSES), wb, side="left") * 16
-               + np.searchsorted(np.asarray(_M_CLASSES), need_m, side="left"))
-        buckets = []
-        # big boxes: targets the reference hands to id_randomized, or too
-        # large for one CTA -> one box at a time over the whole GPU (big.cu)
-        big = own > 0
-        big &= (_bigbox_randomized(m0, nr) | _bigbox_randomized(m1, nc)
-                | (need_n > _BIG_N) | (_level_smem_fixed_vec(need_n, field) > optin))
-        cls = np.where((own > 0) & ~big, cls, -1)
-        merged = None
-        if p <= _SMALL_LEVEL:
-            # few boxes: they all run at once anyway -- one launch for every
-            # box whose target fits shared memory.  Decided and sized over ALL
-            # boxes of the level (not just this rank's), so the kernel
-            # configuration -- hence every rounding -- is the same for any
-            # number of ranks
-            fits_all = (~big | (own == 0)) & (_level_smem_fixed_vec(need_n, field) + wb <= optin)
-            if fits_all.any():
-                mm = (int(need_m[fits_all].max()), int(need_n[fits_all].max()),
-                      int((need_m[fits_all] * need_n[fits_all]).max()))
-                if _level_smem_fixed(mm[1], field) + mm[2] * elem <= optin:
-                    fits = fits_all & (cls >= 0)
-                    cls = np.where(fits, 0, np.where(cls >= 0, cls + 1, -1))
-                    merged = mm
-        buckets = size_buckets(cls, wb)
+        # offsets, target heights, size classes, big boxes, launch buckets:
+        # one native pass (csrc/plan.cpp)
+        pl = plan_id_level(nr, nc, noff, nidx, neff, None if mine is None else own, elem, optin,
+                           _W_CLASSES, _M_CLASSES, _BIG_N, 4096, _SMALL_LEVEL)
+        rdof_off, cdof_off = pl.rdof_off, pl.cdof_off
+        m0, m1 = pl.m0, pl.m1
+        d_off, l_off, r_off = pl.d_off, pl.l_off, pl.r_off
+        need_m, need_n = pl.need_m, pl.need_n
+        big = pl.big
+        buckets = pl.buckets
+        merged = pl.merged if pl.merged_first else None
         _ht and _ht.mark("prep")
         pk = Packer()
         pk.add("rdof_off", rdof_off).add("cdof_off", cdof_off)
@@ -595,7 +571,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         for bi, sel in enumerate(buckets):
             max_m, max_n = int(need_m[sel].max()), int(need_n[sel].max())
             max_w = int((need_m[sel] * need_n[sel]).max())
-            if merged is not None and cls[sel[0]] == 0:
+            if merged is not None and bi == 0:
                 max_m, max_n, max_w = merged
             fixed = _level_smem_fixed(max_n, field)
             if fixed + max_w * elem > optin:

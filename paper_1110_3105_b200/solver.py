@@ -16,6 +16,7 @@ import numpy as np
 
 from . import _native, _profile
 from .errors import InvalidInput, SingularBlock
+from ._plan import plan_factor_level
 from ._staging import Packer, fork, join, on_stream, size_buckets
 from .skel import CompressedMatrix, _dense_apply, _nullctx, _off
 
@@ -37,7 +38,7 @@ class FactoredNode:
 
 class DevFactorLevel:
     def __init__(self, n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, child_off, t, n_own=None,
-                 mine=None):
+                 mine=None, sv=None):
         self.p = n.size
         self.mine = mine            # sharded level: boolean mask of this rank's boxes
         self.n, self.k = n, k
@@ -53,8 +54,9 @@ class DevFactorLevel:
         self.max_k = int(k.max(initial=0))
         # solve-sweep size buckets: (device order, count, max_n, max_k)
         n_own = n if n_own is None else n_own
+        sv = _solve_buckets(n_own) if sv is None else sv
         self.solve_buckets = [(t[f"sv{bi}"], int(sel.size), int(n[sel].max()), int(k[sel].max()))
-                              for bi, sel in enumerate(_solve_buckets(n_own))]
+                              for bi, sel in enumerate(sv)]
 
 
 _SOLVE_CLASSES = (24, 40, 56, 72, 96, 128)
@@ -64,7 +66,13 @@ def _solve_buckets(n):
     """Boxes grouped by size so each sweep launch sizes its shared memory for
     its own boxes (more CTAs per SM for the many small ones)."""
     cls = np.searchsorted(np.asarray(_SOLVE_CLASSES), n, side="left")
-    return size_buckets(np.where(n > 0, cls, -1), n)
+    if _SOLVE_MERGE[0] and n.size <= _SOLVE_MERGE[0]:
+        cls = np.minimum(cls, _SOLVE_MERGE[1])       # few boxes: fewer, wider launches
+    return size_buckets(np.where(n > 0, cls, -1))
+
+
+_SOLVE_MERGE = [int(__import__("os").environ.get("SKEL_SOLVE_MERGE", "0")),
+                int(__import__("os").environ.get("SKEL_SOLVE_MERGE_CLS", "0"))]
 
 
 class FactoredLevel:
@@ -279,42 +287,29 @@ class FactorRun:
         optin = _smem_optin()
         L = _native.lib()
         p_ = _native.ptr
-        sq_bad = dl.nr != dl.nc
-        lam_bad = (~sq_bad) & (dl.nr > 0) & (dl.kr != dl.kc)
-        n = np.where(sq_bad | lam_bad, 0, dl.nr).astype(np.int64)
-        k = np.where(n > 0, dl.kr, 0).astype(np.int64)
         mine = getattr(dl, "mine", None)
         # sharded level: Dd / Ld / Rd slots for this rank's boxes only; the
-        # Lambda slab keeps every box's slot (parents above the split read it)
+        # Lambda slab keeps every box's slot (parents above the split read
+        # it).  Offsets, classes, big boxes and launch buckets: csrc/plan.cpp
+        pl = plan_factor_level(dl.nr, dl.nc, dl.kr, dl.kc, mine, elem, optin, _FAC_CLASSES,
+                               _BIG_FAC_N, 400, _SOLVE_CLASSES)
+        sq_bad, lam_bad, n, k = pl.sq_bad, pl.lam_bad, pl.n, pl.k
         n_own = n if mine is None else n * mine
-        dd_off, ld_off, lam_off = _off(n_own * n_own), _off(n_own * k), _off(k * k)
-        need = (n * n + 4 * n * k + k * k + 3 * n) * elem
-        cls = np.searchsorted(np.asarray(_FAC_CLASSES), need, side="left")
-        # big boxes (3D coarse levels): one box at a time over the whole GPU
-        big = n_own >= _BIG_FAC_N
-        fcls = np.where((n_own > 0) & ~big, cls, -1)
-        merged = None
-        if n.size <= 400:
-            # few boxes: one launch for all that fit shared memory (decided
-            # and sized over all boxes of the level, for any number of ranks)
-            fits_all = (n > 0) & (n < _BIG_FAC_N) & (need + 1024 + 4 * n <= optin)
-            if fits_all.any():
-                mn, mk = int(n[fits_all].max()), int(k[fits_all].max())
-                if (mn * mn + 4 * mn * mk + mk * mk + 3 * mn) * elem + 1024 + 4 * mn <= optin:
-                    fits = fits_all & (fcls >= 0)
-                    fcls = np.where(fits, 0, np.where(fcls >= 0, fcls + 1, -1))
-                    merged = (mn, mk)
-        buckets = size_buckets(fcls, need)
+        dd_off, ld_off, lam_off = pl.dd_off, pl.ld_off, pl.lam_off
+        big = pl.big
+        buckets = pl.buckets
+        merged = pl.merged if pl.merged_first else None
         p = dl.p
         outer = torch.cuda.stream(self.stream) if self.stream is not None else _nullctx()
         with outer:
             pk = Packer()
             pk.add("n", n.astype(np.int32)).add("k", k.astype(np.int32))
-            pk.add("noff", _off(n)).add("koff", _off(k))
+            pk.add("noff", pl.noff).add("koff", pl.koff)
             pk.add("dd_off", dd_off).add("ld_off", ld_off).add("lam_off", lam_off)
             for bi, sel in enumerate(buckets):
                 pk.add(f"order{bi}", sel)
-            for bi, sel in enumerate(_solve_buckets(n_own)):
+            sv = pl.sbuckets if not _SOLVE_MERGE[0] else _solve_buckets(n_own)
+            for bi, sel in enumerate(sv):
                 pk.add(f"sv{bi}", sel)
             t = pk.upload()
             Dd = torch.empty(max(int(dd_off[-1]), 1), dtype=tdt, device=dev)
@@ -327,7 +322,7 @@ class FactorRun:
             rcd = torch.ones(p, dtype=torch.float64, device=dev)
             rcm = torch.ones(p, dtype=torch.float64, device=dev)
             fl = DevFactorLevel(n, k, dd_off, ld_off, lam_off, Dd, Ld, Rd, Lam, dl.child_off, t,
-                                n_own=n_own, mine=mine)
+                                n_own=n_own, mine=mine, sv=sv)
             prev = self.levels[-1][1] if self.levels else None
             F = _native.SkelFactorLevel()
             F.nbox, F.level, F.regularize = p, li, self.regularize
@@ -342,11 +337,10 @@ class FactorRun:
             F.Dd, F.Ld, F.Rd, F.Lam = p_(Dd), p_(Ld), p_(Rd), p_(Lam)
             F.status, F.rcond_d, F.rcond_m = p_(status), p_(rcd), p_(rcm)
             streams = fork(len(buckets), tag="factor") if len(buckets) > 1 else None
-            nf, kf = n.astype(np.float64), k.astype(np.float64)
             for bi, sel in enumerate(buckets):
                 max_n = int(n[sel].max())
                 max_k = int(k[sel].max())
-                if merged is not None and fcls[sel[0]] == 0:
+                if merged is not None and bi == 0:
                     max_n, max_k = merged
                 nd = (max_n * max_n + 4 * max_n * max_k + max_k * max_k + 3 * max_n) * elem
                 F.order, F.nrun = p_(t[f"order{bi}"]), sel.size
@@ -361,6 +355,7 @@ class FactorRun:
                                 "factor_level", level=li)
                 if rec is not None:
                     b_ = sel
+                    nf, kf = n.astype(np.float64), k.astype(np.float64)
                     rec.flops = float((2 * nf[b_] ** 3 + 6 * nf[b_] ** 2 * kf[b_]
                                        + 6 * kf[b_] ** 2 * nf[b_] + 2 * kf[b_] ** 3).sum())
                     rec.nbytes = float(((nf[b_] ** 2 + 2 * nf[b_] * kf[b_]) * 2 + kf[b_] ** 2).sum()) * elem

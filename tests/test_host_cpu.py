@@ -89,3 +89,43 @@ def test_proxy_points_match_oracle():
     P = sk.proxy_points(node, sk.ProxyConfig(), 2).coords
     ref = node.center + oracle.geometry.proxy_radius(node.halfwidth, 2) * oracle.proxy_unit_points(64, 2)
     np.testing.assert_array_equal(P, ref)
+
+
+def test_level_planner_matches_numpy():
+    """csrc/plan.cpp (host bookkeeping of a level) == the numpy formulation:
+    target heights, offsets, big-box selection, size buckets and order."""
+    from paper_1110_3105_b200 import _plan
+    from paper_1110_3105_b200._staging import size_buckets
+    rng = np.random.default_rng(0)
+    p = 5000
+    nr = rng.integers(0, 70, p)
+    nc = nr.copy()
+    noff = np.concatenate([[0], np.cumsum(rng.integers(1, 9, p))])
+    nidx = rng.integers(0, p, noff[-1])
+    neff = np.full(p, 64)
+    W = (18 << 10, 27 << 10, 35 << 10, 46 << 10, 64 << 10, 100 << 10, 214 << 10)
+    M = (64, 128, 192, 256, 384, 512, 768)
+    pl = _plan.plan_id_level(nr, nc, noff, nidx, neff, None, 8, 232448, W, M, 512, 4096, 400)
+    m0 = np.array([nc[nidx[noff[a]:noff[a + 1]]].sum() for a in range(p)]) + 64
+    np.testing.assert_array_equal(pl.m0, m0)
+    np.testing.assert_array_equal(pl.rdof_off, np.concatenate([[0], np.cumsum(nr)]))
+    np.testing.assert_array_equal(pl.d_off, np.concatenate([[0], np.cumsum(nr * nc)]))
+    need_m = np.maximum(pl.m0, pl.m1)
+    need_n = np.maximum(np.maximum(nr, nc), 1)
+    wb = need_m * need_n * 8
+    cls = np.searchsorted(np.asarray(W), wb) * 16 + np.searchsorted(np.asarray(M), need_m)
+    cls = np.where(pl.big, -1, cls)
+    ref = size_buckets(cls, wb)
+    assert len(ref) == len(pl.buckets)
+    for a, b in zip(ref, pl.buckets):
+        np.testing.assert_array_equal(a, b)
+    # factor plan: offsets, solve buckets grouped by size class
+    kr = np.minimum(nr, rng.integers(0, 30, p))
+    fp = _plan.plan_factor_level(nr, nc, kr, kr, None, 8, 232448,
+                                 (24 << 10, 48 << 10, 80 << 10, 112 << 10, 160 << 10, 224 << 10),
+                                 768, 400, (24, 40, 56, 72, 96, 128))
+    np.testing.assert_array_equal(fp.dd_off, np.concatenate([[0], np.cumsum(nr * nr)]))
+    np.testing.assert_array_equal(fp.ld_off, np.concatenate([[0], np.cumsum(nr * kr)]))
+    scls = np.searchsorted(np.asarray((24, 40, 56, 72, 96, 128)), nr)
+    for a, b in zip(size_buckets(np.where(nr > 0, scls, -1)), fp.sbuckets):
+        np.testing.assert_array_equal(a, b)
