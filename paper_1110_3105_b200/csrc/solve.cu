@@ -10,6 +10,8 @@
 // the input segment(s) is staged in shared memory, factor blocks are streamed
 // from HBM exactly once per chunk (read-only path), each thread owns one
 // output (row, column) pair.
+#include <cstdlib>
+
 #include "common.cuh"
 
 // Block GEMM of one tree level, per box a and its slice of RHS columns:
@@ -277,9 +279,12 @@ static int level_gemm(int nbox, const int32_t* p, const int32_t* q, const int32_
       }
     }
   }
+  // register tiles picked per RHS count on B200 (the R=16 sweeps are bound
+  // by shared-memory load issue: TN > 1 reuses each staged A element)
+  if (R <= 2) return go(k_level_gemm<T, 4, 1, 2, true>, k_level_gemm<T, 4, 1, 2, false>, 2);
   if (R <= 8) return go(k_level_gemm<T, 4, 1, 8, true>, k_level_gemm<T, 4, 1, 8, false>, 8);
-  if (R <= 16) return go(k_level_gemm<T, 4, 1, 16, true>, k_level_gemm<T, 4, 1, 16, false>, 16);
-  if (R <= 32) return go(k_level_gemm<T, 4, 1, 32, true>, k_level_gemm<T, 4, 1, 32, false>, 32);
+  if (R <= 16) return go(k_level_gemm<T, 4, 2, 16, true>, k_level_gemm<T, 4, 2, 16, false>, 16);
+  if (R <= 32) return go(k_level_gemm<T, 4, 4, 32, true>, k_level_gemm<T, 4, 4, 32, false>, 32);
   return go(k_level_gemm<T, 4, 4, 64, true>, k_level_gemm<T, 4, 4, 64, false>, 64);
 }
 
