@@ -1,4 +1,6 @@
 """Host profile of FactorRun.add_level and compress_source internals at 2^20."""
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))  # ROOT_FOR_TOOLS
 import cProfile, pstats, warnings, torch
 import paper_1110_3105_b200 as sk
 from paper_1110_3105_b200 import solver

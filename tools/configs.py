@@ -1,5 +1,7 @@
 """Full-size probes of BASELINE configs 3 (CFIE 2^18) and 4 (3D sphere 40000):
 wall time of each phase, ranks, residual against the exact on-the-fly matvec."""
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))  # ROOT_FOR_TOOLS
 import sys, time, warnings
 import numpy as np
 import torch

@@ -1,5 +1,7 @@
 """Host-side breakdown of the bench's e2e call (bie.solve_dirichlet with host
 geometry and a pinned host RHS)."""
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))  # ROOT_FOR_TOOLS
 import cProfile, pstats, sys, time, warnings
 import numpy as np
 import torch

@@ -1,4 +1,6 @@
 """Does an eager solve between graph replays slow the replays down?"""
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))  # ROOT_FOR_TOOLS
 import sys, torch, numpy as np, warnings
 warnings.simplefilter("ignore")
 import paper_1110_3105_b200 as sk

@@ -1,4 +1,6 @@
 """Host-side profile (cProfile) of one factor step at a given N."""
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))  # ROOT_FOR_TOOLS
 import cProfile, pstats, sys, time, warnings
 import torch
 import paper_1110_3105_b200 as sk

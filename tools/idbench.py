@@ -1,4 +1,6 @@
 """Developer micro-benchmark: level-0 compression only, per variant."""
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))  # ROOT_FOR_TOOLS
 import os, sys, time, warnings
 import torch
 import paper_1110_3105_b200 as sk

@@ -1,4 +1,6 @@
 """Aggregate ncu source-page samples per CUDA source line (cuda,sass view)."""
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))  # ROOT_FOR_TOOLS
 import csv, subprocess, sys, collections
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30

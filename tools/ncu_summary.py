@@ -1,4 +1,6 @@
 """Summarise an ncu report (details page) for the kernels in it."""
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))  # ROOT_FOR_TOOLS
 import csv, subprocess, sys
 KEYS = ['Duration', 'Registers Per Thread', 'Achieved Occupancy', 'Theoretical Occupancy',
         'Block Limit Shared Mem', 'Block Limit Registers', 'Compute (SM) Throughput',

@@ -1,5 +1,7 @@
 """Developer timing probe (not the bench contract): per-phase timings of
 compress / factor / solve at a given N, plus per-level device spans."""
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))  # ROOT_FOR_TOOLS
 import sys, time
 import numpy as np
 import torch

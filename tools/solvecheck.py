@@ -1,3 +1,5 @@
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))  # ROOT_FOR_TOOLS
 import sys, time, torch, numpy as np, warnings
 sys.path.insert(0, "/root/repo")
 warnings.simplefilter("ignore")
