@@ -199,12 +199,32 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
   double t0 = now_ms();
   T.dim = d;
   T.n = n;
+  unsigned hwc = std::thread::hardware_concurrency();
+  const int nthreads = (int)std::max(1u, std::min(hwc == 0 ? 1u : hwc, 32u));
+  auto parallel = [&](auto fn) {        // fn(t, a0, a1) over point chunks
+    const int64_t chunk = (n + nthreads - 1) / nthreads;
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthreads; ++t)
+      th.emplace_back([&, t]() { fn(t, t * chunk, std::min(n, (int64_t)(t + 1) * chunk)); });
+    for (auto& x : th) x.join();
+  };
+  // bounding box (per-thread extrema, then reduced)
+  std::vector<std::array<double, 6>> ext_t(nthreads);
+  parallel([&](int t, int64_t a0, int64_t a1) {
+    std::array<double, 6> e = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = a0; i < a1; ++i)
+      for (int a = 0; a < d; ++a) {
+        const double v = X[i * d + a];
+        e[a] = std::min(e[a], v);
+        e[3 + a] = std::max(e[3 + a], v);
+      }
+    ext_t[t] = e;
+  });
   double lo_c[3] = {INFINITY, INFINITY, INFINITY}, hi_c[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int64_t i = 0; i < n; ++i)
+  for (int t = 0; t < nthreads; ++t)
     for (int a = 0; a < d; ++a) {
-      double v = X[i * d + a];
-      lo_c[a] = std::min(lo_c[a], v);
-      hi_c[a] = std::max(hi_c[a], v);
+      lo_c[a] = std::min(lo_c[a], ext_t[t][a]);
+      hi_c[a] = std::max(hi_c[a], ext_t[t][3 + a]);
     }
   double c0[3] = {0, 0, 0}, ext = 0.0, cabs = 0.0;
   for (int a = 0; a < d; ++a) {
@@ -222,6 +242,7 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
   static std::vector<int64_t> s_tmpi;
   static std::vector<double> s_px[3], s_tmpx[3];
   static std::vector<uint8_t> s_code;
+  static std::vector<uint16_t> s_top;
   std::lock_guard<std::mutex> guard(scratch_mu);
   std::vector<int64_t> perm(n);
   std::vector<int64_t>& tmpi = s_tmpi;
@@ -231,21 +252,6 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
   for (int a = 0; a < d; ++a) {
     if ((int64_t)pxv[a].size() < n) pxv[a].resize(n);
     if ((int64_t)tmpx[a].size() < n) tmpx[a].resize(n);
-  }
-  {
-    unsigned hc = std::thread::hardware_concurrency();
-    const int T = (int)std::max(1u, std::min(hc == 0 ? 1u : hc, 32u));
-    const int64_t chunk = (n + T - 1) / T;
-    std::vector<std::thread> th;
-    for (int t = 0; t < T; ++t)
-      th.emplace_back([&, t]() {
-        const int64_t a0 = t * chunk, a1 = std::min(n, a0 + chunk);
-        for (int64_t i = a0; i < a1; ++i) {
-          perm[i] = i;
-          for (int a = 0; a < d; ++a) pxv[a][i] = X[i * d + a];
-        }
-      });
-    for (auto& x : th) x.join();
   }
   std::vector<uint8_t>& code = s_code;
   if ((int64_t)code.size() < n) code.resize(n);
@@ -259,16 +265,83 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
     B.px[a] = a < d ? pxv[a].data() : nullptr;
     B.tmpx[a] = &tmpx[a];
   }
-
-  double t0b = now_ms();
-  // top part, breadth first: all open nodes of a depth are split together
-  // (in parallel across nodes, or with the parallel counting sort for the
-  // few huge ones), down to a frontier of ranges small enough to become
-  // independent subtree tasks
-  unsigned hwc = std::thread::hardware_concurrency();
-  const int nthreads = (int)std::max(1u, std::min(hwc == 0 ? 1u : hwc, 32u));
   B.nthreads = nthreads;
   const int64_t frontier_size = std::max<int64_t>(4 * max_leaf, n / (4 * nthreads));
+
+  double t0b = now_ms();
+  // ---- top part, all at once: every point's child digits for the first DT
+  // levels (the same centre arithmetic as the node splits, so the same
+  // comparisons), one histogram, per-level counts, the depth at which each
+  // top cell stops (leaf, or subtree task), and ONE stable counting sort by
+  // the stopping prefix -- points of a node end up in original order, the
+  // nodes in preorder, exactly as the recursive stable partitioning leaves them.
+  const int DT = d == 2 ? 6 : 4;
+  const int NB = 1 << (d * DT);
+  std::vector<uint16_t>& tcode = s_top;
+  if ((int64_t)tcode.size() < n) tcode.resize(n);
+  std::vector<std::vector<int64_t>> hist_t(nthreads, std::vector<int64_t>(NB, 0));
+  parallel([&](int t, int64_t a0, int64_t a1) {
+    std::vector<int64_t>& h = hist_t[t];
+    for (int64_t i = a0; i < a1; ++i) {
+      double cen[3] = {c0[0], c0[1], c0[2]};
+      double hw = hw0;
+      unsigned cd = 0;
+      for (int lev = 0; lev < DT; ++lev) {
+        unsigned k = 0;
+        for (int a = 0; a < d; ++a) k |= (X[i * d + a] >= cen[a] ? 1u : 0u) << a;
+        cd = (cd << d) | k;
+        for (int a = 0; a < d; ++a) cen[a] = cen[a] + (((k >> a) & 1) ? 0.5 : -0.5) * hw;
+        hw = 0.5 * hw;
+      }
+      tcode[i] = (uint16_t)cd;
+      h[cd]++;
+    }
+  });
+  // counts of every prefix at every depth 0..DT
+  std::vector<std::vector<int64_t>> cnt(DT + 1);
+  cnt[DT].assign(NB, 0);
+  for (int t = 0; t < nthreads; ++t)
+    for (int b = 0; b < NB; ++b) cnt[DT][b] += hist_t[t][b];
+  for (int l = DT - 1; l >= 0; --l) {
+    cnt[l].assign((size_t)1 << (d * l), 0);
+    for (size_t q = 0; q < cnt[l + 1].size(); ++q) cnt[l][q >> d] += cnt[l + 1][q];
+  }
+  auto stops = [&](int l, int64_t c) {
+    const bool leaf = c <= max_leaf || l >= kMaxDepth;
+    return leaf || c <= frontier_size || l == DT;
+  };
+  // sort key of each top cell: its stopping prefix, left-aligned
+  std::vector<int32_t> key(NB);
+  for (int b = 0; b < NB; ++b) {
+    int l = 0;
+    while (!stops(l, cnt[l][b >> (d * (DT - l))])) ++l;
+    const int sh = d * (DT - l);
+    key[b] = (b >> sh) << sh;
+  }
+  // stable counting sort by key: per-thread counts, key-major offsets
+  std::vector<std::vector<int64_t>> kc_t(nthreads, std::vector<int64_t>(NB, 0));
+  parallel([&](int t, int64_t a0, int64_t a1) {
+    std::vector<int64_t>& c = kc_t[t];
+    for (int64_t i = a0; i < a1; ++i) c[key[tcode[i]]]++;
+  });
+  {
+    int64_t run = 0;
+    for (int b = 0; b < NB; ++b)
+      for (int t = 0; t < nthreads; ++t) {
+        const int64_t c = kc_t[t][b];
+        kc_t[t][b] = run;
+        run += c;
+      }
+  }
+  parallel([&](int t, int64_t a0, int64_t a1) {
+    std::vector<int64_t>& pos = kc_t[t];
+    for (int64_t i = a0; i < a1; ++i) {
+      const int64_t dst = pos[key[tcode[i]]]++;
+      perm[dst] = i;
+      for (int a = 0; a < d; ++a) pxv[a][dst] = X[i * d + a];
+    }
+  });
+  // the top nodes, in preorder over the prefix counts
   struct TNode {
     NodeRec rec;
     bool task, leaf;
@@ -276,66 +349,42 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
   };
   std::vector<TNode> top;
   {
-    TNode r;
-    for (int a = 0; a < 3; ++a) r.rec.c[a] = c0[a];
-    r.rec.hw = hw0; r.rec.lo = 0; r.rec.hi = n; r.rec.depth = 0; r.rec.parent = -1; r.rec.nchild = 0;
-    top.push_back(r);
-  }
-  std::vector<int64_t> open = {0};
-  while (!open.empty()) {
-    std::vector<int64_t> to_split;
-    for (int64_t id : open) {
-      TNode& t = top[id];
-      const int64_t sz = t.rec.hi - t.rec.lo;
-      t.leaf = sz <= max_leaf || t.rec.depth >= kMaxDepth;
-      t.task = !t.leaf && sz <= frontier_size;
-      if (!t.leaf && !t.task) to_split.push_back(id);
-    }
-    std::vector<std::array<int64_t, 8>> counts(to_split.size());
-    const int big = (int)std::count_if(to_split.begin(), to_split.end(), [&](int64_t id) {
-      return top[id].rec.hi - top[id].rec.lo >= ((int64_t)1 << 17);
-    });
-    if ((int)to_split.size() < nthreads || big == (int)to_split.size()) {
-      for (size_t q = 0; q < to_split.size(); ++q) {
-        const NodeRec& r = top[to_split[q]].rec;
-        B.split(r.lo, r.hi, r.c, counts[q].data());
+    struct Frame { int l; int64_t q, lo, parent; double c[3]; double hw; };
+    std::vector<Frame> st;
+    Frame f0{0, 0, 0, -1, {c0[0], c0[1], c0[2]}, hw0};
+    st.push_back(f0);
+    while (!st.empty()) {
+      Frame f = st.back();
+      st.pop_back();
+      const int64_t c = cnt[f.l][f.q];
+      TNode t;
+      for (int a = 0; a < 3; ++a) t.rec.c[a] = a < d ? f.c[a] : 0.0;
+      t.rec.hw = f.hw; t.rec.lo = f.lo; t.rec.hi = f.lo + c; t.rec.depth = f.l;
+      t.rec.parent = f.parent; t.rec.nchild = 0;
+      t.leaf = c <= max_leaf || f.l >= kMaxDepth;
+      t.task = !t.leaf && stops(f.l, c);
+      const int64_t id = (int64_t)top.size();
+      top.push_back(t);
+      if (f.parent >= 0) {
+        top[f.parent].kids.push_back(id);
+        top[f.parent].rec.nchild += 1;
       }
-    } else {
-      std::atomic_int next(0);
-      Builder Bs = B;
-      Bs.nthreads = 1;
-      std::vector<std::thread> pool;
-      auto worker = [&]() {
-        for (;;) {
-          int q = next.fetch_add(1);
-          if (q >= (int)to_split.size()) break;
-          const NodeRec& r = top[to_split[q]].rec;
-          Bs.split(r.lo, r.hi, r.c, counts[q].data());
-        }
-      };
-      for (int i = 0; i < nthreads; ++i) pool.emplace_back(worker);
-      for (auto& th : pool) th.join();
-    }
-    std::vector<int64_t> nxt;
-    for (size_t q = 0; q < to_split.size(); ++q) {
-      const int64_t id = to_split[q];
-      int64_t s0 = top[id].rec.lo;
-      for (int c = 0; c < (1 << d); ++c) {
-        const int64_t cnt = counts[q][c];
-        if (cnt == 0) continue;
-        TNode k;
-        const NodeRec& pr = top[id].rec;
-        for (int a = 0; a < 3; ++a) k.rec.c[a] = a < d ? pr.c[a] + (((c >> a) & 1) ? 0.5 : -0.5) * pr.hw : 0.0;
-        k.rec.hw = 0.5 * pr.hw; k.rec.lo = s0; k.rec.hi = s0 + cnt; k.rec.depth = pr.depth + 1;
-        k.rec.parent = id; k.rec.nchild = 0;
-        s0 += cnt;
-        top.push_back(k);
-        top[id].kids.push_back((int64_t)top.size() - 1);
-        top[id].rec.nchild += 1;
-        nxt.push_back((int64_t)top.size() - 1);
+      if (t.leaf || t.task) continue;
+      // children pushed in reverse so they are visited (and numbered) in code order
+      int64_t offs[8];
+      int64_t off = f.lo;
+      const int nk = 1 << d;
+      for (int k = 0; k < nk; ++k) { offs[k] = off; off += cnt[f.l + 1][(f.q << d) | k]; }
+      for (int k = nk - 1; k >= 0; --k) {
+        const int64_t cc = cnt[f.l + 1][(f.q << d) | k];
+        if (cc == 0) continue;
+        Frame g;
+        g.l = f.l + 1; g.q = (f.q << d) | k; g.lo = offs[k]; g.parent = id;
+        for (int a = 0; a < 3; ++a) g.c[a] = a < d ? f.c[a] + (((k >> a) & 1) ? 0.5 : -0.5) * f.hw : 0.0;
+        g.hw = 0.5 * f.hw;
+        st.push_back(g);
       }
     }
-    open.swap(nxt);
   }
   // preorder item list of the top part (children in code order)
   std::vector<TopItem> items;
