@@ -177,7 +177,9 @@ static __host__ __device__ inline size_t fac_elems(int n, int k) {
 }
 
 template <class T, bool GW, int NT>
-__global__ void __launch_bounds__(NT) k_factor_level(const SkelFactorLevel F, int max_n, int max_k) {
+// (real, 256 threads: capped at 64 registers for 4 CTAs / SM -- no spills)
+__global__ void __launch_bounds__(NT, ((NT == 256 && sizeof(T) == sizeof(double)) ? 4 : 1))
+    k_factor_level(const SkelFactorLevel F, int max_n, int max_k) {
   extern __shared__ __align__(16) unsigned char smem[];
   FacShared<T>& sh = *reinterpret_cast<FacShared<T>*>(smem);
   int* ipiv = reinterpret_cast<int*>(smem + 512);
