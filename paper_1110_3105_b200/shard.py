@@ -24,8 +24,6 @@ bit-identical for every world size.
 
 import numpy as np
 
-from . import _native
-
 
 class ShardPlan:
     def __init__(self, tree, world, rank, group=None, min_boxes_per_rank=16):
@@ -119,8 +117,8 @@ class ShardPlan:
         return dist.get_backend(self.group)
 
     def all_reduce(self, t, op="sum"):
-        """In-place all-reduce of a CUDA (or CPU) tensor over the plan's group."""
-        import torch
+        """In-place all-reduce of a CUDA (or CPU) tensor over the plan's group
+        (gloo: staged through host memory)."""
         import torch.distributed as dist
         rop = {"sum": dist.ReduceOp.SUM, "min": dist.ReduceOp.MIN,
                "max": dist.ReduceOp.MAX}[op]
@@ -130,7 +128,6 @@ class ShardPlan:
             t.copy_(h.to(t.device))
         else:
             dist.all_reduce(t, op=rop, group=self.group)
-        del torch
         return t
 
 
@@ -147,4 +144,3 @@ def default_plan(tree):
 
 
 __all__ = ["ShardPlan", "default_plan"]
-_ = _native

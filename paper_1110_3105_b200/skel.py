@@ -25,7 +25,7 @@ from .errors import InvalidInput, RefusedTooLarge
 from .geom import OrthTree, PointSet
 from .kernels import KernelSpec
 from ._plan import plan_id_level
-from ._staging import Packer, eager_stream, fork, join, on_stream, size_buckets
+from ._staging import Packer, eager_stream, fork, join, on_stream
 
 DEFAULT_N_PROXY = {2: 64, 3: 512}        # skel.py:29
 _RANDOMIZED_CUTOFF = 4096                # skel.py:33
@@ -491,7 +491,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
     for li in range(top_run):
         _ht = _HostTimer(li) if _HOST_TIMING else None
         lev_ctx = _profile.timed("level", level=li)
-        lev_rec = lev_ctx.__enter__()
+        lev_ctx.__enter__()
         if nvtx:
             torch.cuda.nvtx.range_push(f"level{li}")
         geo = geo_next
@@ -739,14 +739,6 @@ def _smem_optin():
 
 _BIG_N = 512                 # boxes wider than this take the whole-GPU path
 _SMALL_LEVEL = 400           # levels with at most this many boxes: one ID launch
-
-
-def _bigbox_randomized(m, n):
-    return m > np.maximum(4096, 4 * n + 256)        # skel.py:419-421
-
-
-def _level_smem_fixed_vec(n, field):
-    return _level_smem_fixed(np.asarray(n, dtype=np.int64), field)
 
 
 def _level_smem_fixed(max_n, field):
