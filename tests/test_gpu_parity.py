@@ -345,3 +345,27 @@ def test_single_box_degenerate_tree():
     b = np.random.default_rng(1).standard_normal(48)
     A = system.matrix()
     np.testing.assert_allclose(A @ sk.solve(fi, b), b, atol=1e-12)
+
+
+@gpu
+def test_full_size_config2_properties():
+    """BASELINE config 2 at its full size (N = 2^20, eps = 1e-12): the oracle
+    cannot run here, so size-independent properties -- residual against the
+    exact operator (K6 on-the-fly matvec), solve / apply round trip, ranks
+    grow slowly, factor storage at the reference's 1784 B/pt."""
+    sk = _sk()
+    n = 2 ** 20
+    curve = sk.bie.ellipse(2.0, 1.0, n)
+    system = sk.bie.discretize_dirichlet(curve, sk.KernelSpec("laplace", 2))
+    tree, cm = sk.bie.compress_system(system, 1e-12, 64)
+    fi = sk.factor(cm)
+    B = np.random.default_rng(0).standard_normal((n, 2))
+    X = sk.solve(fi, B)
+    src = sk.bie.BieSource(system, tree.perm)
+    res = np.linalg.norm(sk.bie.dense_matvec(src, X[:, :1]) - B[:, :1]) / np.linalg.norm(B[:, :1])
+    assert res <= 1e-10, res
+    # apply(solve(b)) = b through the compressed operator
+    Y = sk.apply(cm, X)
+    assert np.linalg.norm(Y - B) / np.linalg.norm(B) <= 1e-10
+    assert cm.S_shape()[0] <= 400 and cm.nlevels == 14
+    assert abs(fi.factor_bytes() / n - 1784) < 60
