@@ -83,13 +83,19 @@ __device__ int sm_invert(T* A, int lda, int p, T* scratch, int* ipiv, FacShared<
       }
       if (best > 0.0) {
         const int pr = bi;
-        for (int j = lane; j < p; j += 32) {
-          rowp[j] = A[(int64_t)pr * lda + j];
-          rowk[j] = A[(int64_t)kk * lda + j];
-        }
+        const T inv = T(1.0) / A[(int64_t)pr * lda + kk];
         for (int i = lane; i < p; i += 32) {
           // pivot column after the exchange of rows kk and pr
           colk[i] = (i == pr) ? A[(int64_t)kk * lda + kk] : A[(int64_t)i * lda + kk];
+        }
+        __syncwarp();
+        for (int j = lane; j < p; j += 32) {
+          // the scaled pivot row (its column kk holds 1/pivot), and the
+          // exchange done in place: row pr takes old row kk
+          const T vp = A[(int64_t)pr * lda + j];
+          const T vk = A[(int64_t)kk * lda + j];
+          rowp[j] = (j == kk) ? inv : vp * inv;
+          if (pr != kk) A[(int64_t)pr * lda + j] = vk;
         }
       }
       if (lane == 0) {
@@ -100,34 +106,38 @@ __device__ int sm_invert(T* A, int lda, int p, T* scratch, int* ipiv, FacShared<
     }
     __syncthreads();
     if (sh.amax == 0.0) return 1;
-    const int pr = sh.piv_row;
-    const T inv = T(1.0) / rowp[kk];
+    // eliminate column kk everywhere (rows already exchanged, pivot row
+    // scaled in rowp with 1/pivot in its column kk): a_ij -= a_ik * r_j, and
+    // column kk becomes -a_ik / pivot (in-place inverse)
     for (int i = warp; i < p; i += (nt >> 5)) {
       T* Ai = A + (int64_t)i * lda;
       const T f = colk[i];
-      for (int j = lane; j < p; j += 32) {
-        const T rk = (j == kk) ? inv : rowp[j] * inv;     // new (scaled) pivot row
-        T v;
-        if (i == kk) v = rk;
-        else if (j == kk) v = -(f * inv);
-        else v = ((i == pr) ? rowk[j] : Ai[j]) - f * rk;
-        Ai[j] = v;
+      if (i == kk) {
+        for (int j = lane; j < p; j += 32) Ai[j] = rowp[j];
+      } else {
+        for (int j = lane; j < p; j += 32) {
+          const T a = (j == kk) ? T(0.0) : Ai[j];
+          Ai[j] = a - f * rowp[j];
+        }
       }
     }
     __syncthreads();
   }
-  // undo the row interchanges as column interchanges, last first
-  for (int kk = p - 1; kk >= 0; --kk) {
-    int pr = ipiv[kk];
-    if (pr != kk) {
-      for (int i = tid; i < p; i += nt) {
-        T t = A[(int64_t)i * lda + kk];
-        A[(int64_t)i * lda + kk] = A[(int64_t)i * lda + pr];
-        A[(int64_t)i * lda + pr] = t;
+  // undo the row interchanges as column interchanges, last first: rows are
+  // independent, so each thread replays the whole sequence on its own rows
+  // (one barrier instead of one per column)
+  for (int i = tid; i < p; i += nt) {
+    T* Ai = A + (int64_t)i * lda;
+    for (int kk = p - 1; kk >= 0; --kk) {
+      const int pr = ipiv[kk];
+      if (pr != kk) {
+        const T t = Ai[kk];
+        Ai[kk] = Ai[pr];
+        Ai[pr] = t;
       }
     }
-    __syncthreads();
   }
+  __syncthreads();
   return 0;
 }
 
