@@ -141,39 +141,49 @@ __device__ int sm_invert(T* A, int lda, int p, T* scratch, int* ipiv, FacShared<
   return 0;
 }
 
-// C (p x q, ldc) = [C -] A (p x r) * B (r x q), row-major, 4x4 register tiles.
-template <class T, bool SUB>
-__device__ void sm_gemm(T* C, int ldc, const T* A, int lda, const T* B, int ldb, int p, int q,
-                        int r) {
-  const int tp = (p + 3) >> 2, tq = (q + 3) >> 2;
+// C (p x q, ldc) = [C -] A (p x r) * B (r x q), row-major, TS x TS register
+// tiles (the caller picks TS so that enough threads get a tile).
+template <class T, bool SUB, int TS>
+__device__ void sm_gemm_t(T* C, int ldc, const T* A, int lda, const T* B, int ldb, int p, int q,
+                          int r) {
+  const int tp = (p + TS - 1) / TS, tq = (q + TS - 1) / TS;
   for (int t = threadIdx.x; t < tp * tq; t += blockDim.x) {
-    const int i0 = (t / tq) * 4, j0 = (t % tq) * 4;
-    T acc[4][4];
+    const int i0 = (t / tq) * TS, j0 = (t % tq) * TS;
+    T acc[TS][TS];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < TS; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = T(0.0);
+      for (int b = 0; b < TS; ++b) acc[a][b] = T(0.0);
     for (int s = 0; s < r; ++s) {
-      T av[4], bv[4];
+      T av[TS], bv[TS];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) av[a] = (i0 + a < p) ? A[(int64_t)(i0 + a) * lda + s] : T(0.0);
+      for (int a = 0; a < TS; ++a) av[a] = (i0 + a < p) ? A[(int64_t)(i0 + a) * lda + s] : T(0.0);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = (j0 + b < q) ? B[(int64_t)s * ldb + j0 + b] : T(0.0);
+      for (int b = 0; b < TS; ++b) bv[b] = (j0 + b < q) ? B[(int64_t)s * ldb + j0 + b] : T(0.0);
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < TS; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] += av[a] * bv[b];
+        for (int b = 0; b < TS; ++b) acc[a][b] += av[a] * bv[b];
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < TS; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
+      for (int b = 0; b < TS; ++b)
         if (i0 + a < p && j0 + b < q) {
           T* c = C + (int64_t)(i0 + a) * ldc + j0 + b;
           if (SUB) *c = *c - acc[a][b];
           else *c = acc[a][b];
         }
   }
+}
+
+template <class T, bool SUB>
+__device__ void sm_gemm(T* C, int ldc, const T* A, int lda, const T* B, int ldb, int p, int q,
+                        int r) {
+  const int nt = blockDim.x;
+  if (((p + 3) >> 2) * ((q + 3) >> 2) >= nt) sm_gemm_t<T, SUB, 4>(C, ldc, A, lda, B, ldb, p, q, r);
+  else if (((p + 1) >> 1) * ((q + 1) >> 1) >= nt / 2) sm_gemm_t<T, SUB, 2>(C, ldc, A, lda, B, ldb, p, q, r);
+  else sm_gemm_t<T, SUB, 1>(C, ldc, A, lda, B, ldb, p, q, r);
 }
 
 template <class T>
