@@ -109,16 +109,22 @@ __device__ int sm_invert(T* A, int lda, int p, T* scratch, int* ipiv, FacShared<
     // eliminate column kk everywhere (rows already exchanged, pivot row
     // scaled in rowp with 1/pivot in its column kk): a_ij -= a_ik * r_j, and
     // column kk becomes -a_ik / pivot (in-place inverse)
-    for (int i = warp; i < p; i += (nt >> 5)) {
-      T* Ai = A + (int64_t)i * lda;
-      const T f = colk[i];
-      if (i == kk) {
-        for (int j = lane; j < p; j += 32) Ai[j] = rowp[j];
-      } else {
-        for (int j = lane; j < p; j += 32) {
-          const T a = (j == kk) ? T(0.0) : Ai[j];
-          Ai[j] = a - f * rowp[j];
+    {
+      // flat (row, column) walk: every thread gets ~p^2 / nt elements
+      const int di = nt / p, dj = nt - (nt / p) * p;
+      int i = tid / p, j = tid - (tid / p) * p;
+      for (int e = tid; e < p * p; e += nt) {
+        T* Aij = A + (int64_t)i * lda + j;
+        const T r = rowp[j];
+        if (i == kk) {
+          *Aij = r;
+        } else {
+          const T a = (j == kk) ? T(0.0) : *Aij;
+          *Aij = a - colk[i] * r;
         }
+        i += di;
+        j += dj;
+        if (j >= p) { j -= p; ++i; }
       }
     }
     __syncthreads();
