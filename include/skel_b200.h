@@ -339,6 +339,21 @@ int skel_sweep_down_ex(int32_t nbox, const int32_t* n, const int32_t* k,
                        const void* u, const void* v, void* w, int32_t R, int32_t field,
                        int32_t max_n, int32_t max_k, const int32_t* order, void* stream);
 
+/* The same sweeps with the finest level's tree-order gather / scatter of the
+ * right-hand sides fused in (solver.py:288,316-318): u rows are read as
+ * u[urows[noff[a] + j]] and w rows written to w[wrows[noff[a] + i]] (NULL =
+ * plain).  R <= 16 (returns -3 otherwise). */
+int skel_sweep_up_rows(int32_t nbox, const int32_t* n, const int32_t* k, const int64_t* noff,
+                       const int64_t* koff, const int64_t* m_off, const void* M, const void* u,
+                       void* out, int32_t R, int32_t field, int32_t max_n, int32_t max_k,
+                       const int32_t* order, const int64_t* urows, void* stream);
+int skel_sweep_down_rows(int32_t nbox, const int32_t* n, const int32_t* k, const int64_t* noff,
+                         const int64_t* koff, const int64_t* a_off, const void* A,
+                         const int64_t* b_off, const void* B, const void* u, const void* v, void* w,
+                         int32_t R, int32_t field, int32_t max_n, int32_t max_k,
+                         const int32_t* order, const int64_t* urows, const int64_t* wrows,
+                         void* stream);
+
 /* y = M x for a dense K x K row-major M, R columns (top-level S^-1 / S). */
 int skel_dense_apply(const void* M, int32_t K, int32_t Kc, const void* x, void* y,
                      int32_t R, int32_t field, void* stream);

@@ -83,6 +83,10 @@ _SIGS = {
                          c_i32, c_i32, c_vp, c_vp],
     "skel_sweep_down_ex": [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                            c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp],
+    "skel_sweep_up_rows": [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32,
+                           c_i32, c_i32, c_vp, c_vp, c_vp],
+    "skel_sweep_down_rows": [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                             c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp],
     "skel_dense_apply": [c_vp, c_i32, c_i32, c_vp, c_vp, c_i32, c_i32, c_vp],
     "skel_permute_rows": [c_vp, c_i64, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp],
     "skel_compact_i32": [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
@@ -128,7 +132,7 @@ _LAUNCHING = {"skel_id_level", "skel_assemble_D", "skel_assemble_S", "skel_eval_
               "skel_compact_i32", "skel_dense_matvec", "skel_fp64_probe", "skel_big_target",
               "skel_cpqr_big", "skel_big_interp", "skel_big_output", "skel_gemm_tn", "skel_gemv",
               "skel_big_probe", "skel_dense_inverse_big", "skel_factor_big", "skel_dense_lu",
-              "skel_lu_inverse", "skel_bessel_h0"}
+              "skel_lu_inverse", "skel_bessel_h0", "skel_sweep_up_rows", "skel_sweep_down_rows"}
 launch_count = [0]
 
 

@@ -24,18 +24,20 @@
 // shared memory (3D coarse levels): operands are read through L1 directly.
 
 template <class T, int CB>
-__device__ __forceinline__ void stage_chunk(T* sX, const T* Xg, int q, int R, int c0, int cb) {
+__device__ __forceinline__ void stage_chunk(T* sX, const T* Xg, int q, int R, int c0, int cb,
+                                            const int64_t* rows = nullptr) {
   constexpr int W = sizeof(T) / 8;   // 8-byte words per element
   for (int e = threadIdx.x; e < q * CB * W; e += blockDim.x) {
     const int el = e / W, wd = e - el * W;
     const int j = el / CB, c = el - j * CB;
     double* d = reinterpret_cast<double*>(sX + el) + wd;
-    if (c < cb) cp_async8(d, reinterpret_cast<const double*>(Xg + (int64_t)j * R + c0 + c) + wd);
+    const T* xr = rows ? Xg + rows[j] * R : Xg + (int64_t)j * R;   // rows: gathered segment
+    if (c < cb) cp_async8(d, reinterpret_cast<const double*>(xr + c0 + c) + wd);
     else *d = 0.0;
   }
 }
 
-template <class T, int TM, int TN, int CB, bool STAGE>
+template <class T, int TM, int TN, int CB, bool STAGE, bool ROWS = false>
 __global__ void __launch_bounds__(128) k_level_gemm(
     const int32_t* __restrict__ pp, const int32_t* __restrict__ qq, const int32_t* __restrict__ rr,
     const int64_t* __restrict__ a_off, const T* __restrict__ A,
@@ -43,7 +45,11 @@ __global__ void __launch_bounds__(128) k_level_gemm(
     const int64_t* __restrict__ x_off, const T* __restrict__ X,
     const int64_t* __restrict__ y_off, const T* __restrict__ Y,
     const int64_t* __restrict__ o_off, T* __restrict__ O, int R, int cols_per_cta, int max_q,
-    int max_r, const int32_t* __restrict__ order) {
+    int max_r, const int32_t* __restrict__ order, const int64_t* __restrict__ xrows,
+    const int64_t* __restrict__ orows) {
+  // xrows / orows (optional): X rows are X[xrows[x_off + j]] and output rows
+  // go to O[orows[o_off + i]] -- the solve's tree-order gather / scatter of
+  // the right-hand sides fused into the finest level's sweeps
   extern __shared__ __align__(16) unsigned char smem[];
   const int a = order ? order[blockIdx.x] : blockIdx.x;
   const int p = pp[a], q = qq[a], r = rr ? rr[a] : 0;
@@ -54,9 +60,11 @@ __global__ void __launch_bounds__(128) k_level_gemm(
   const int tid = threadIdx.x, nt = blockDim.x;
   const T* Ag = A + a_off[a];
   const T* Bg = r ? Bm + b_off[a] : nullptr;
-  const T* Xg = X + x_off[a] * R;
+  const int64_t* xr = (ROWS && xrows) ? xrows + x_off[a] : nullptr;
+  const int64_t* orw = (ROWS && orows) ? orows + o_off[a] : nullptr;
+  const T* Xg = xr ? X : X + x_off[a] * R;
   const T* Yg = r ? Y + y_off[a] * R : nullptr;
-  T* Og = O + o_off[a] * R;
+  T* Og = orw ? O : O + o_off[a] * R;
   T* sA = reinterpret_cast<T*>(smem);
   T* sB = sA + (STAGE ? (size_t)p * q : 0);
   T* const sXY0 = sB + (STAGE ? (size_t)p * r : 0);
@@ -69,7 +77,7 @@ __global__ void __launch_bounds__(128) k_level_gemm(
       cp_async8(reinterpret_cast<double*>(sA) + e, reinterpret_cast<const double*>(Ag) + e);
     for (int e = tid; e < p * r * W; e += nt)
       cp_async8(reinterpret_cast<double*>(sB) + e, reinterpret_cast<const double*>(Bg) + e);
-    stage_chunk<T, CB>(sXY0, Xg, q, R, cbeg, min(CB, cend - cbeg));
+    stage_chunk<T, CB>(sXY0, Xg, q, R, cbeg, min(CB, cend - cbeg), xr);
     if (r) stage_chunk<T, CB>(sXY0 + (size_t)q * CB, Yg, r, R, cbeg, min(CB, cend - cbeg));
     cp_async_commit();
   }
@@ -84,7 +92,7 @@ __global__ void __launch_bounds__(128) k_level_gemm(
       const int c1 = c0 + CB;
       if (c1 < cend) {
         T* nb = sXY0 + (buf ^ 1) * sxy_stride;
-        stage_chunk<T, CB>(nb, Xg, q, R, c1, min(CB, cend - c1));
+        stage_chunk<T, CB>(nb, Xg, q, R, c1, min(CB, cend - c1), xr);
         if (r) stage_chunk<T, CB>(nb + (size_t)q * CB, Yg, r, R, c1, min(CB, cend - c1));
       }
       cp_async_commit();
@@ -107,7 +115,8 @@ __global__ void __launch_bounds__(128) k_level_gemm(
 #pragma unroll
         for (int v = 0; v < TN; ++v)
           xv[v] = STAGE ? sX[j * CB + j0 + v]
-                        : ((j0 + v < cb) ? __ldg_T(Xg + (int64_t)j * R + c0 + j0 + v) : T(0.0));
+                        : ((j0 + v < cb) ? __ldg_T((xr ? Xg + xr[j] * R : Xg + (int64_t)j * R) + c0 + j0 + v)
+                                         : T(0.0));
 #pragma unroll
         for (int u = 0; u < TM; ++u)
 #pragma unroll
@@ -131,7 +140,8 @@ __global__ void __launch_bounds__(128) k_level_gemm(
       for (int u = 0; u < TM; ++u)
 #pragma unroll
         for (int v = 0; v < TN; ++v)
-          if (i0 + u < p && j0 + v < cb) Og[(int64_t)(i0 + u) * R + c0 + j0 + v] = acc[u][v];
+          if (i0 + u < p && j0 + v < cb)
+            (orw ? Og + orw[i0 + u] * R : Og + (int64_t)(i0 + u) * R)[c0 + j0 + v] = acc[u][v];
     }
     if (STAGE) __syncthreads();   // buffer `buf` is refilled two chunks later
   }
@@ -233,7 +243,8 @@ static int level_gemm(int nbox, const int32_t* p, const int32_t* q, const int32_
                       const int64_t* a_off, const void* A, const int64_t* b_off, const void* B,
                       const int64_t* x_off, const void* X, const int64_t* y_off, const void* Y,
                       const int64_t* o_off, void* O, int R, int max_p, int max_q, int max_r,
-                      const int32_t* order, cudaStream_t st) {
+                      const int32_t* order, cudaStream_t st, const int64_t* xrows = nullptr,
+                      const int64_t* orows = nullptr) {
   // nbox = number of CTAs' boxes: order[0..nbox) when order != NULL
   if (nbox <= 0 || R <= 0) return 0;
   const size_t optin = (size_t)skel_smem_optin();
@@ -250,16 +261,16 @@ static int level_gemm(int nbox, const int32_t* p, const int32_t* q, const int32_
       SKEL_TRY(cudaFuncSetAttribute(kern_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern_s<<<grid, 128, smem, st>>>(p, q, r, a_off, (const T*)A, b_off, (const T*)B, x_off,
                                       (const T*)X, y_off, (const T*)Y, o_off, (T*)O, R, cols, max_q,
-                                      max_r, order);
+                                      max_r, order, xrows, orows);
     } else {
       kern_g<<<grid, 128, 0, st>>>(p, q, r, a_off, (const T*)A, b_off, (const T*)B, x_off,
                                    (const T*)X, y_off, (const T*)Y, o_off, (T*)O, R, cols, max_q,
-                                   max_r, order);
+                                   max_r, order, xrows, orows);
     }
     return skel_last_error();
   };
   if constexpr (sizeof(T) == sizeof(double)) {
-    if (R >= 64) {
+    if (R >= 64 && !xrows && !orows) {
       constexpr int CB = 32;
       const int maxk = max_q + max_r;
       size_t smem = ((((size_t)max_p + 7) & ~(size_t)7) * (maxk + 1 + 4) +
@@ -281,9 +292,17 @@ static int level_gemm(int nbox, const int32_t* p, const int32_t* q, const int32_
   }
   // register tiles picked per RHS count on B200 (the R=16 sweeps are bound
   // by shared-memory load issue: TN > 1 reuses each staged A element)
-  if (R <= 2) return go(k_level_gemm<T, 4, 1, 2, true>, k_level_gemm<T, 4, 1, 2, false>, 2);
-  if (R <= 8) return go(k_level_gemm<T, 4, 1, 8, true>, k_level_gemm<T, 4, 1, 8, false>, 8);
-  if (R <= 16) return go(k_level_gemm<T, 4, 2, 16, true>, k_level_gemm<T, 4, 2, 16, false>, 16);
+  const bool rows = xrows || orows;
+  if (R <= 2)
+    return rows ? go(k_level_gemm<T, 4, 1, 2, true, true>, k_level_gemm<T, 4, 1, 2, false, true>, 2)
+                : go(k_level_gemm<T, 4, 1, 2, true>, k_level_gemm<T, 4, 1, 2, false>, 2);
+  if (R <= 8)
+    return rows ? go(k_level_gemm<T, 4, 1, 8, true, true>, k_level_gemm<T, 4, 1, 8, false, true>, 8)
+                : go(k_level_gemm<T, 4, 1, 8, true>, k_level_gemm<T, 4, 1, 8, false>, 8);
+  if (R <= 16)
+    return rows ? go(k_level_gemm<T, 4, 2, 16, true, true>, k_level_gemm<T, 4, 2, 16, false, true>, 16)
+                : go(k_level_gemm<T, 4, 2, 16, true>, k_level_gemm<T, 4, 2, 16, false>, 16);
+  if (rows) return -3;                     // row maps: R <= 16 only
   if (R <= 32) return go(k_level_gemm<T, 4, 4, 32, true>, k_level_gemm<T, 4, 4, 32, false>, 32);
   return go(k_level_gemm<T, 4, 4, 64, true>, k_level_gemm<T, 4, 4, 64, false>, 64);
 }
@@ -341,13 +360,22 @@ int skel_sweep_up_ex(int32_t nbox, const int32_t* n, const int32_t* k, const int
                      const int64_t* koff, const int64_t* m_off, const void* M, const void* u,
                      void* out, int32_t R, int32_t field, int32_t max_n, int32_t max_k,
                      const int32_t* order, void* stream) {
+  return skel_sweep_up_rows(nbox, n, k, noff, koff, m_off, M, u, out, R, field, max_n, max_k, order,
+                            nullptr, stream);
+}
+
+int skel_sweep_up_rows(int32_t nbox, const int32_t* n, const int32_t* k, const int64_t* noff,
+                       const int64_t* koff, const int64_t* m_off, const void* M, const void* u,
+                       void* out, int32_t R, int32_t field, int32_t max_n, int32_t max_k,
+                       const int32_t* order, const int64_t* urows, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  // out (k x R) = M (k x n) u (n x R)
+  // out (k x R) = M (k x n) u (n x R); u rows gathered through urows if given
+  if (urows && R > 16) return -3;
   if (field == 0)
     return level_gemm<double>(nbox, k, n, nullptr, m_off, M, nullptr, nullptr, noff, u, nullptr,
-                              nullptr, koff, out, R, max_k, max_n, 0, order, st);
+                              nullptr, koff, out, R, max_k, max_n, 0, order, st, urows, nullptr);
   return level_gemm<zc>(nbox, k, n, nullptr, m_off, M, nullptr, nullptr, noff, u, nullptr, nullptr,
-                        koff, out, R, max_k, max_n, 0, order, st);
+                        koff, out, R, max_k, max_n, 0, order, st, urows, nullptr);
 }
 
 int skel_sweep_down_ex(int32_t nbox, const int32_t* n, const int32_t* k, const int64_t* noff,
@@ -355,13 +383,25 @@ int skel_sweep_down_ex(int32_t nbox, const int32_t* n, const int32_t* k, const i
                        const int64_t* b_off, const void* B, const void* u, const void* v, void* w,
                        int32_t R, int32_t field, int32_t max_n, int32_t max_k,
                        const int32_t* order, void* stream) {
+  return skel_sweep_down_rows(nbox, n, k, noff, koff, a_off, A, b_off, B, u, v, w, R, field, max_n,
+                              max_k, order, nullptr, nullptr, stream);
+}
+
+int skel_sweep_down_rows(int32_t nbox, const int32_t* n, const int32_t* k, const int64_t* noff,
+                         const int64_t* koff, const int64_t* a_off, const void* A,
+                         const int64_t* b_off, const void* B, const void* u, const void* v, void* w,
+                         int32_t R, int32_t field, int32_t max_n, int32_t max_k,
+                         const int32_t* order, const int64_t* urows, const int64_t* wrows,
+                         void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  // w (n x R) = A (n x n) u (n x R) + B (n x k) v (k x R)
+  // w (n x R) = A (n x n) u (n x R) + B (n x k) v (k x R); u rows gathered
+  // through urows, w rows scattered through wrows, if given
+  if ((urows || wrows) && R > 16) return -3;
   if (field == 0)
     return level_gemm<double>(nbox, n, n, k, a_off, A, b_off, B, noff, u, koff, v, noff, w, R, max_n,
-                              max_n, max_k, order, st);
+                              max_n, max_k, order, st, urows, wrows);
   return level_gemm<zc>(nbox, n, n, k, a_off, A, b_off, B, noff, u, koff, v, noff, w, R, max_n, max_n,
-                        max_k, order, st);
+                        max_k, order, st, urows, wrows);
 }
 
 int skel_dense_apply(const void* M, int32_t K, int32_t Kc, const void* x, void* y, int32_t R,

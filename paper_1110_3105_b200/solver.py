@@ -499,8 +499,9 @@ def solve(fi: FactoredInverse, b):
     return x[:, 0] if single else x
 
 
-def _sweep_launch(L, d, direction, u, v, out, Rn, field):
-    """One level of the up- or down-sweep: size buckets on side streams."""
+def _sweep_launch(L, d, direction, u, v, out, Rn, field, urows=None, wrows=None):
+    """One level of the up- or down-sweep: size buckets on side streams.
+    urows / wrows: the finest level's fused gather / scatter (tree order)."""
     torch = _native.require_cuda()
     p_ = _native.ptr
     bks = d.solve_buckets
@@ -513,14 +514,15 @@ def _sweep_launch(L, d, direction, u, v, out, Rn, field):
         if direction == "up":
             if mk == 0:
                 continue
-            _native.check(L.skel_sweep_up_ex(cnt, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
-                                             p_(d.t_ld_off), p_(d.Rd), p_(u), p_(out), Rn, field,
-                                             mn, mk, p_(order), st), "sweep_up")
+            _native.check(L.skel_sweep_up_rows(cnt, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
+                                               p_(d.t_ld_off), p_(d.Rd), p_(u), p_(out), Rn, field,
+                                               mn, mk, p_(order), p_(urows), st), "sweep_up")
         else:
-            _native.check(L.skel_sweep_down_ex(cnt, p_(d.t_n), p_(d.t_k), p_(d.t_noff), p_(d.t_koff),
-                                               p_(d.t_dd_off), p_(d.Dd), p_(d.t_ld_off), p_(d.Ld),
-                                               p_(u), p_(v), p_(out), Rn, field, mn, mk, p_(order),
-                                               st), "sweep_down")
+            _native.check(L.skel_sweep_down_rows(cnt, p_(d.t_n), p_(d.t_k), p_(d.t_noff),
+                                                 p_(d.t_koff), p_(d.t_dd_off), p_(d.Dd),
+                                                 p_(d.t_ld_off), p_(d.Ld), p_(u), p_(v), p_(out), Rn,
+                                                 field, mn, mk, p_(order), p_(urows), p_(wrows), st),
+                          "sweep_down")
     if streams:
         join(streams)
 
@@ -588,8 +590,14 @@ def _solve_device_eager(fi: FactoredInverse, B):
     field = fi.field
     Rn = B.shape[1]
     perm = fi.perm_dev()
-    bt = torch.empty_like(B)
-    _native.check(L.skel_permute_rows(p_(perm), fi.n, p_(B), p_(bt), Rn, 0, field, st), "permute")
+    # few RHS, one rank: the tree-order gather of B and scatter of X are fused
+    # into the finest level's sweeps (row maps), no permuted copies
+    fuse = bool(fi.levels) and fi.shard is None and Rn <= 16 and B.is_contiguous()
+    if fuse:
+        bt, rows = B, perm
+    else:
+        bt, rows = torch.empty_like(B), None
+        _native.check(L.skel_permute_rows(p_(perm), fi.n, p_(B), p_(bt), Rn, 0, field, st), "permute")
     if not fi.levels:
         xt = _dense_apply(fi.S_inv, bt, field) if fi.S_inv is not None else bt
     else:
@@ -601,7 +609,7 @@ def _solve_device_eager(fi: FactoredInverse, B):
             sh = d.mine is not None
             nxt = torch.empty((int(d.k.sum()), Rn), dtype=B.dtype, device="cuda")
             with _profile.timed("sweep", dir="up") as rec:
-                _sweep_launch(L, d, "up", u, None, nxt, Rn, field)
+                _sweep_launch(L, d, "up", u, None, nxt, Rn, field, urows=rows if li == 0 else None)
             if sh and li == shard.split:
                 # split-level vector: every rank's rows, on every rank
                 shard.gather_rows(nxt, _off(d.k), li)
@@ -613,15 +621,19 @@ def _solve_device_eager(fi: FactoredInverse, B):
         for li in range(len(fi.levels) - 1, -1, -1):
             d = fi.levels[li].dev
             sh = d.mine is not None
+            last = li == 0 and fuse
             w = torch.empty((int(d.n.sum()), Rn), dtype=B.dtype, device="cuda")
             with _profile.timed("sweep", dir="down") as rec:
-                _sweep_launch(L, d, "down", us[li], v, w, Rn, field)
+                _sweep_launch(L, d, "down", us[li], v, w, Rn, field, urows=rows if li == 0 else None,
+                              wrows=rows if last else None)
             if sh and li == 0:
                 shard.gather_rows(w, _off(d.n), 0)   # every rank's solution rows
             if rec is not None:
                 _sweep_work(rec, d, Rn, field, up=False)
             v = w
         xt = v
+        if fuse:
+            return xt                                 # already in original order
     X = torch.empty_like(xt)
     _native.check(L.skel_permute_rows(p_(perm), fi.n, p_(xt), p_(X), Rn, 1, field, st), "permute")
     return X
