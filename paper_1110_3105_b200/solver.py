@@ -66,13 +66,10 @@ def _solve_buckets(n):
     """Boxes grouped by size so each sweep launch sizes its shared memory for
     its own boxes (more CTAs per SM for the many small ones)."""
     cls = np.searchsorted(np.asarray(_SOLVE_CLASSES), n, side="left")
-    if _SOLVE_MERGE[0] and n.size <= _SOLVE_MERGE[0]:
-        cls = np.minimum(cls, _SOLVE_MERGE[1])       # few boxes: fewer, wider launches
     return size_buckets(np.where(n > 0, cls, -1))
 
 
-_SOLVE_MERGE = [int(__import__("os").environ.get("SKEL_SOLVE_MERGE", "0")),
-                int(__import__("os").environ.get("SKEL_SOLVE_MERGE_CLS", "0"))]
+
 
 
 class FactoredLevel:
@@ -308,7 +305,7 @@ class FactorRun:
             pk.add("dd_off", dd_off).add("ld_off", ld_off).add("lam_off", lam_off)
             for bi, sel in enumerate(buckets):
                 pk.add(f"order{bi}", sel)
-            sv = pl.sbuckets if not _SOLVE_MERGE[0] else _solve_buckets(n_own)
+            sv = pl.sbuckets
             for bi, sel in enumerate(sv):
                 pk.add(f"sv{bi}", sel)
             t = pk.upload()
