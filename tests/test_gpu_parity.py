@@ -369,3 +369,48 @@ def test_full_size_config2_properties():
     assert np.linalg.norm(Y - B) / np.linalg.norm(B) <= 1e-10
     assert cm.S_shape()[0] <= 400 and cm.nlevels == 14
     assert abs(fi.factor_bytes() / n - 1784) < 60
+
+
+@gpu
+@pytest.mark.parametrize("R", [1, 2, 7, 16, 33, 64, 200])
+def test_multi_rhs_widths_agree(R):
+    """Every RHS-width path of the sweeps (row-map fused R <= 16, register
+    tiles for R <= 32 / 64, DMMA for R >= 64, graph replay on repeat) gives
+    the columns of the single-column solve, and matches the oracle."""
+    sk = _sk()
+    n = 4096
+    curve = sk.bie.ellipse(2.0, 1.0, n)
+    system = sk.bie.discretize_dirichlet(curve, sk.KernelSpec("laplace", 2))
+    tree, cm = sk.bie.compress_system(system, 1e-10, 64)
+    fi = sk.factor(cm)
+    B = np.random.default_rng(R).standard_normal((n, R))
+    X = sk.solve(fi, B)
+    for c in (0, R // 2, R - 1):
+        xc = sk.solve(fi, B[:, c])
+        np.testing.assert_allclose(X[:, c], xc, rtol=0, atol=1e-12 * np.abs(xc).max())
+    import torch
+    Bd = torch.from_numpy(B).cuda()
+    X1 = sk.solve_device(fi, Bd)
+    X2 = sk.solve_device(fi, Bd)            # graph capture + replay
+    X3 = sk.solve_device(fi, Bd)
+    np.testing.assert_array_equal(X2.cpu().numpy(), X3.cpu().numpy())
+    np.testing.assert_allclose(X1.cpu().numpy(), X, rtol=0, atol=1e-12 * np.abs(X).max())
+
+
+@gpu
+def test_config3_full_size_residual():
+    """BASELINE config 3 at its full size: CFIE (complex128) on the ellipse,
+    N = 2^18, perimeter = 8 wavelengths, eps = 1e-9, 4 complex RHS."""
+    sk = _sk()
+    n = 2 ** 18
+    k = 2 * np.pi * 8 / oracle.ellipse_perimeter(2.0, 1.0)
+    curve = sk.bie.ellipse(2.0, 1.0, n)
+    system = sk.bie.combined_field_system(curve, k)
+    tree, cm = sk.bie.compress_system(system, 1e-9, 64)
+    fi = sk.factor(cm)
+    rng = np.random.default_rng(0)
+    B = rng.standard_normal((n, 4)) + 1j * rng.standard_normal((n, 4))
+    X = sk.solve(fi, B)
+    src = sk.bie.BieSource(system, tree.perm)
+    res = np.linalg.norm(sk.bie.dense_matvec(src, X[:, :1]) - B[:, :1]) / np.linalg.norm(B[:, :1])
+    assert res <= 1e-7, res
