@@ -379,12 +379,21 @@ class FactorRun:
             torch.cuda.current_stream().wait_event(ev)
         warns = []
         flevels = []
-        for li, ((sq_bad, lam_bad, n, k), fl, status, rcd, rcm, dl) in enumerate(self.levels):
+        for (_, fl, status, rcd, rcm, _) in self.levels:
             if fl.mine is not None:
                 self.shard.all_reduce(status, "max")
                 self.shard.all_reduce(rcd, "min")
                 self.shard.all_reduce(rcm, "min")
-            sts, rd_h, rm_h = status.cpu().numpy(), rcd.cpu().numpy(), rcm.cpu().numpy()
+        # every level's status / rcond in one device->host copy
+        if self.levels:
+            cat_s = torch.cat([x[2] for x in self.levels]).cpu().numpy()
+            cat_r = torch.cat([torch.cat([x[3], x[4]]) for x in self.levels]).cpu().numpy()
+        so, ro = 0, 0
+        for li, ((sq_bad, lam_bad, n, k), fl, status, rcd, rcm, dl) in enumerate(self.levels):
+            p = status.numel()
+            sts = cat_s[so:so + p]
+            rd_h, rm_h = cat_r[ro:ro + p], cat_r[ro + p:ro + 2 * p]
+            so, ro = so + p, ro + 2 * p
             fails = np.nonzero(sq_bad | lam_bad | (sts != 0))[0]
             if fails.size:
                 a = int(fails[0])
