@@ -10,6 +10,7 @@
 // the input segment(s) is staged in shared memory, factor blocks are streamed
 // from HBM exactly once per chunk (read-only path), each thread owns one
 // output (row, column) pair.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -238,6 +239,100 @@ __global__ void __launch_bounds__(128) k_level_dmma(
   }
 }
 
+// DMMA variant for few RHS (R <= 8 * NT): one CTA per box, one warp per
+// 8-row output tile with NT 8x8 accumulators.  Only the (small) X / Y slab is
+// staged in shared memory; the factor blocks A (p x q) and B (p x r) -- the
+// bytes that bound the sweep -- go straight from HBM into the A fragments
+// (each lane reads 4 consecutive doubles of one row per k-step, the unrolled
+// k-loop keeps several loads in flight), so there is no shared-memory round
+// trip and no CTA-wide barrier for them.  Slab layout: rows [0, q) = X,
+// zero pad to Qp = q rounded up to 4, rows [Qp, Qp + r) = Y, pad to 4;
+// row stride 8 * NT + 8 doubles so a B-fragment load touches each bank pair
+// exactly twice (the 2-wavefront minimum for 32 doubles).
+template <int NT, bool ROWS>
+__global__ void __launch_bounds__(256) k_level_dmma_few(
+    const int32_t* __restrict__ pp, const int32_t* __restrict__ qq, const int32_t* __restrict__ rr,
+    const int64_t* __restrict__ a_off, const double* __restrict__ A,
+    const int64_t* __restrict__ b_off, const double* __restrict__ Bm,
+    const int64_t* __restrict__ x_off, const double* __restrict__ X,
+    const int64_t* __restrict__ y_off, const double* __restrict__ Y,
+    const int64_t* __restrict__ o_off, double* __restrict__ O, int R,
+    const int32_t* __restrict__ order, const int64_t* __restrict__ xrows,
+    const int64_t* __restrict__ orows) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int CW = 8 * NT, LDX = CW + 8;
+  const int a = order ? order[blockIdx.x] : blockIdx.x;
+  const int p = pp[a], q = qq[a], r = rr ? rr[a] : 0;
+  if (p == 0) return;
+  const int Qp = (q + 3) & ~3, Rp = (r + 3) & ~3, Kp = Qp + Rp;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  double* sX = reinterpret_cast<double*>(smem);
+  const int64_t* xr = (ROWS && xrows) ? xrows + x_off[a] : nullptr;
+  const int64_t* orw = (ROWS && orows) ? orows + o_off[a] : nullptr;
+  for (int e = tid; e < Kp * CW; e += nt) {
+    const int j = e / CW, c = e - j * CW;
+    double* d = sX + j * LDX + c;
+    const double* src = nullptr;
+    if (c < R) {
+      if (j < q) src = (xr ? X + xr[j] * R : X + (x_off[a] + j) * R) + c;
+      else if (j >= Qp && j - Qp < r) src = Y + (y_off[a] + (j - Qp)) * R + c;
+    }
+    if (src) cp_async8(d, src);
+    else *d = 0.0;
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const int g = lane >> 2, t4 = lane & 3;
+  const int ntile = (p + 7) >> 3;
+  for (int rt = warp; rt < ntile; rt += nt >> 5) {
+    const int row = rt * 8 + g;
+    const bool ok = row < p;
+    double acc[NT][2];
+#pragma unroll
+    for (int u = 0; u < NT; ++u) acc[u][0] = acc[u][1] = 0.0;
+    const double* arow = A + a_off[a] + (int64_t)(ok ? row : 0) * q;
+    const double* xs = sX + t4 * LDX + g;
+#pragma unroll 4
+    for (int k0 = 0; k0 < Qp; k0 += 4) {
+      const double av = (ok && k0 + t4 < q) ? __ldg(arow + k0 + t4) : 0.0;
+#pragma unroll
+      for (int u = 0; u < NT; ++u) dmma884(acc[u][0], acc[u][1], av, xs[k0 * LDX + u * 8]);
+    }
+    if (r) {
+      const double* brow = Bm + b_off[a] + (int64_t)(ok ? row : 0) * r;
+      const double* ys = xs + Qp * LDX;
+#pragma unroll 4
+      for (int k0 = 0; k0 < Rp; k0 += 4) {
+        const double bv = (ok && k0 + t4 < r) ? __ldg(brow + k0 + t4) : 0.0;
+#pragma unroll
+        for (int u = 0; u < NT; ++u) dmma884(acc[u][0], acc[u][1], bv, ys[k0 * LDX + u * 8]);
+      }
+    }
+    if (ok) {
+      double* orow = orw ? O + orw[row] * R : O + (o_off[a] + row) * R;
+#pragma unroll
+      for (int u = 0; u < NT; ++u) {
+        const int col = u * 8 + 2 * t4;
+        if (col + 1 < R && !(R & 1)) {
+          *reinterpret_cast<double2*>(orow + col) = make_double2(acc[u][0], acc[u][1]);
+        } else {
+          if (col < R) orow[col] = acc[u][0];
+          if (col + 1 < R) orow[col + 1] = acc[u][1];
+        }
+      }
+    }
+  }
+}
+
+static bool dmma_few_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SKEL_SOLVE_DMMA_FEW");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <class T>
 static int level_gemm(int nbox, const int32_t* p, const int32_t* q, const int32_t* r,
                       const int64_t* a_off, const void* A, const int64_t* b_off, const void* B,
@@ -270,6 +365,25 @@ static int level_gemm(int nbox, const int32_t* p, const int32_t* q, const int32_
     return skel_last_error();
   };
   if constexpr (sizeof(T) == sizeof(double)) {
+    if (R >= 3 && R <= 32 && dmma_few_enabled()) {
+      const int nt = R <= 8 ? 1 : (R <= 16 ? 2 : 4);
+      const int kmax = ((max_q + 3) & ~3) + ((max_r + 3) & ~3);
+      const size_t smem = (size_t)kmax * (8 * nt + 8) * sizeof(double);
+      const int threads = 32 * std::min(8, std::max(1, (max_p + 7) / 8));
+      if (smem <= optin) {
+        const bool rows = xrows || orows;
+        auto launch = [&](auto kern) -> int {
+          SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          kern<<<nbox, threads, smem, st>>>(p, q, r, a_off, (const double*)A, b_off, (const double*)B,
+                                            x_off, (const double*)X, y_off, (const double*)Y, o_off,
+                                            (double*)O, R, order, xrows, orows);
+          return skel_last_error();
+        };
+        if (nt == 1) return rows ? launch(k_level_dmma_few<1, true>) : launch(k_level_dmma_few<1, false>);
+        if (nt == 2) return rows ? launch(k_level_dmma_few<2, true>) : launch(k_level_dmma_few<2, false>);
+        return rows ? launch(k_level_dmma_few<4, true>) : launch(k_level_dmma_few<4, false>);
+      }
+    }
     if (R >= 64 && !xrows && !orows) {
       constexpr int CB = 32;
       const int maxk = max_q + max_r;
