@@ -12,6 +12,7 @@
 // output (row, column) pair.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -325,6 +326,162 @@ __global__ void __launch_bounds__(256) k_level_dmma_few(
   }
 }
 
+// Pipelined DMMA variant for many RHS.  One CTA per (box, column range);
+// [A | B] is staged in shared memory once (row stride = 4 mod 16 doubles, so
+// an A-fragment load is conflict-free).  A warp task is up to MT 8-row tiles
+// x 16 columns, columns paired so lane g of n-tile u holds column c0 + 2g + u
+// (one 16-byte load feeds both n-tiles; each lane stores 4 consecutive
+// outputs).  Each warp streams its X / Y rows through a private NS-stage
+// shared-memory ring with 16-byte cp.async: the bytes in flight live in
+// shared memory, not registers, so NS - 1 chunks of 16 rows x 16 columns per
+// warp are outstanding while the DMMAs of the current chunk issue; every B
+// fragment feeds all the task's row tiles.  No CTA-wide barrier after the A
+// stage (the ring is warp-private, __syncwarp only).
+template <int MT, int NS>
+__global__ void __launch_bounds__(256, 2) k_level_dmma_pipe(
+    const int32_t* __restrict__ pp, const int32_t* __restrict__ qq, const int32_t* __restrict__ rr,
+    const int64_t* __restrict__ a_off, const double* __restrict__ A,
+    const int64_t* __restrict__ b_off, const double* __restrict__ Bm,
+    const int64_t* __restrict__ x_off, const double* __restrict__ X,
+    const int64_t* __restrict__ y_off, const double* __restrict__ Y,
+    const int64_t* __restrict__ o_off, double* __restrict__ O, int R, int cols_per_cta,
+    const int32_t* __restrict__ order, int a_words) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int CW = 16, KC = 16;       // columns per task, K rows per chunk
+  constexpr int RING = NS * KC * CW;    // doubles per warp ring
+  const int a = order ? order[blockIdx.x] : blockIdx.x;
+  const int p = pp[a], q = qq[a], r = rr ? rr[a] : 0;
+  if (p == 0) return;
+  const int cbeg = blockIdx.y * cols_per_cta;
+  const int cend = min(R, cbeg + cols_per_cta);
+  if (cbeg >= cend) return;
+  const int Qp = (q + 3) & ~3, Kp = Qp + ((r + 3) & ~3);
+  const int ldA = Kp + ((4 - Kp) & 15);
+  const int P8 = (p + 7) & ~7;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  double* sA = reinterpret_cast<double*>(smem);
+  double* ring = sA + a_words + warp * RING;
+  const double* Ag = A + a_off[a];
+  const double* Bg = r ? Bm + b_off[a] : nullptr;
+  for (int e = tid; e < P8 * Kp; e += nt) {
+    const int i = e / Kp, j = e - i * Kp;
+    double* d = sA + i * ldA + j;
+    if (i < p && j < q) cp_async8(d, Ag + (int64_t)i * q + j);
+    else if (i < p && j >= Qp && j - Qp < r) cp_async8(d, Bg + (int64_t)i * r + (j - Qp));
+    else *d = 0.0;
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const int g = lane >> 2, t4 = lane & 3;
+  const int ntile = P8 >> 3, nrb = (ntile + MT - 1) / MT;
+  const int ncg = (cend - cbeg + CW - 1) / CW;
+  const int nch = (Kp + KC - 1) / KC;
+  const double* Xb = X + x_off[a] * R;
+  const double* Yb = r ? Y + (y_off[a] - Qp) * R : nullptr;   // row k >= Qp is Y row k - Qp
+  double* Og = O + o_off[a] * R;
+  const bool even = !(R & 1);
+  for (int task = warp; task < nrb * ncg; task += nt >> 5) {
+    const int rb = task / ncg, cg = task - rb * ncg;
+    const int c0 = cbeg + cg * CW;
+    const bool full = c0 + CW <= cend && even;
+    // chunk c -> ring slot c % NS: 16 rows x 8 16-byte pieces, 4 per lane
+    auto issue = [&](int c) {
+      double* slot = ring + (c % NS) * (KC * CW);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int piece = lane + 32 * t, row = piece >> 3, pc = (piece & 7) * 2;
+        const int k = c * KC + row;
+        const double* src = k < q ? Xb : ((k >= Qp && k - Qp < r) ? Yb : nullptr);
+        double* d = slot + row * CW + pc;
+        if (src && full) {
+          cp_async16(d, src + (int64_t)k * R + c0 + pc);
+        } else {
+          d[0] = (src && c0 + pc < cend) ? __ldg(src + (int64_t)k * R + c0 + pc) : 0.0;
+          d[1] = (src && c0 + pc + 1 < cend) ? __ldg(src + (int64_t)k * R + c0 + pc + 1) : 0.0;
+        }
+      }
+    };
+    double acc[MT][2][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) acc[m][0][0] = acc[m][0][1] = acc[m][1][0] = acc[m][1][1] = 0.0;
+    auto chunk = [&](auto mc, double (&ac)[MT][2][2], const double* slot, int kc, int ns, int rb_) {
+      constexpr int M = decltype(mc)::value;
+      const double* arow = sA + (rb_ * MT * 8 + g) * ldA + kc + t4;
+      auto step = [&](int s) {
+        const double2 b = *reinterpret_cast<const double2*>(slot + 4 * s * CW);
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const double av = arow[m * 8 * ldA + 4 * s];
+          dmma884(ac[m][0][0], ac[m][0][1], av, b.x);
+          dmma884(ac[m][1][0], ac[m][1][1], av, b.y);
+        }
+      };
+      if (ns == KC / 4) {
+#pragma unroll
+        for (int s = 0; s < KC / 4; ++s) step(s);
+      } else {
+#pragma unroll 1
+        for (int s = 0; s < ns; ++s) step(s);
+      }
+    };
+#pragma unroll
+    for (int c = 0; c < NS - 1; ++c) {
+      if (c < nch) issue(c);
+      cp_async_commit();
+    }
+    for (int c = 0; c < nch; ++c) {
+      cp_async_wait<NS - 2>();
+      __syncwarp();
+      const double* slot = ring + (c % NS) * (KC * CW) + t4 * CW + 2 * g;
+      const int kc = c * KC;
+      const int ns = min(KC / 4, (Kp - kc) >> 2);
+      // exact row-tile count and k-step count: a predicated-off DMMA still
+      // occupies the FP64 tensor pipe, so nothing here is guarded per step
+      switch (min(MT, ntile - rb * MT)) {
+        case 1: chunk(std::integral_constant<int, 1>(), acc, slot, kc, ns, rb); break;
+        case 2: chunk(std::integral_constant<int, 2>(), acc, slot, kc, ns, rb); break;
+        case 3: chunk(std::integral_constant<int, 3>(), acc, slot, kc, ns, rb); break;
+        case 4: chunk(std::integral_constant<int, 4>(), acc, slot, kc, ns, rb); break;
+        case 5: if constexpr (MT >= 5) chunk(std::integral_constant<int, 5>(), acc, slot, kc, ns, rb); break;
+        case 6: if constexpr (MT >= 6) chunk(std::integral_constant<int, 6>(), acc, slot, kc, ns, rb); break;
+        case 7: if constexpr (MT >= 7) chunk(std::integral_constant<int, 7>(), acc, slot, kc, ns, rb); break;
+        default: if constexpr (MT >= 8) chunk(std::integral_constant<int, 8>(), acc, slot, kc, ns, rb); break;
+      }
+      __syncwarp();   // every lane is done with slot c % NS before it is refilled
+      if (c + NS - 1 < nch) issue(c + NS - 1);
+      cp_async_commit();
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    const int col = c0 + 4 * t4;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      const int row = (rb * MT + m) * 8 + g;
+      if (row < p) {
+        double* orow = Og + (int64_t)row * R + col;
+        if (full) {
+          *reinterpret_cast<double2*>(orow) = make_double2(acc[m][0][0], acc[m][1][0]);
+          *reinterpret_cast<double2*>(orow + 2) = make_double2(acc[m][0][1], acc[m][1][1]);
+        } else {
+          if (col < cend) orow[0] = acc[m][0][0];
+          if (col + 1 < cend) orow[1] = acc[m][1][0];
+          if (col + 2 < cend) orow[2] = acc[m][0][1];
+          if (col + 3 < cend) orow[3] = acc[m][1][1];
+        }
+      }
+    }
+  }
+}
+
+static int dmma_many_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("SKEL_SOLVE_DMMA_MANY");
+    return e ? std::atoi(e) : 1;
+  }();
+  return mode;
+}
+
 static bool dmma_few_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("SKEL_SOLVE_DMMA_FEW");
@@ -382,6 +539,30 @@ static int level_gemm(int nbox, const int32_t* p, const int32_t* q, const int32_
         if (nt == 1) return rows ? launch(k_level_dmma_few<1, true>) : launch(k_level_dmma_few<1, false>);
         if (nt == 2) return rows ? launch(k_level_dmma_few<2, true>) : launch(k_level_dmma_few<2, false>);
         return rows ? launch(k_level_dmma_few<4, true>) : launch(k_level_dmma_few<4, false>);
+      }
+    }
+    if (R >= 64 && !xrows && !orows && dmma_many_mode() == 1) {
+      const int kp = ((max_q + 3) & ~3) + ((max_r + 3) & ~3);
+      {
+        int chunks = (R + 31) / 32;
+        int per = 1;
+        while (per < chunks && (long long)nbox * ((chunks + per * 2 - 1) / (per * 2)) >= 4LL * 148 * 4) per *= 2;
+        const int cols = per * 32;
+        dim3 grid(nbox, (R + cols - 1) / cols);
+        const int tasks = ((max_p + 7) / 8 + 7) / 8 * ((cols + 15) / 16);
+        const int threads = 32 * std::min(8, tasks);
+        const int aw = (int)((((size_t)max_p + 7) & ~(size_t)7) * (kp + 16));
+        const size_t psmem = (size_t)aw * sizeof(double) + (size_t)(threads / 32) * 4 * 16 * 16 * sizeof(double);
+        if (psmem <= optin) {
+          auto launch = [&](auto kern) -> int {
+            SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+            kern<<<grid, threads, psmem, st>>>(p, q, r, a_off, (const double*)A, b_off, (const double*)B,
+                                               x_off, (const double*)X, y_off, (const double*)Y, o_off,
+                                               (double*)O, R, cols, order, aw);
+            return skel_last_error();
+          };
+          return max_p <= 32 ? launch(k_level_dmma_pipe<4, 4>) : launch(k_level_dmma_pipe<8, 4>);
+        }
       }
     }
     if (R >= 64 && !xrows && !orows) {
