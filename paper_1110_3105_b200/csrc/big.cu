@@ -242,34 +242,37 @@ __global__ void __launch_bounds__(256)
     for (int c = s1 + gw; c < n; c += tw) {
       const int col = (c == j) ? ps_old : ldcg(pcur + c);
       T* wc = W + (int64_t)col * ld;
-      // 4 rows per lane per pass: independent loads in flight, 4 partial sums
+      // U rows per lane per pass (all loads of a pass issued before any use:
+      // the trailing matrix lives in L2 / HBM, so the pass is load-latency
+      // bound), 4 partial sums
+      constexpr int U = sizeof(T) == sizeof(double) ? 16 : 8;
       T d4[4] = {T(0.0), T(0.0), T(0.0), T(0.0)};
-      for (int i0 = s; i0 < m; i0 += 128) {
-        T wv[4], vq[4];
+      for (int i0 = s; i0 < m; i0 += 32 * U) {
+        T wv[U], vq[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int i = i0 + lane + 32 * u;
           wv[u] = i < m ? ldcg(wc + i) : T(0.0);
           vq[u] = i < m ? (vsmem ? vs[i] : ((i == s) ? v0 : ldcg(vcol + i))) : T(0.0);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) d4[u] += sk_conj(vq[u]) * wv[u];
+        for (int u = 0; u < U; ++u) d4[u & 3] += sk_conj(vq[u]) * wv[u];
       }
       T dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
       dot = warp_sum(dot);
       const T f = dot * beta;
       double a4[4] = {0.0, 0.0, 0.0, 0.0};
       T row = T(0.0);
-      for (int i0 = s; i0 < m; i0 += 128) {
-        T wv[4], vq[4];
+      for (int i0 = s; i0 < m; i0 += 32 * U) {
+        T wv[U], vq[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int i = i0 + lane + 32 * u;
           wv[u] = i < m ? ldcg(wc + i) : T(0.0);
           vq[u] = i < m ? (vsmem ? vs[i] : ((i == s) ? v0 : ldcg(vcol + i))) : T(0.0);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int i = i0 + lane + 32 * u;
           if (i < m) {
             T w = wv[u];
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(256)
               w -= vq[u] * f;
               wc[i] = w;
             }
-            if (i > s) a4[u] += sk_abs2(w);
+            if (i > s) a4[u & 3] += sk_abs2(w);
             if (i == s) row = w;
           }
         }
