@@ -486,6 +486,8 @@ inline bool touch(const Tree& T, int64_t na, int64_t nb, double tol) {
 
 void all_neighbors(Tree& T) {
   if (T.nbr_done) return;
+  const bool timing = getenv("SKEL_TREE_TIMING") != nullptr;
+  const double tn0 = now_ms();
   const int nc = (int)T.covers.size();
   T.nbr_off.assign(nc, {});
   T.nbr_idx.assign(nc, {});
@@ -514,20 +516,48 @@ void all_neighbors(Tree& T) {
       for (int64_t t = cstart[u]; t < cstart[u + 1]; ++t) par[t] = u;
     const std::vector<int64_t>& uoff = T.nbr_off[li + 1];
     const std::vector<int64_t>& uidx = T.nbr_idx[li + 1];
-    std::vector<int64_t> cand;
-    for (int64_t a = 0; a < p; ++a) {
-      cand.clear();
-      const int64_t u = par[a];
-      auto take = [&](int64_t w) {
-        for (int64_t t = cstart[w]; t < cstart[w + 1]; ++t)
-          if (t != a && touch(T, ids[a], ids[t], tol)) cand.push_back(t);
-      };
-      take(u);
-      for (int64_t s = uoff[u]; s < uoff[u + 1]; ++s) take(uidx[s]);
-      std::sort(cand.begin(), cand.end());
-      idx.insert(idx.end(), cand.begin(), cand.end());
-      off[a + 1] = (int64_t)idx.size();
+    // candidates of boxes a0..a1: the children of the cover parent and of
+    // the parent's neighbours, sorted; appended to out, counts per box
+    auto scan = [&](int64_t a0, int64_t a1, std::vector<int64_t>& out, int64_t* cnt) {
+      std::vector<int64_t> cand;
+      for (int64_t a = a0; a < a1; ++a) {
+        cand.clear();
+        const int64_t u = par[a];
+        auto take = [&](int64_t w) {
+          for (int64_t t = cstart[w]; t < cstart[w + 1]; ++t)
+            if (t != a && touch(T, ids[a], ids[t], tol)) cand.push_back(t);
+        };
+        take(u);
+        for (int64_t s = uoff[u]; s < uoff[u + 1]; ++s) take(uidx[s]);
+        std::sort(cand.begin(), cand.end());
+        out.insert(out.end(), cand.begin(), cand.end());
+        cnt[a - a0] = (int64_t)cand.size();
+      }
+    };
+    std::vector<int64_t> cnt(p);
+    unsigned hwc = std::thread::hardware_concurrency();
+    const int nt = p >= 4096 ? (int)std::max(1u, std::min(hwc == 0 ? 1u : hwc, 16u)) : 1;
+    if (nt == 1) {
+      scan(0, p, idx, cnt.data());
+    } else {
+      // boxes are independent given the parent cover's lists: chunks in
+      // parallel, concatenated in box order (identical to the serial lists)
+      const int64_t chunk = (p + nt - 1) / nt;
+      std::vector<std::vector<int64_t>> part(nt);
+      std::vector<std::thread> th;
+      for (int t = 0; t < nt; ++t) {
+        const int64_t a0 = std::min(p, t * chunk), a1 = std::min(p, (t + 1) * chunk);
+        th.emplace_back([&, t, a0, a1]() { scan(a0, a1, part[t], cnt.data() + a0); });
+      }
+      for (auto& x : th) x.join();
+      size_t tot = 0;
+      for (auto& v : part) tot += v.size();
+      idx.reserve(tot);
+      for (auto& v : part) idx.insert(idx.end(), v.begin(), v.end());
     }
+    for (int64_t a = 0; a < p; ++a) off[a + 1] = off[a] + cnt[a];
+    if (timing) fprintf(stderr, "nbr level %d: %lld boxes, %d threads, %.2f ms since start\n", li,
+                        (long long)p, nt, now_ms() - tn0);
   }
   T.nbr_done = true;
 }
