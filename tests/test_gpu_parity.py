@@ -398,6 +398,43 @@ def test_multi_rhs_widths_agree(R):
 
 
 @gpu
+def test_solve_graph_paths():
+    """The replayed solve graphs: the private-buffer graph (any B) and the
+    graph captured on a repeated B tensor read the CURRENT right-hand sides
+    (in-place updates of the same tensor, other tensors interleaved), never
+    write into the caller's B, and return fresh tensors."""
+    import torch
+    sk = _sk()
+    n = 4096
+    curve = sk.bie.ellipse(2.0, 1.0, n)
+    system = sk.bie.discretize_dirichlet(curve, sk.KernelSpec("laplace", 2))
+    tree, cm = sk.bie.compress_system(system, 1e-10, 64)
+    fi = sk.factor(cm)
+    rng = np.random.default_rng(5)
+    Bs = [rng.standard_normal((n, 16)) for _ in range(4)]
+    ref = [sk.solve(fi, b) for b in Bs]
+    tol = lambda x: 1e-12 * np.abs(x).max()  # noqa: E731
+    Bd = torch.from_numpy(Bs[0].copy()).cuda()
+    other = torch.from_numpy(Bs[1].copy()).cuda()
+    outs = []
+    for it in range(6):
+        X = sk.solve_device(fi, Bd)
+        np.testing.assert_allclose(X.cpu().numpy(), ref[0], rtol=0, atol=tol(ref[0]))
+        outs.append(X)
+        Y = sk.solve_device(fi, other)
+        np.testing.assert_allclose(Y.cpu().numpy(), ref[1], rtol=0, atol=tol(ref[1]))
+    # the same tensor, new contents: the pointer-bound graph reads them
+    for k in (2, 3, 0):
+        Bd.copy_(torch.from_numpy(Bs[k]))
+        X = sk.solve_device(fi, Bd)
+        np.testing.assert_allclose(X.cpu().numpy(), ref[k], rtol=0, atol=tol(ref[k]))
+    np.testing.assert_array_equal(other.cpu().numpy(), Bs[1])       # caller's B untouched
+    assert len({o.data_ptr() for o in outs}) == len(outs)           # fresh results
+    for o in outs:
+        np.testing.assert_allclose(o.cpu().numpy(), ref[0], rtol=0, atol=tol(ref[0]))
+
+
+@gpu
 def test_config3_full_size_residual():
     """BASELINE config 3 at its full size: CFIE (complex128) on the ellipse,
     N = 2^18, perimeter = 8 wavelengths, eps = 1e-9, 4 complex RHS."""
