@@ -548,51 +548,52 @@ def _sweep_work(rec, d, Rn, field, up):
 
 
 _GRAPH_CACHE = 4
+_GRAPH_MAX_R = 64
 
 
 def solve_device(fi: FactoredInverse, B, graph: bool = True):
     """Device-resident solve of an (N, R) CUDA tensor (original ordering).
 
     The ~30-40 launches of one solve (gather, per-level size-bucketed sweeps
-    on side streams, top GEMM, scatter) are captured once per (R, dtype) into
-    a CUDA graph and replayed: B is copied into the graph's static input and
-    the result copied out.  When the SAME contiguous B tensor comes back
-    (few RHS, the multi-RHS reuse pattern), a second graph captured on that
-    tensor itself is replayed with no input copy (the cache holds a
-    reference, so the storage cannot be recycled under the graph)."""
+    on side streams, top GEMM, scatter) are captured into a CUDA graph on the
+    first repeat of a shape and replayed from then on.  When the SAME
+    contiguous B tensor comes back (the multi-RHS reuse pattern) the graph is
+    captured on that tensor itself and replays with no input copy (the cache
+    holds a reference, so the storage cannot be recycled under the graph);
+    other tensors of that shape are copied into a private-input graph.  The
+    result is always a fresh tensor."""
     torch = _native.require_cuda()
     if (not graph or _profile.enabled or torch.cuda.is_current_stream_capturing()
-            or fi.shard is not None):
+            or fi.shard is not None or B.shape[1] > _GRAPH_MAX_R):
+        # many RHS: launch overhead is noise next to the sweeps, and the
+        # graph's output copy would not be (8.6 GB at 2^20 x 1024)
         return _solve_device_eager(fi, B)
     key = (int(B.shape[1]), B.dtype)
+    pkey = key + (B.data_ptr(), tuple(B.stride()))
     cache = fi.__dict__.setdefault("_graphs", {})
     seen = fi.__dict__.setdefault("_graph_seen", set())
-    ent = cache.get(key)
-    if ent is None and key not in seen:
-        # first solve with this shape runs eagerly; a repeat (the multi-RHS
-        # reuse pattern) pays the one-time capture and replays from then on
-        seen.add(key)
-        return _solve_device_eager(fi, B)
-    if ent is None:
-        static_B = torch.empty_like(B)
-        static_B.copy_(B)
-        ent = cache[key] = _capture(fi, static_B, cache)
-    pkey = key + (B.data_ptr(), tuple(B.stride()))
-    pent = cache.get(pkey)
-    if pent is None and B.is_contiguous() and key[0] <= _PTR_GRAPH_MAX_R \
-            and fi.__dict__.get("_last_pkey") == pkey:
-        pent = cache[pkey] = _capture(fi, B, cache)
+    last = fi.__dict__.get("_last_pkey")
     fi.__dict__["_last_pkey"] = pkey
-    if pent is not None:
-        g, _, static_X = pent
+    ent = cache.get(pkey)
+    if ent is None and pkey == last and B.is_contiguous():
+        ent = cache[pkey] = _capture(fi, B, cache)          # same tensor again
+    if ent is not None:
+        g, _, static_X = ent
     else:
+        ent = cache.get(key)
+        if ent is None and key not in seen:
+            # first solve with this shape runs eagerly; a repeat pays the
+            # one-time capture and replays from then on
+            seen.add(key)
+            return _solve_device_eager(fi, B)
+        if ent is None:
+            static_B = torch.empty_like(B)
+            static_B.copy_(B)
+            ent = cache[key] = _capture(fi, static_B, cache)
         g, static_B, static_X = ent
         static_B.copy_(B)
     g.replay()
     return static_X.clone()
-
-
-_PTR_GRAPH_MAX_R = 64
 
 
 def _capture(fi, static_B, cache):
