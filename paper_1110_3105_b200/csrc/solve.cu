@@ -270,16 +270,20 @@ __global__ void __launch_bounds__(256) k_level_dmma_few(
   double* sX = reinterpret_cast<double*>(smem);
   const int64_t* xr = (ROWS && xrows) ? xrows + x_off[a] : nullptr;
   const int64_t* orw = (ROWS && orows) ? orows + o_off[a] : nullptr;
-  for (int e = tid; e < Kp * CW; e += nt) {
-    const int j = e / CW, c = e - j * CW;
+  // stage in 16-byte pieces (column pairs; rows are 16-byte aligned for even R)
+  constexpr int CP = CW / 2;
+  for (int e = tid; e < Kp * CP; e += nt) {
+    const int j = e / CP, c = 2 * (e - j * CP);
     double* d = sX + j * LDX + c;
     const double* src = nullptr;
-    if (c < R) {
-      if (j < q) src = (xr ? X + xr[j] * R : X + (x_off[a] + j) * R) + c;
-      else if (j >= Qp && j - Qp < r) src = Y + (y_off[a] + (j - Qp)) * R + c;
+    if (j < q) src = (xr ? X + xr[j] * R : X + (x_off[a] + j) * R) + c;
+    else if (j >= Qp && j - Qp < r) src = Y + (y_off[a] + (j - Qp)) * R + c;
+    if (src && c + 1 < R && !(reinterpret_cast<uintptr_t>(src) & 15)) {
+      cp_async16(d, src);
+    } else {
+      d[0] = (src && c < R) ? __ldg(src) : 0.0;
+      d[1] = (src && c + 1 < R) ? __ldg(src + 1) : 0.0;
     }
-    if (src) cp_async8(d, src);
-    else *d = 0.0;
   }
   cp_async_commit();
   cp_async_wait<0>();
