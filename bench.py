@@ -57,6 +57,9 @@ def dist_env():
     return ws, rank, local
 
 
+SOLVES_PER_STEP = 10     # 16-RHS solves per timed solve step (mean reported)
+
+
 def _ncu_traffic(name):
     """dram__bytes_read.sum + dram__bytes_write.sum of the committed
     `ncu --set full` capture of the dominant kernel (profiles/<name>, written
@@ -304,11 +307,12 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)
         e1.record()
-        X = sk.solve_device(fi, B_dev)
+        for _ in range(SOLVES_PER_STEP):     # back to back: factor data (1.9 GB) >> L2
+            X = sk.solve_device(fi, B_dev)
         e2.record()
         torch.cuda.synchronize()
         barrier()
-        sts.append(e1.elapsed_time(e2) * 1e-3)
+        sts.append(e1.elapsed_time(e2) * 1e-3 / SOLVES_PER_STEP)
     clk = clocks.stop()
     factor_s = max_over_ranks(statistics.mean(fts))
     solve_s = max_over_ranks(statistics.mean(sts))
@@ -463,6 +467,7 @@ def run_ours(args):
                        "levels": cm.nlevels, "S": list(cm.S_shape()),
                        "factor_bytes_per_point": fi.factor_bytes() / n},
             "solve": {"R": R, "nrhs_per_s": n * R / solve_s, "ms": solve_s * 1e3,
+                      "solves_per_step": SOLVES_PER_STEP,
                       "ms_steps": [round(t * 1e3, 4) for t in sts]},
             "solve_1024": big,
             "roofline": roofline,
