@@ -8,6 +8,9 @@ import torch
 import paper_1110_3105_b200 as sk
 from paper_1110_3105_b200 import _profile
 
+LEVELS_SHOWN = tuple(int(x) for x in __import__("os").environ.get("PERF_LEVELS", "0,1,2").split(","))
+
+
 def run(n, eps, R, reps=4, detail=True):
     curve = sk.bie.ellipse(2.0, 1.0, n)
     system = sk.bie.discretize_dirichlet(curve, sk.KernelSpec("laplace", 2))
@@ -48,7 +51,7 @@ def run(n, eps, R, reps=4, detail=True):
             print(f"  level {li:2d}: span {r.ms():7.3f} ms  id-kernels(sum) {kms:7.3f} ms  launches {len(ks)} "
                   f"boxes {sum(x.meta['sel'].size for x in ks)}  GF/s {sum(x.flops for x in ks)/max(kms,1e-9)/1e6:8.1f}")
         for x in idl:
-            if x.meta["level"] in (0, 1, 2):
+            if x.meta["level"] in LEVELS_SHOWN:
                 print(f"     L{x.meta['level']} bucket boxes {x.meta['sel'].size:6d} max_m {x.meta['max_m']:4d} "
                       f"max_n {x.meta['max_n']:3d} max_w {x.meta['max_w']:6d}  {x.ms():8.3f} ms")
         fl = [r for r in _profile.records if r.kind == "factor_level"]
