@@ -465,6 +465,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": factor_s, "unit": "s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * (factor_s + solve_s),
+            "value_steps": [round(t, 5) for t in fts],
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (analytic ellipse nodes, seeded N(0,1) RHS)",
             "config": {"workload": CONFIG_NAME, "n": n, "eps": eps, "nrhs": R,
