@@ -180,6 +180,7 @@ struct Tree {
   std::vector<std::vector<int64_t>> covers;             // finest first
   std::vector<std::vector<int64_t>> nbr_off, nbr_idx;   // per cover
   bool nbr_done = false;
+  bool nonfinite = false;      // build() saw a NaN / inf coordinate
 };
 
 // Item of the serial top part: a node, or a subtree task spliced in later.
@@ -209,17 +210,27 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
     for (auto& x : th) x.join();
   };
   // bounding box (per-thread extrema, then reduced)
+  // (and the finiteness check of geom.py:133, in the same pass)
   std::vector<std::array<double, 6>> ext_t(nthreads);
+  std::vector<char> bad_t(nthreads, 0);
   parallel([&](int t, int64_t a0, int64_t a1) {
     std::array<double, 6> e = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    bool bad = false;
     for (int64_t i = a0; i < a1; ++i)
       for (int a = 0; a < d; ++a) {
         const double v = X[i * d + a];
+        bad |= !std::isfinite(v);
         e[a] = std::min(e[a], v);
         e[3 + a] = std::max(e[3 + a], v);
       }
     ext_t[t] = e;
+    bad_t[t] = bad;
   });
+  for (int t = 0; t < nthreads; ++t)
+    if (bad_t[t]) {
+      T.nonfinite = true;
+      return;
+    }
   double lo_c[3] = {INFINITY, INFINITY, INFINITY}, hi_c[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int t = 0; t < nthreads; ++t)
     for (int a = 0; a < d; ++a) {
@@ -570,6 +581,10 @@ int skel_tree_build(const double* coords, int64_t n, int32_t dim, int64_t max_le
   if (!coords || n < 1 || (dim != 2 && dim != 3) || max_leaf < 1 || !handle) return -1;
   Tree* T = new Tree();
   build(*T, coords, n, dim, max_leaf);
+  if (T->nonfinite) {
+    delete T;
+    return -3;   // non-finite coordinate
+  }
   *handle = T;
   return 0;
 }

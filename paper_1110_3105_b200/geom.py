@@ -191,12 +191,12 @@ def build_tree(points: PointSet, max_leaf_size: int | None = None) -> OrthTree:
     if max_leaf_size < 1:
         raise InvalidInput("max_leaf_size must be >= 1")
     coords = np.ascontiguousarray(points.coords, dtype=np.float64)
-    if not np.isfinite(coords).all():
-        raise InvalidInput("non-finite coordinate")
     h = ctypes.c_void_p()
-    _native.check(_native.lib().skel_tree_build(coords.ctypes.data_as(ctypes.c_void_p),
-                                                points.n, d, int(max_leaf_size),
-                                                ctypes.byref(h)), "skel_tree_build")
+    rc = _native.lib().skel_tree_build(coords.ctypes.data_as(ctypes.c_void_p), points.n, d,
+                                       int(max_leaf_size), ctypes.byref(h))
+    if rc == -3:        # checked in the native bounding-box pass (geom.py:133)
+        raise InvalidInput("non-finite coordinate")
+    _native.check(rc, "skel_tree_build")
     return OrthTree(h.value, d, points.n)
 
 
