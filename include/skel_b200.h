@@ -390,6 +390,9 @@ int skel_tree_cover(void* handle, int32_t li, int64_t* count, int64_t* ids);
 int skel_tree_neighbors(void* handle, int32_t li, int64_t* off, int64_t* count,
                         int64_t* idx);
 int skel_tree_free(void* handle);
+/* mean(w[perm]) with numpy's float64 pairwise summation order (bit-identical
+ * to np.mean(w[perm])): the proxy weight scale of _BieSource (bie.py:251). */
+int skel_perm_mean(const double* w, const int64_t* perm, int64_t n, double* out);
 
 /* FP64 throughput probe: kind 0 = DFMA chains, 1 = DMMA (mma.sync m8n8k4
  * f64).  *flops receives the launch's flop count; time it with events. */

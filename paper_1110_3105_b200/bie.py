@@ -173,6 +173,19 @@ def discretize_dirichlet(curve: Curve2D, spec: KernelSpec, quad: str | None = No
     return BieSystem(spec, curve, quad)
 
 
+def perm_mean(w, perm):
+    """np.mean(w[perm]) bit for bit (numpy's pairwise order), without the
+    gathered copy: native, threaded over the top of the summation tree."""
+    import ctypes
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    perm = np.ascontiguousarray(perm, dtype=np.int64)
+    out = ctypes.c_double()
+    _native.check(_native.lib().skel_perm_mean(w.ctypes.data_as(ctypes.c_void_p),
+                                                perm.ctypes.data_as(ctypes.c_void_p), perm.size,
+                                                ctypes.byref(out)), "skel_perm_mean")
+    return float(out.value)
+
+
 class BieSource(_DeviceSourceMixin):
     """A BieSystem in tree order (bie.py:233-262): row proxies scaled by the
     mean quadrature weight, column proxies weighted."""
@@ -184,7 +197,7 @@ class BieSource(_DeviceSourceMixin):
         self.dtype = system.dtype
         self.wavenumber = system.spec.wavenumber
         self.geo = system.geometry(self.perm)
-        self.wscale = float(np.mean(system.curve.weights[self.perm]))
+        self.wscale = perm_mean(system.curve.weights, self.perm)
 
     def _desc(self):
         return self.system.descriptor(self.geo, self.wscale)

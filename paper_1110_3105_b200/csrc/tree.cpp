@@ -573,6 +573,44 @@ void all_neighbors(Tree& T) {
   T.nbr_done = true;
 }
 
+
+// numpy's pairwise summation of float64 (the add.reduce inner loop of a
+// contiguous array: < 8 elements sequentially, <= 128 with 8 accumulators
+// combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus the tail, otherwise
+// split at n/2 rounded down to a multiple of 8), over w[perm[0..n)]
+static double pw_sum(const double* w, const int64_t* perm, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r += w[perm[i]];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = w[perm[j]];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += w[perm[i + j]];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += w[perm[i]];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return pw_sum(w, perm, n2) + pw_sum(w + 0, perm + n2, n - n2);
+}
+
+// the same sum with the top `depth` recursion levels run on threads
+static double pw_sum_par(const double* w, const int64_t* perm, int64_t n, int depth) {
+  if (depth == 0 || n <= 128 * 64) return pw_sum(w, perm, n);
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  double a = 0.0;
+  std::thread th([&]() { a = pw_sum_par(w, perm, n2, depth - 1); });
+  const double b = pw_sum_par(w, perm + n2, n - n2, depth - 1);
+  th.join();
+  return a + b;
+}
+
 }  // namespace
 
 extern "C" {
@@ -628,6 +666,12 @@ int skel_tree_neighbors(void* handle, int32_t li, int64_t* off, int64_t* count, 
   *count = (int64_t)T->nbr_idx[li].size();
   if (off) std::memcpy(off, T->nbr_off[li].data(), T->nbr_off[li].size() * sizeof(int64_t));
   if (idx) std::memcpy(idx, T->nbr_idx[li].data(), T->nbr_idx[li].size() * sizeof(int64_t));
+  return 0;
+}
+
+int skel_perm_mean(const double* w, const int64_t* perm, int64_t n, double* out) {
+  if (!w || !perm || !out || n < 1) return -1;
+  *out = pw_sum_par(w, perm, n, 4) / (double)n;
   return 0;
 }
 

@@ -129,3 +129,14 @@ def test_level_planner_matches_numpy():
     scls = np.searchsorted(np.asarray((24, 40, 56, 72, 96, 128)), nr)
     for a, b in zip(size_buckets(np.where(nr > 0, scls, -1)), fp.sbuckets):
         np.testing.assert_array_equal(a, b)
+
+
+def test_perm_mean_matches_numpy_bitwise():
+    """The native mean(w[perm]) (proxy weight scale, bie.py:251) reproduces
+    numpy's pairwise summation order bit for bit, with no gathered copy."""
+    from paper_1110_3105_b200.bie import perm_mean
+    rng = np.random.default_rng(11)
+    for n in list(range(1, 260)) + [1023, 4096, 4097, 65543, 2 ** 20 + 5]:
+        w = rng.standard_normal(n) * rng.uniform(0.1, 10.0) + 2.0
+        perm = rng.permutation(n)
+        assert perm_mean(w, perm) == float(np.mean(w[perm])), n
