@@ -27,6 +27,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
 #include <thread>
 #include <utility>
 #include <vector>
@@ -34,6 +36,81 @@
 #include "../../include/skel_b200.h"
 
 namespace {
+
+// Persistent worker pool: the tree build and the neighbour scan run several
+// short parallel passes per call, and spawning 16 std::threads per pass cost
+// more than some passes.  run(n, f) executes f(0..n-1) on the caller and the
+// workers; nested calls (from a worker) run serially.  Every worker takes
+// part in every generation, so no worker can touch a finished job.
+class Pool {
+ public:
+  explicit Pool(int n) {
+    for (int i = 0; i < n - 1; ++i) th_.emplace_back([this] { loop(); });
+  }
+  int size() const { return (int)th_.size() + 1; }
+  void run(int n, const std::function<void(int)>& f) {
+    if (in_worker() || th_.empty() || n <= 1) {
+      for (int t = 0; t < n; ++t) f(t);
+      return;
+    }
+    std::lock_guard<std::mutex> rl(run_m_);
+    {
+      std::lock_guard<std::mutex> l(m_);
+      job_ = &f;
+      njobs_ = n;
+      next_ = 0;
+      finished_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    in_worker() = true;          // a nested run() from the caller's share is serial
+    for (int t; (t = next_.fetch_add(1)) < n;) f(t);
+    in_worker() = false;
+    std::unique_lock<std::mutex> l(m_);
+    done_.wait(l, [&] { return finished_ == (int)th_.size(); });
+  }
+
+ private:
+  static bool& in_worker() {
+    thread_local bool w = false;
+    return w;
+  }
+  void loop() {
+    in_worker() = true;
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* j;
+      int nj;
+      {
+        std::unique_lock<std::mutex> l(m_);
+        cv_.wait(l, [&] { return gen_ != seen; });
+        seen = gen_;
+        j = job_;
+        nj = njobs_;
+      }
+      for (int t; (t = next_.fetch_add(1)) < nj;) (*j)(t);
+      std::lock_guard<std::mutex> l(m_);
+      if (++finished_ == (int)th_.size()) done_.notify_all();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_, run_m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int njobs_ = 0, finished_ = 0;
+  std::atomic<int> next_{0};
+  uint64_t gen_ = 0;
+};
+
+// one pool per process, never destroyed (its threads die with the process)
+static Pool& pool() {
+  static Pool* p = [] {
+    unsigned hwc = std::thread::hardware_concurrency();
+    return new Pool((int)std::max(1u, std::min(hwc == 0 ? 1u : hwc, 32u)));
+  }();
+  return *p;
+}
+
 
 constexpr double kRootPad = 1e-12;
 constexpr int kMaxDepth = 60;
@@ -74,11 +151,7 @@ struct Builder {
         c[k]++;
       }
     };
-    {
-      std::vector<std::thread> th;
-      for (int t = 0; t < T; ++t) th.emplace_back(count, t);
-      for (auto& x : th) x.join();
-    }
+    pool().run(T, count);
     std::vector<std::array<int64_t, 8>> st(T);
     int64_t s = lo;
     for (int k = 0; k < nk; ++k) {
@@ -100,22 +173,14 @@ struct Builder {
         for (int a = 0; a < d; ++a) (*tmpx[a])[dst] = px[a][i];
       }
     };
-    {
-      std::vector<std::thread> th;
-      for (int t = 0; t < T; ++t) th.emplace_back(scatter, t);
-      for (auto& x : th) x.join();
-    }
+    pool().run(T, scatter);
     auto copyback = [&](int t) {
       const int64_t a0 = lo + t * chunk, a1 = std::min(hi, a0 + chunk);
       if (a1 <= a0) return;
       std::memcpy(P + a0, TI + a0, (a1 - a0) * sizeof(int64_t));
       for (int a = 0; a < d; ++a) std::memcpy(px[a] + a0, tmpx[a]->data() + a0, (a1 - a0) * sizeof(double));
     };
-    {
-      std::vector<std::thread> th;
-      for (int t = 0; t < T; ++t) th.emplace_back(copyback, t);
-      for (auto& x : th) x.join();
-    }
+    pool().run(T, copyback);
   }
 
   // split [lo, hi) of node `cen/hw` into children ranges; returns counts
@@ -204,10 +269,9 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
   const int nthreads = (int)std::max(1u, std::min(hwc == 0 ? 1u : hwc, 32u));
   auto parallel = [&](auto fn) {        // fn(t, a0, a1) over point chunks
     const int64_t chunk = (n + nthreads - 1) / nthreads;
-    std::vector<std::thread> th;
-    for (int t = 0; t < nthreads; ++t)
-      th.emplace_back([&, t]() { fn(t, t * chunk, std::min(n, (int64_t)(t + 1) * chunk)); });
-    for (auto& x : th) x.join();
+    pool().run(nthreads, [&](int t) {
+      fn(t, std::min(n, (int64_t)t * chunk), std::min(n, (int64_t)(t + 1) * chunk));
+    });
   };
   // bounding box (per-thread extrema, then reduced)
   // (and the finiteness check of geom.py:133, in the same pass)
@@ -421,19 +485,10 @@ void build(Tree& T, const double* X, int64_t n, int d, int64_t max_leaf) {
     if (items[i].task) task_ids.push_back(i);
   std::vector<std::vector<NodeRec>> sub(task_ids.size());
   {
-    std::vector<std::thread> pool;
-    std::atomic_int next(0);
-    auto worker = [&]() {
-      for (;;) {
-        int t = next.fetch_add(1);
-        if (t >= (int)task_ids.size()) break;
-        const NodeRec& r = items[task_ids[t]].rec;
-        B.build_sub(sub[t], r.lo, r.hi, r.c, r.hw, r.depth, -1);
-      }
-    };
-    int nt = std::min<int>(nthreads, (int)task_ids.size());
-    for (int i = 0; i < nt; ++i) pool.emplace_back(worker);
-    for (auto& th : pool) th.join();
+    pool().run((int)task_ids.size(), [&](int t) {
+      const NodeRec& r = items[task_ids[t]].rec;
+      B.build_sub(sub[t], r.lo, r.hi, r.c, r.hw, r.depth, -1);
+    });
   }
   double t2 = now_ms();
   // splice in preorder
@@ -555,12 +610,10 @@ void all_neighbors(Tree& T) {
       // parallel, concatenated in box order (identical to the serial lists)
       const int64_t chunk = (p + nt - 1) / nt;
       std::vector<std::vector<int64_t>> part(nt);
-      std::vector<std::thread> th;
-      for (int t = 0; t < nt; ++t) {
+      pool().run(nt, [&](int t) {
         const int64_t a0 = std::min(p, t * chunk), a1 = std::min(p, (t + 1) * chunk);
-        th.emplace_back([&, t, a0, a1]() { scan(a0, a1, part[t], cnt.data() + a0); });
-      }
-      for (auto& x : th) x.join();
+        scan(a0, a1, part[t], cnt.data() + a0);
+      });
       size_t tot = 0;
       for (auto& v : part) tot += v.size();
       idx.reserve(tot);

@@ -38,6 +38,23 @@ def test_native_tree_equals_oracle(n, dim):
             np.testing.assert_array_equal(T.cover_children(li), oracle.cover_children(O, li))
 
 
+@pytest.mark.parametrize("n,dim", [(2 ** 20, 2), (300000, 3)])
+def test_native_tree_equals_oracle_large(n, dim):
+    """Sizes where the native build runs its parallel split passes (ranges of
+    >= 2^17 points) on the persistent worker pool: perm, nodes and covers
+    identical to the oracle."""
+    import paper_1110_3105_b200 as sk
+    X = oracle.ellipse(2.0, 1.0, n)["xy"] if dim == 2 else oracle.fib_sphere(n)
+    T = sk.build_tree(sk.PointSet(X), 64)
+    O = oracle.build_tree(X, 64)
+    np.testing.assert_array_equal(T.perm, O.perm)
+    np.testing.assert_array_equal(T.center, O.center)
+    np.testing.assert_array_equal(T.hw, O.hw)
+    assert len(T.levels) == len(O.covers)
+    for li in range(len(T.levels)):
+        np.testing.assert_array_equal(T.levels[li], O.covers[li])
+
+
 def test_native_tree_matches_golden(golden):
     import paper_1110_3105_b200 as sk
     g = golden("sphere_2000_1e-6")
