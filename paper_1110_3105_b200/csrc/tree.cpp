@@ -652,18 +652,38 @@ static double pw_sum(const double* w, const int64_t* perm, int64_t n) {
   return pw_sum(w, perm, n2) + pw_sum(w + 0, perm + n2, n - n2);
 }
 
-// the same sum with the top `depth` recursion levels run on threads
-static double pw_sum_par(const double* w, const int64_t* perm, int64_t n, int depth) {
-  if (depth == 0 || n <= 128 * 64) return pw_sum(w, perm, n);
+// the same sum with the top recursion levels' subtrees summed on the pool:
+// leaves (in order) are ranges the recursion reaches at `depth` or at
+// <= 8192 elements; combining them back along the same splits keeps
+// numpy's association exactly
+static void pw_leaves(int64_t a, int64_t n, int depth, std::vector<std::pair<int64_t, int64_t>>& out) {
+  if (depth == 0 || n <= 8192) {
+    out.push_back({a, n});
+    return;
+  }
   int64_t n2 = n / 2;
   n2 -= n2 % 8;
-  double a = 0.0;
-  std::thread th([&]() { a = pw_sum_par(w, perm, n2, depth - 1); });
-  const double b = pw_sum_par(w, perm + n2, n - n2, depth - 1);
-  th.join();
-  return a + b;
+  pw_leaves(a, n2, depth - 1, out);
+  pw_leaves(a + n2, n - n2, depth - 1, out);
 }
-
+static double pw_combine(int64_t n, int depth, const double* sums, size_t& k) {
+  if (depth == 0 || n <= 8192) return sums[k++];
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  const double x = pw_combine(n2, depth - 1, sums, k);
+  const double y = pw_combine(n - n2, depth - 1, sums, k);
+  return x + y;
+}
+static double pw_sum_par(const double* w, const int64_t* perm, int64_t n, int depth) {
+  std::vector<std::pair<int64_t, int64_t>> leaves;
+  pw_leaves(0, n, depth, leaves);
+  std::vector<double> sums(leaves.size());
+  pool().run((int)leaves.size(), [&](int t) {
+    sums[t] = pw_sum(w, perm + leaves[t].first, leaves[t].second);
+  });
+  size_t k = 0;
+  return pw_combine(n, depth, sums.data(), k);
+}
 }  // namespace
 
 extern "C" {
