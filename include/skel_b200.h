@@ -390,6 +390,10 @@ int skel_tree_cover(void* handle, int32_t li, int64_t* count, int64_t* ids);
 int skel_tree_neighbors(void* handle, int32_t li, int64_t* off, int64_t* count,
                         int64_t* idx);
 int skel_tree_free(void* handle);
+/* PointSet validation (geom.py:42 and the unit-normal rule): 0 ok, -3 a
+ * non-finite coordinate, -4 a normal with | |n| - 1 | > 1e-12 (normals may be
+ * NULL); |n| is formed as np.linalg.norm(axis=1) does. */
+int skel_check_points(const double* coords, const double* normals, int64_t n, int32_t dim);
 /* mean(w[perm]) with numpy's float64 pairwise summation order (bit-identical
  * to np.mean(w[perm])): the proxy weight scale of _BieSource (bie.py:251). */
 int skel_perm_mean(const double* w, const int64_t* perm, int64_t n, double* out);

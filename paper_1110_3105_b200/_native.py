@@ -93,6 +93,7 @@ _SIGS = {
     "skel_dense_matvec": [_P(SkelSource), c_vp, c_vp, c_i32, c_i32, c_vp],
     "skel_tree_build": [c_vp, c_i64, c_i32, c_i64, _P(c_vp)],
     "skel_perm_mean": [c_vp, c_vp, c_i64, _P(c_f64)],
+    "skel_check_points": [c_vp, c_vp, c_i64, c_i32],
     "skel_tree_sizes": [c_vp, _P(c_i64), _P(c_i32)],
     "skel_tree_nodes": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "skel_tree_cover": [c_vp, c_i32, _P(c_i64), c_vp],

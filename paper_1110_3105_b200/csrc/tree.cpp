@@ -742,6 +742,34 @@ int skel_tree_neighbors(void* handle, int32_t li, int64_t* off, int64_t* count, 
   return 0;
 }
 
+int skel_check_points(const double* coords, const double* normals, int64_t n, int32_t dim) {
+  if (!coords || n < 1 || (dim != 2 && dim != 3)) return -1;
+  const int T = pool().size();
+  const int64_t chunk = (n + T - 1) / T;
+  std::vector<char> bad_c(T, 0), bad_n(T, 0);
+  pool().run(T, [&](int t) {
+    const int64_t a0 = std::min(n, (int64_t)t * chunk), a1 = std::min(n, (int64_t)(t + 1) * chunk);
+    bool bc = false, bn = false;
+    for (int64_t i = a0; i < a1; ++i) {
+      for (int a = 0; a < dim; ++a) bc |= !std::isfinite(coords[i * dim + a]);
+      if (normals) {
+        // |n| as np.linalg.norm(axis=1): squares, summed left to right, sqrt
+        const double* v = normals + i * dim;
+        double s = v[0] * v[0];
+        for (int a = 1; a < dim; ++a) s = s + v[a] * v[a];
+        bn |= std::fabs(std::sqrt(s) - 1.0) > 1e-12;   // NaN compares false, as in numpy
+      }
+    }
+    bad_c[t] = bc;
+    bad_n[t] = bn;
+  });
+  for (int t = 0; t < T; ++t)
+    if (bad_c[t]) return -3;
+  for (int t = 0; t < T; ++t)
+    if (bad_n[t]) return -4;
+  return 0;
+}
+
 int skel_perm_mean(const double* w, const int64_t* perm, int64_t n, double* out) {
   if (!w || !perm || !out || n < 1) return -1;
   *out = pw_sum_par(w, perm, n, 4) / (double)n;

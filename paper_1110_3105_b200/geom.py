@@ -34,15 +34,23 @@ class PointSet:
             raise InvalidInput(f"coords must be (N, d) with d in {{2,3}}, got {c.shape}")
         if c.shape[0] < 1:
             raise InvalidInput("need at least one point")
-        if not np.isfinite(c).all():
-            raise InvalidInput("non-finite coordinate")
-        self.coords = c
+        nrm = None
         if self.normals is not None:
             nrm = np.ascontiguousarray(self.normals, dtype=np.float64)
+        # finiteness, then (shape and) unit normals, in the reference's order;
+        # the two numeric checks are one threaded native pass
+        rc = _native.lib().skel_check_points(
+            c.ctypes.data_as(ctypes.c_void_p),
+            nrm.ctypes.data_as(ctypes.c_void_p) if nrm is not None and nrm.shape == c.shape else None,
+            c.shape[0], c.shape[1])
+        if rc == -3:
+            raise InvalidInput("non-finite coordinate")
+        _native.check(rc if rc != -4 else 0, "skel_check_points")
+        self.coords = c
+        if nrm is not None:
             if nrm.shape != c.shape:
                 raise InvalidInput("normals must match coords shape")
-            # |n| per row (same sum of squares and sqrt as np.linalg.norm(axis=1))
-            if np.any(np.abs(np.sqrt(np.einsum("ij,ij->i", nrm, nrm)) - 1.0) > 1e-12):
+            if rc == -4:
                 raise InvalidInput("normals must be unit vectors (|n| = 1 within 1e-12)")
             self.normals = nrm
         for name in ("weights", "curvatures"):

@@ -157,3 +157,30 @@ def test_perm_mean_matches_numpy_bitwise():
         w = rng.standard_normal(n) * rng.uniform(0.1, 10.0) + 2.0
         perm = rng.permutation(n)
         assert perm_mean(w, perm) == float(np.mean(w[perm])), n
+
+
+def test_native_point_checks_match_numpy_rules():
+    """PointSet's native finiteness / unit-normal pass decides exactly as the
+    reference's numpy expressions (geom.py:42-49), including NaN normals
+    (which compare false there) and rows at the 1e-12 threshold."""
+    import ctypes
+    from paper_1110_3105_b200 import _native
+    L = _native.lib()
+    rng = np.random.default_rng(2)
+    for d in (2, 3):
+        for trial in range(60):
+            n = 500
+            v = rng.standard_normal((n, d))
+            v /= np.linalg.norm(v, axis=1, keepdims=True)
+            k = rng.integers(0, n, 3)
+            v[k] *= 1 + rng.uniform(-2e-12, 2e-12, (3, 1))
+            if trial % 7 == 0:
+                v[k[0], 0] = np.nan
+            ref = bool(np.any(np.abs(np.linalg.norm(v, axis=1) - 1.0) > 1e-12))
+            c = rng.standard_normal((n, d))
+            if trial % 11 == 0:
+                c[k[1], d - 1] = np.inf
+            rc = L.skel_check_points(c.ctypes.data_as(ctypes.c_void_p),
+                                     v.ctypes.data_as(ctypes.c_void_p), n, d)
+            want = -3 if not np.isfinite(c).all() else (-4 if ref else 0)
+            assert rc == want, (d, trial, rc, want)
