@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(128) k_level_dmma(
 // zero pad to Qp = q rounded up to 4, rows [Qp, Qp + r) = Y, pad to 4;
 // row stride 8 * NT + 8 doubles so a B-fragment load touches each bank pair
 // exactly twice (the 2-wavefront minimum for 32 doubles).
-template <int NT, bool ROWS>
+template <int NT, bool ROWS, bool CPLX = false>
 __global__ void __launch_bounds__(256) k_level_dmma_few(
     const int32_t* __restrict__ pp, const int32_t* __restrict__ qq, const int32_t* __restrict__ rr,
     const int64_t* __restrict__ a_off, const double* __restrict__ A,
@@ -260,10 +260,16 @@ __global__ void __launch_bounds__(256) k_level_dmma_few(
     const int64_t* __restrict__ o_off, double* __restrict__ O, int R,
     const int32_t* __restrict__ order, const int64_t* __restrict__ xrows,
     const int64_t* __restrict__ orows) {
+  // CPLX: complex128 blocks and vectors (interleaved re, im) as the real GEMM
+  // [Re | Im] (p x 2q) x X' (2q x 2R), X' rows 2k = (re, im) pairs of X row k
+  // and 2k+1 = (-im, re): column pair (2c, 2c+1) of the result is (Re, Im)
+  // of A X, already interleaved.  R, offsets and row maps stay in complex
+  // units; below every extent is in doubles.
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int CW = 8 * NT, LDX = CW + 8;
+  constexpr int CW = 8 * NT, LDX = CW + 8, CF = CPLX ? 2 : 1;
   const int a = order ? order[blockIdx.x] : blockIdx.x;
-  const int p = pp[a], q = qq[a], r = rr ? rr[a] : 0;
+  const int p = pp[a], q = CF * qq[a], r = rr ? CF * rr[a] : 0;
+  R *= CF;
   if (p == 0) return;
   const int Qp = (q + 3) & ~3, Rp = (r + 3) & ~3, Kp = Qp + Rp;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
@@ -276,9 +282,20 @@ __global__ void __launch_bounds__(256) k_level_dmma_few(
     const int j = e / CP, c = 2 * (e - j * CP);
     double* d = sX + j * LDX + c;
     const double* src = nullptr;
-    if (j < q) src = (xr ? X + xr[j] * R : X + (x_off[a] + j) * R) + c;
-    else if (j >= Qp && j - Qp < r) src = Y + (y_off[a] + (j - Qp)) * R + c;
-    if (src && c + 1 < R && !(reinterpret_cast<uintptr_t>(src) & 15)) {
+    int par = 0;
+    if (j < q) {
+      const int kx = j / CF;
+      par = j - kx * CF;
+      src = (xr ? X + xr[kx] * R : X + (x_off[a] + kx) * R) + c;
+    } else if (j >= Qp && j - Qp < r) {
+      const int ky = (j - Qp) / CF;
+      par = (j - Qp) - ky * CF;
+      src = Y + (y_off[a] + ky) * R + c;
+    }
+    if (CPLX && par) {               // (-im, re) of complex element c / 2
+      d[0] = (src && c < R) ? -__ldg(src + 1) : 0.0;
+      d[1] = (src && c < R) ? __ldg(src) : 0.0;
+    } else if (src && c + 1 < R && !(reinterpret_cast<uintptr_t>(src) & 15)) {
       cp_async16(d, src);
     } else {
       d[0] = (src && c < R) ? __ldg(src) : 0.0;
@@ -296,7 +313,7 @@ __global__ void __launch_bounds__(256) k_level_dmma_few(
     double acc[NT][2];
 #pragma unroll
     for (int u = 0; u < NT; ++u) acc[u][0] = acc[u][1] = 0.0;
-    const double* arow = A + a_off[a] + (int64_t)(ok ? row : 0) * q;
+    const double* arow = A + CF * a_off[a] + (int64_t)(ok ? row : 0) * q;
     const double* xs = sX + t4 * LDX + g;
 #pragma unroll 4
     for (int k0 = 0; k0 < Qp; k0 += 4) {
@@ -305,7 +322,7 @@ __global__ void __launch_bounds__(256) k_level_dmma_few(
       for (int u = 0; u < NT; ++u) dmma884(acc[u][0], acc[u][1], av, xs[k0 * LDX + u * 8]);
     }
     if (r) {
-      const double* brow = Bm + b_off[a] + (int64_t)(ok ? row : 0) * r;
+      const double* brow = Bm + CF * b_off[a] + (int64_t)(ok ? row : 0) * r;
       const double* ys = xs + Qp * LDX;
 #pragma unroll 4
       for (int k0 = 0; k0 < Rp; k0 += 4) {
@@ -525,6 +542,27 @@ static int level_gemm(int nbox, const int32_t* p, const int32_t* q, const int32_
     }
     return skel_last_error();
   };
+  if constexpr (sizeof(T) != sizeof(double)) {
+    // complex, few RHS: the real-ified DMMA kernel (2R real columns)
+    if (R >= 1 && R <= 8 && dmma_few_enabled()) {
+      const int nt = 2 * R <= 8 ? 1 : 2;
+      const int kmax = ((2 * max_q + 3) & ~3) + ((2 * max_r + 3) & ~3);
+      const size_t smem = (size_t)kmax * (8 * nt + 8) * sizeof(double);
+      const int threads = 32 * std::min(8, std::max(1, (max_p + 7) / 8));
+      if (smem <= optin) {
+        const bool rows = xrows || orows;
+        auto launch = [&](auto kern) -> int {
+          SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          kern<<<nbox, threads, smem, st>>>(p, q, r, a_off, (const double*)A, b_off, (const double*)B,
+                                            x_off, (const double*)X, y_off, (const double*)Y, o_off,
+                                            (double*)O, R, order, xrows, orows);
+          return skel_last_error();
+        };
+        if (nt == 1) return rows ? launch(k_level_dmma_few<1, true, true>) : launch(k_level_dmma_few<1, false, true>);
+        return rows ? launch(k_level_dmma_few<2, true, true>) : launch(k_level_dmma_few<2, false, true>);
+      }
+    }
+  }
   if constexpr (sizeof(T) == sizeof(double)) {
     if (R >= 3 && R <= 32 && dmma_few_enabled()) {
       const int nt = R <= 8 ? 1 : (R <= 16 ? 2 : 4);
