@@ -564,7 +564,7 @@ static int level_gemm(int nbox, const int32_t* p, const int32_t* q, const int32_
     }
   }
   if constexpr (sizeof(T) == sizeof(double)) {
-    if (R >= 3 && R <= 32 && dmma_few_enabled()) {
+    if (R >= 1 && R <= 32 && dmma_few_enabled()) {
       const int nt = R <= 8 ? 1 : (R <= 16 ? 2 : 4);
       const int kmax = ((max_q + 3) & ~3) + ((max_r + 3) & ~3);
       const size_t smem = (size_t)kmax * (8 * nt + 8) * sizeof(double);
