@@ -245,6 +245,8 @@ struct Tree {
   std::vector<std::vector<int64_t>> covers;             // finest first
   std::vector<std::vector<int64_t>> nbr_off, nbr_idx;   // per cover
   bool nbr_done = false;
+  std::thread nbr_thread;      // neighbour lists computed in the background after build
+  std::mutex nbr_m;            // serialises the join of nbr_thread
   bool nonfinite = false;      // build() saw a NaN / inf coordinate
 };
 
@@ -696,6 +698,10 @@ int skel_tree_build(const double* coords, int64_t n, int32_t dim, int64_t max_le
     delete T;
     return -3;   // non-finite coordinate
   }
+  // the neighbour lists of every cover are needed right after (the finest
+  // level's first): start them now, overlapping the caller's node-array
+  // copies and source setup; readers join first
+  T->nbr_thread = std::thread([T]() { all_neighbors(*T); });
   *handle = T;
   return 0;
 }
@@ -735,6 +741,10 @@ int skel_tree_cover(void* handle, int32_t li, int64_t* count, int64_t* ids) {
 int skel_tree_neighbors(void* handle, int32_t li, int64_t* off, int64_t* count, int64_t* idx) {
   Tree* T = (Tree*)handle;
   if (!T || li < 0 || li >= (int32_t)T->covers.size()) return -1;
+  {
+    std::lock_guard<std::mutex> l(T->nbr_m);
+    if (T->nbr_thread.joinable()) T->nbr_thread.join();
+  }
   all_neighbors(*T);
   *count = (int64_t)T->nbr_idx[li].size();
   if (off) std::memcpy(off, T->nbr_off[li].data(), T->nbr_off[li].size() * sizeof(int64_t));
@@ -777,7 +787,9 @@ int skel_perm_mean(const double* w, const int64_t* perm, int64_t n, double* out)
 }
 
 int skel_tree_free(void* handle) {
-  delete (Tree*)handle;
+  Tree* T = (Tree*)handle;
+  if (T && T->nbr_thread.joinable()) T->nbr_thread.join();
+  delete T;
   return 0;
 }
 
