@@ -43,8 +43,6 @@ def parse():
     ap.add_argument("--eps", type=float, default=1e-12)
     ap.add_argument("--nrhs", type=int, default=16)
     ap.add_argument("--nrhs-big", type=int, default=1024)
-    ap.add_argument("--sample-n", type=int, default=16384,
-                    help="CPU oracle sample size (scaled linearly to --n)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-residual", action="store_true")
     return ap.parse_args()
@@ -131,23 +129,30 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle (test infrastructure: the cpu_baseline leg / --impl reference)
 
-def oracle_sample(n_s, eps, nrhs):
-    """Time the oracle's factor path (tree + compress + factor) and a
-    nrhs-solve on an n_s-point instance of the same workload."""
+def oracle_full(n, eps, nrhs, workers=None):
+    """The reference algorithm on the host cores at the FULL workload size:
+    oracle/ (numpy+scipy restatement of skelkit, pinned bit-exact to the live
+    reference) with the boxes of each level farmed out to a process pool
+    (oracle/parallel.py, the reference's _map_nodes structure).  Returns
+    (factor seconds = tree + compress + factor, solve seconds for nrhs RHS,
+    worker count, the factorization)."""
     import numpy as np
 
     import oracle
-    cur = oracle.ellipse(2.0, 1.0, n_s)
+    from oracle.parallel import ParallelRun
+    cur = oracle.ellipse(2.0, 1.0, n)
     t0 = time.perf_counter()
     T = oracle.build_tree(cur["xy"], 64)
     src = oracle.BieSource(cur, T.perm)
-    oc = oracle.compress(src, T, eps)
-    of = oracle.factor(oc)
+    with ParallelRun(src, T, eps, workers) as pr:
+        of = pr.compress_factor()
+        nw = pr.workers
     t1 = time.perf_counter()
-    B = np.random.default_rng(0).standard_normal((n_s, nrhs))
-    oracle.solve(of, B)
+    B = np.random.default_rng(0).standard_normal((n, nrhs))
     t2 = time.perf_counter()
-    return t1 - t0, t2 - t1
+    oracle.solve(of, B)
+    t3 = time.perf_counter()
+    return t1 - t0, t3 - t2, nw, of
 
 
 def host_cores():
@@ -157,41 +162,59 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+REF_MAX_STEPS = 3        # full-size CPU steps take ~20 s each on 16 cores
+
+
+def ref_description(nw):
+    return (f"oracle/ (numpy+scipy restatement of skelkit 0.1.0, pinned bit-exact to the live "
+            f"reference) at the FULL config-2 size, boxes of each level farmed to {nw} worker "
+            f"processes (oracle/parallel.py = the reference's _map_nodes pool with processes, one "
+            f"BLAS thread each); O(p) neighbour lists (the as-shipped O(p^2) scan would add "
+            f"~5900 s at 2^20, SURVEY F4); compressed D/L/R stay in the workers")
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     import warnings
     warnings.simplefilter("ignore")
-    scale = args.n / args.sample_n
-    for _ in range(args.warmup):
-        oracle_sample(args.sample_n, args.eps, args.nrhs)
+    # warm-up: page in numpy/scipy and fork the pool once, on a small instance
+    for _ in range(min(args.warmup, 1)):
+        oracle_full(1 << 16, args.eps, args.nrhs)
+    steps = max(1, min(args.steps, REF_MAX_STEPS))
     fts, sts = [], []
-    for _ in range(args.steps):
-        ft, stt = oracle_sample(args.sample_n, args.eps, args.nrhs)
+    nw = None
+    for _ in range(steps):
+        ft, stt, nw, _of = oracle_full(args.n, args.eps, args.nrhs)
+        del _of
         fts.append(ft)
         sts.append(stt)
-    ft = statistics.mean(fts) * scale
+    ft = statistics.mean(fts)
     st = statistics.mean(sts)
-    cores = host_cores()
-    sample = (f"oracle/ (numpy+scipy restatement of skelkit, bit-exact vs the reference) on "
-              f"N={args.sample_n}, eps={args.eps:g}: tree+compress+factor, scaled x{scale:g} to "
-              f"N={args.n} (O(N) algorithm); O(p) neighbour lists (the as-shipped O(p^2) scan "
-              f"would add ~5900 s at 2^20, SURVEY F4)")
     line = {
         "impl": "reference", "metric": METRIC, "value": ft, "unit": "s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * (statistics.mean(fts) + st),
+        "steps": steps, "warmup": min(args.warmup, 1), "steps_requested": args.steps,
+        "warmup_requested": args.warmup, "ms_per_step": 1e3 * (ft + st),
+        "value_steps": [round(t, 3) for t in fts],
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (analytic ellipse nodes, seeded N(0,1) RHS)",
-        "config": {"workload": CONFIG_NAME, "n": args.n, "eps": args.eps, "nrhs": args.nrhs,
-                   "sample_n": args.sample_n, "l2": "n/a (CPU)"},
-        "solve": {"nrhs_per_s": args.sample_n * args.nrhs / st, "R": args.nrhs,
-                  "note": f"measured at N={args.sample_n}"},
-        "cpu_baseline": {"value": ft, "unit": "s", "cores": cores, "kind": "port",
-                         "sample": sample},
+        "config": config_dict(args),
+        "solve": {"nrhs_per_s": args.n * args.nrhs / st, "R": args.nrhs, "ms": st * 1e3},
+        "cpu_baseline": {"value": ft, "unit": "s", "cores": nw, "kind": "port",
+                         "sample": ref_description(nw) + (
+                             f"; {steps} full-size steps (capped at {REF_MAX_STEPS}), warm-up on "
+                             f"N=2^16")},
         "e2e": {"value": ft, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def config_dict(args):
+    """Identical on both arms: the workload, not how it ran."""
+    return {"workload": CONFIG_NAME, "n": args.n, "eps": args.eps, "nrhs": args.nrhs,
+            "nrhs_big": args.nrhs_big,
+            "l2": "GPU: 512 MB buffer written between timed steps; factor data 1.9 GB > L2"}
 
 
 # ---------------------------------------------------------------------------
@@ -362,13 +385,20 @@ def run_ours(args):
                    "achieved": fflops / (fms * 1e-3) / 1e12 if fms else 0.0, "peak": fp64_pk,
                    "unit": "TFLOP/s"}
     roof_factor["frac"] = roof_factor["achieved"] / fp64_pk
-    # algorithmic bytes of one solve (factor blocks + vectors,
-    # summed over the sweep launches) over the graph-replayed solve time; the
-    # eager per-launch event sum is reported beside it
+    # algorithmic bytes of one solve, SURVEY 8(d) exactly: every factor block
+    # read once (sum_a 8(n^2 + 2nk) + 8 K_top^2 = fi.factor_bytes()) plus B
+    # read and X written once (16 N R), over the graph-replayed solve time.
+    # The per-level vector round trips the sweeps actually make (each level
+    # writes its u / w slab and the next reads it back) are reported beside
+    # it as modelled traffic, not counted as useful bytes.
+    alg_bytes = fi.factor_bytes() + 16.0 * n * len(cols)
     roof_solve = {"kernel": "k_level_dmma_few sweeps (R=%d), whole solve" % len(cols), "bound": "hbm",
-                  "achieved": sbytes / solve_s / 1e9 if solve_s else 0.0, "peak": hbm_pk,
+                  "achieved": alg_bytes / solve_s / 1e9 if solve_s else 0.0, "peak": hbm_pk,
                   "unit": "GB/s", "peak_source": hbm_src, "launches": sc,
-                  "bytes_per_solve": sbytes,
+                  "bytes_per_solve": alg_bytes,
+                  "bytes_rule": "SURVEY 8(d): factor blocks + 8 K_top^2 + 16 N R",
+                  "traffic_model_bytes": sbytes,
+                  "traffic_model_rule": "factor blocks + every level's vector slabs read/written",
                   "eager_launch_sum_gbs": sbytes / (sms * 1e-3) / 1e9 if sms else 0.0}
     roof_solve["frac"] = roof_solve["achieved"] / hbm_pk
 
@@ -453,13 +483,11 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        ft, st_ = oracle_sample(args.sample_n, args.eps, R)
-        scale = args.n / args.sample_n
-        cpu = {"value": ft * scale, "unit": "s", "cores": host_cores(), "kind": "port",
-               "sample": f"oracle/ (bit-exact restatement of skelkit) tree+compress+factor at "
-                         f"N={args.sample_n}, eps={args.eps:g}, scaled x{scale:g} to N={args.n}; "
-                         f"16-RHS solve {args.sample_n * R / st_:.3e} N*RHS/s at that N",
-               "solve_nrhs_per_s": args.sample_n * R / st_}
+        ft, st_, nw, _of = oracle_full(args.n, args.eps, R)
+        del _of
+        cpu = {"value": ft, "unit": "s", "cores": nw, "kind": "port",
+               "sample": ref_description(nw) + "; one full-size step",
+               "solve_nrhs_per_s": args.n * R / st_}
 
     if rank == 0:
         line = {
@@ -468,13 +496,12 @@ def run_ours(args):
             "value_steps": [round(t, 5) for t in fts],
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (analytic ellipse nodes, seeded N(0,1) RHS)",
-            "config": {"workload": CONFIG_NAME, "n": n, "eps": eps, "nrhs": R,
-                       "parallelism": ("single GPU" if ws == 1 else
-                                       f"subtree-sharded factor over {ws} ranks below split level "
-                                       f"{cm.shard.split}, replicated above; box-sharded solve"),
-                       "l2": "512 MB buffer written between timed steps; factor data 1.9 GB > L2",
-                       "levels": cm.nlevels, "S": list(cm.S_shape()),
-                       "factor_bytes_per_point": fi.factor_bytes() / n},
+            "config": config_dict(args),
+            "run": {"parallelism": ("single GPU" if ws == 1 else
+                                    f"subtree-sharded factor over {ws} ranks below split level "
+                                    f"{cm.shard.split}, replicated above; box-sharded solve"),
+                    "levels": cm.nlevels, "S": list(cm.S_shape()),
+                    "factor_bytes_per_point": fi.factor_bytes() / n},
             "solve": {"R": R, "nrhs_per_s": n * R / solve_s, "ms": solve_s * 1e3,
                       "solves_per_step": SOLVES_PER_STEP,
                       "ms_steps": [round(t * 1e3, 4) for t in sts]},

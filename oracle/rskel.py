@@ -99,6 +99,55 @@ def run_id(A, eps, seed, tag):
     return id_fixed(A, eps), False
 
 
+def _blk(src, r, c):
+    if r.size == 0 or c.size == 0:
+        return np.zeros((r.size, c.size), dtype=src.dtype)
+    return src.block(r, c)
+
+
+def compress_box(src, tree, li, a, nid, rd, cd, zero, ncols, nrows, eps, npx, radius_factor,
+                 mode, equalize, seed):
+    """build_node (skel.py:341-391) for box ``a`` of cover ``li`` (tree node
+    ``nid``): D with the children's diagonal blocks (``zero`` = their (kr, kc))
+    cleared, the proxy (or global) targets, both IDs, equalisation and the
+    sorted skeletons.  Returns (row_skel, col_skel, D, L, R, n_randomized)."""
+    dtype = src.dtype
+    dim = tree.dim
+    kw = float(getattr(src, "wavenumber", 0.0))
+    D = np.ascontiguousarray(_blk(src, rd, cd), dtype=dtype)
+    if zero:
+        r0 = c0 = 0
+        for kr_c, kc_c in zero:
+            D[r0:r0 + kr_c, c0:c0 + kc_c] = 0
+            r0 += kr_c
+            c0 += kc_c
+    if mode == "proxy":
+        r = proxy_radius(tree.hw[nid], dim, radius_factor)
+        neff = npx
+        if kw > 0:
+            neff += int(np.ceil(4.0 * kw * r))
+        pxy = tree.center[nid] + r * proxy_unit_points(neff, dim)
+        t_row = (np.hstack([_blk(src, rd, ncols), src.proxy_row_block(rd, pxy)])
+                 if rd.size else np.zeros((0, neff), dtype=dtype))
+        t_col = (np.vstack([_blk(src, nrows, cd), src.proxy_col_block(cd, pxy)])
+                 if cd.size else np.zeros((neff, 0), dtype=dtype))
+    else:
+        t_row = _blk(src, rd, ncols)
+        t_col = _blk(src, nrows, cd)
+    (sr, Pr, kr, _), rz1 = run_id(t_row.T, eps, seed, (li, a, 0))
+    (sc, Pc, kc, _), rz2 = run_id(t_col, eps, seed, (li, a, 1))
+    if equalize and kr != kc:
+        k = max(kr, kc)
+        if kr < k:
+            sr, Pr, kr, _ = id_fixed(t_row.T, eps, min_rank=k)
+        else:
+            sc, Pc, kc, _ = id_fixed(t_col, eps, min_rank=k)
+    ro = np.argsort(sr)
+    co = np.argsort(sc)
+    return (rd[sr[ro]], cd[sc[co]], D, np.ascontiguousarray(Pr.T[:, ro], dtype=dtype),
+            np.ascontiguousarray(Pc[co, :], dtype=dtype), int(rz1) + int(rz2))
+
+
 def compress(src, tree: Tree, eps, n_proxy=None, radius_factor=1.0,
              mode="proxy", equalize=True, seed=0):
     """Level sweep of skel.py:286-411 over an oracle source."""
@@ -112,12 +161,6 @@ def compress(src, tree: Tree, eps, n_proxy=None, radius_factor=1.0,
         allidx = np.arange(n)
         return OracleCompressed([], np.ascontiguousarray(src.block(allidx, allidx), dtype=dtype),
                                 n, eps, tree.perm.copy(), dtype)
-    kw = float(getattr(src, "wavenumber", 0.0))
-
-    def blk(r, c):
-        if r.size == 0 or c.size == 0:
-            return np.zeros((r.size, c.size), dtype=dtype)
-        return src.block(r, c)
 
     levels = []
     prev = None
@@ -142,49 +185,26 @@ def compress(src, tree: Tree, eps, n_proxy=None, radius_factor=1.0,
         lv = OracleLevel([], [], [], [], [], coff, ids)
         for a in range(p):
             rd, cd = rows[a], cols[a]
-            D = np.ascontiguousarray(blk(rd, cd), dtype=dtype)
+            zero = None
             if li > 0:
-                r0 = c0 = 0
-                for c in range(coff[a], coff[a + 1]):
-                    kr_c, kc_c = prev.row_skel[c].size, prev.col_skel[c].size
-                    D[r0:r0 + kr_c, c0:c0 + kc_c] = 0
-                    r0 += kr_c
-                    c0 += kc_c
+                zero = [(prev.row_skel[c].size, prev.col_skel[c].size)
+                        for c in range(coff[a], coff[a + 1])]
             nb = nidx[noff[a]:noff[a + 1]]
-            ncols = np.concatenate([cols[b] for b in nb]) if nb.size else np.empty(0, dtype=np.int64)
-            nrows = np.concatenate([rows[b] for b in nb]) if nb.size else np.empty(0, dtype=np.int64)
             if mode == "proxy":
-                nid = ids[a]
-                r = proxy_radius(tree.hw[nid], dim, radius_factor)
-                neff = npx
-                if kw > 0:
-                    neff += int(np.ceil(4.0 * kw * r))
-                pxy = tree.center[nid] + r * proxy_unit_points(neff, dim)
-                t_row = (np.hstack([blk(rd, ncols), src.proxy_row_block(rd, pxy)])
-                         if rd.size else np.zeros((0, neff), dtype=dtype))
-                t_col = (np.vstack([blk(nrows, cd), src.proxy_col_block(cd, pxy)])
-                         if cd.size else np.zeros((neff, 0), dtype=dtype))
+                ncols = np.concatenate([cols[b] for b in nb]) if nb.size else np.empty(0, dtype=np.int64)
+                nrows = np.concatenate([rows[b] for b in nb]) if nb.size else np.empty(0, dtype=np.int64)
             else:
-                oc = np.concatenate([cols[b] for b in range(p) if b != a])
-                orr = np.concatenate([rows[b] for b in range(p) if b != a])
-                t_row = blk(rd, oc)
-                t_col = blk(orr, cd)
-            (sr, Pr, kr, _), rz1 = run_id(t_row.T, eps, seed, (li, a, 0))
-            (sc, Pc, kc, _), rz2 = run_id(t_col, eps, seed, (li, a, 1))
-            n_rand += int(rz1) + int(rz2)
-            if equalize and kr != kc:
-                k = max(kr, kc)
-                if kr < k:
-                    sr, Pr, kr, _ = id_fixed(t_row.T, eps, min_rank=k)
-                else:
-                    sc, Pc, kc, _ = id_fixed(t_col, eps, min_rank=k)
-            ro = np.argsort(sr)
-            co = np.argsort(sc)
-            lv.row_skel.append(rd[sr[ro]])
-            lv.col_skel.append(cd[sc[co]])
+                ncols = np.concatenate([cols[b] for b in range(p) if b != a])
+                nrows = np.concatenate([rows[b] for b in range(p) if b != a])
+            sr, sc, D, L, R, nr_ = compress_box(src, tree, li, a, ids[a], rd, cd, zero, ncols,
+                                                nrows, eps, npx, radius_factor, mode, equalize,
+                                                seed)
+            n_rand += nr_
+            lv.row_skel.append(sr)
+            lv.col_skel.append(sc)
             lv.D.append(D)
-            lv.L.append(np.ascontiguousarray(Pr.T[:, ro], dtype=dtype))
-            lv.R.append(np.ascontiguousarray(Pc[co, :], dtype=dtype))
+            lv.L.append(L)
+            lv.R.append(R)
         levels.append(lv)
         prev = lv
 
@@ -222,6 +242,41 @@ def _lu(B, level, node, what, regularize, dtype):
     return lu, piv
 
 
+def factor_box(D, L, R, k, lams, li, a, regularize, dtype):
+    """factor_node (solver.py:224-262) for box ``a`` of level ``li``: D_eff =
+    D with the children's Lambda (``lams``) on the diagonal blocks, LU, D^-1,
+    X, RD^-1, Lambda, Rd, Ld, Dd.  Returns (Dd, Ld, Rd, Lam, warnings)."""
+    warns = []
+    De = np.array(D, dtype=dtype)
+    if lams:
+        r0 = 0
+        for lc in lams:
+            De[r0:r0 + lc.shape[0], r0:r0 + lc.shape[1]] = lc
+            r0 += lc.shape[0]
+    nn = De.shape[0]
+    luD = _lu(De, li + 1, a, "D", regularize, dtype)
+    if luD is None:
+        z = np.zeros((0, 0), dtype=dtype)
+        return z, z, z, z, warns
+    Dinv = lu_solve(luD, np.eye(nn, dtype=dtype), check_finite=False)
+    rc = _rcond1(De, Dinv)
+    if rc < RCOND_WARN:
+        warns.append((li + 1, a, "D", rc))
+    if k == 0:
+        return (Dinv, np.zeros((nn, 0), dtype=dtype), np.zeros((0, nn), dtype=dtype),
+                np.zeros((0, 0), dtype=dtype), warns)
+    X = lu_solve(luD, L, check_finite=False)
+    RD = lu_solve(luD, R.T, trans=1, check_finite=False).T
+    M = R @ X
+    luM = _lu(M, li + 1, a, "Lambda", regularize, dtype)
+    Lam = lu_solve(luM, np.eye(k, dtype=dtype), check_finite=False)
+    rc = _rcond1(M, Lam)
+    if rc < RCOND_WARN:
+        warns.append((li + 1, a, "Lambda", rc))
+    Rd = Lam @ RD
+    return Dinv - X @ Rd, X @ Lam, Rd, Lam, warns
+
+
 def factor(oc: OracleCompressed, regularize=0.0):
     """Telescoping inverse (solver.py:187-276)."""
     dtype = oc.dtype
@@ -235,44 +290,13 @@ def factor(oc: OracleCompressed, regularize=0.0):
     for li, lv in enumerate(oc.levels):
         Dd_l, Ld_l, Rd_l, Lam_l = [], [], [], []
         for a in range(len(lv.D)):
-            De = np.array(lv.D[a], dtype=dtype)
+            lams = None
             if li > 0:
-                r0 = 0
-                for c in range(lv.child_off[a], lv.child_off[a + 1]):
-                    lc = lam_prev[c]
-                    De[r0:r0 + lc.shape[0], r0:r0 + lc.shape[1]] = lc
-                    r0 += lc.shape[0]
-            nn = De.shape[0]
-            k = lv.row_skel[a].size
-            luD = _lu(De, li + 1, a, "D", regularize, dtype)
-            if luD is None:
-                z = np.zeros((0, 0), dtype=dtype)
-                Dd_l.append(z); Ld_l.append(z); Rd_l.append(z); Lam_l.append(z)
-                continue
-            Dinv = lu_solve(luD, np.eye(nn, dtype=dtype), check_finite=False)
-            rc = _rcond1(De, Dinv)
-            if rc < RCOND_WARN:
-                warns.append((li + 1, a, "D", rc))
-            if k == 0:
-                Dd_l.append(Dinv)
-                Ld_l.append(np.zeros((nn, 0), dtype=dtype))
-                Rd_l.append(np.zeros((0, nn), dtype=dtype))
-                Lam_l.append(np.zeros((0, 0), dtype=dtype))
-                continue
-            L, R = lv.L[a], lv.R[a]
-            X = lu_solve(luD, L, check_finite=False)
-            RD = lu_solve(luD, R.T, trans=1, check_finite=False).T
-            M = R @ X
-            luM = _lu(M, li + 1, a, "Lambda", regularize, dtype)
-            Lam = lu_solve(luM, np.eye(k, dtype=dtype), check_finite=False)
-            rc = _rcond1(M, Lam)
-            if rc < RCOND_WARN:
-                warns.append((li + 1, a, "Lambda", rc))
-            Rd = Lam @ RD
-            Dd_l.append(Dinv - X @ Rd)
-            Ld_l.append(X @ Lam)
-            Rd_l.append(Rd)
-            Lam_l.append(Lam)
+                lams = [lam_prev[c] for c in range(lv.child_off[a], lv.child_off[a + 1])]
+            Dd, Ld, Rd, Lam, w = factor_box(lv.D[a], lv.L[a], lv.R[a], lv.row_skel[a].size,
+                                            lams, li, a, regularize, dtype)
+            warns.extend(w)
+            Dd_l.append(Dd); Ld_l.append(Ld); Rd_l.append(Rd); Lam_l.append(Lam)
         Dd_all.append(Dd_l); Ld_all.append(Ld_l); Rd_all.append(Rd_l); Lam_all.append(Lam_l)
         lam_prev = Lam_l
     last = oc.levels[-1]

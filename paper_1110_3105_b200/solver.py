@@ -498,7 +498,7 @@ def solve(fi: FactoredInverse, b):
         B = ba.reshape(fi.n, -1).to(_native.torch_dtype(field)).contiguous()
     else:
         B = torch.from_numpy(np.ascontiguousarray(ba.reshape(fi.n, -1), dtype=dtype)).to("cuda")
-    X = solve_device(fi, B)
+    X = solve_device(fi, B, _private=not on_dev)
     if on_dev:
         return X[:, 0] if single else X
     x = _native.to_host(X)
@@ -551,17 +551,58 @@ _GRAPH_CACHE = 4
 _GRAPH_MAX_R = 64
 
 
-def solve_device(fi: FactoredInverse, B, graph: bool = True):
+def _device_rhs(fi: FactoredInverse, B):
+    """Validate / normalise a device RHS for the sweeps: (N, R) or (N,), on
+    the GPU, the factorization's field (real B for a complex factorization is
+    promoted), row-major contiguous.  Anything else is InvalidInput."""
+    torch = _native.require_cuda()
+    if not isinstance(B, torch.Tensor) or not B.is_cuda:
+        raise InvalidInput("solve_device expects a CUDA tensor")
+    if B.ndim not in (1, 2) or B.shape[0] != fi.n:
+        raise InvalidInput(f"length mismatch: system is {fi.n}, rhs shape {tuple(B.shape)}")
+    if B.dtype not in (torch.float64, torch.complex128, torch.float32, torch.complex64):
+        raise InvalidInput(f"unsupported rhs dtype {B.dtype}")
+    if B.ndim == 1:
+        B = B.reshape(fi.n, 1)
+    want = _native.torch_dtype(fi.field)
+    if B.dtype != want:
+        if B.is_complex() and fi.field == 0:
+            raise InvalidInput("complex rhs with a real factorization: use solve() "
+                               "(two real solves) or pass the real and imaginary parts")
+        B = B.to(want)
+    return B.contiguous()
+
+
+def solve_device(fi: FactoredInverse, B, graph: bool = True, _private: bool = False):
     """Device-resident solve of an (N, R) CUDA tensor (original ordering).
 
     The ~30-40 launches of one solve (gather, per-level size-bucketed sweeps
     on side streams, top GEMM, scatter) are captured into a CUDA graph on the
-    first repeat of a shape and replayed from then on.  When the SAME
-    contiguous B tensor comes back (the multi-RHS reuse pattern) the graph is
-    captured on that tensor itself and replays with no input copy (the cache
-    holds a reference, so the storage cannot be recycled under the graph);
-    other tensors of that shape are copied into a private-input graph.  The
-    result is always a fresh tensor."""
+    first repeat of a shape and replayed from then on.  When the SAME tensor
+    object comes back (the multi-RHS reuse pattern) the graph is captured on
+    that tensor itself and replays with no input copy (the cache holds a
+    reference, so the storage cannot be recycled under the graph); other
+    tensors of that shape -- and every call from ``solve()``, whose uploads
+    are fresh temporaries (``_private``) -- are copied into a private-input
+    graph.  A complex B with a real factorization runs as two real solves.
+    The result is always a fresh tensor."""
+    import weakref
+    torch = _native.require_cuda()
+    if (isinstance(B, torch.Tensor) and B.is_cuda and B.is_complex() and fi.field == 0
+            and B.ndim in (1, 2) and B.shape[0] == fi.n):
+        xr = solve_device(fi, B.real, graph, _private=True)
+        xi = solve_device(fi, B.imag, graph, _private=True)
+        return torch.complex(xr, xi)
+    single = isinstance(B, torch.Tensor) and B.ndim == 1
+    user = B
+    B = _device_rhs(fi, B)
+    if B is not user:
+        _private = True                      # a converted copy: never bind a graph to it
+    X = _solve_graph(fi, B, graph, _private, user, weakref)
+    return X[:, 0] if single else X
+
+
+def _solve_graph(fi, B, graph, private, user, weakref):
     torch = _native.require_cuda()
     if (not graph or _profile.enabled or torch.cuda.is_current_stream_capturing()
             or fi.shard is not None or B.shape[1] > _GRAPH_MAX_R):
@@ -569,14 +610,17 @@ def solve_device(fi: FactoredInverse, B, graph: bool = True):
         # graph's output copy would not be (8.6 GB at 2^20 x 1024)
         return _solve_device_eager(fi, B)
     key = (int(B.shape[1]), B.dtype)
-    pkey = key + (B.data_ptr(), tuple(B.stride()))
     cache = fi.__dict__.setdefault("_graphs", {})
     seen = fi.__dict__.setdefault("_graph_seen", set())
-    last = fi.__dict__.get("_last_pkey")
-    fi.__dict__["_last_pkey"] = pkey
-    ent = cache.get(pkey)
-    if ent is None and pkey == last and B.is_contiguous():
-        ent = cache[pkey] = _capture(fi, B, cache)          # same tensor again
+    ent = None
+    if not private:
+        last = fi.__dict__.get("_last_user")
+        fi.__dict__["_last_user"] = weakref.ref(user)
+        ent = cache.get(("user", id(user)))
+        if ent is not None and ent[1] is not user:
+            ent = None                       # id() recycled by another object
+        if ent is None and last is not None and last() is user:
+            ent = cache[("user", id(user))] = _capture(fi, B, cache)   # same tensor again
     if ent is not None:
         g, _, static_X = ent
     else:
