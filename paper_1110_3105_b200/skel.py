@@ -246,6 +246,19 @@ class CompressedLevel:
             self._nodes = out
         return self._nodes
 
+    def skeleton_arrays(self):
+        """(row_skel, col_skel) of every box, concatenated in box order (host
+        int64) -- the skeleton lists without copying D / L / R to the host."""
+        if self._nodes is not None or self.dev is None:
+            nd = self.nodes
+            cat = lambda xs: (np.concatenate(xs).astype(np.int64) if xs  # noqa: E731
+                              else np.zeros(0, dtype=np.int64))
+            return cat([x.row_skel for x in nd]), cat([x.col_skel for x in nd])
+        d = self.dev
+        rs = d.rskel.cpu().numpy()[:int(self.kr_off[-1])].astype(np.int64)
+        cs = d.cskel.cpu().numpy()[:int(self.kc_off[-1])].astype(np.int64)
+        return rs, cs
+
     @property
     def K_r(self):
         return int(self.kr_off[-1])

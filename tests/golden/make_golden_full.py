@@ -110,7 +110,6 @@ def config2():
     Om = np.random.default_rng(1).standard_normal((n, 8))
     out["c5_sketch"] = Om.T @ X5
     out["c5_colnorm"] = np.linalg.norm(X5, axis=0)
-    out["c5_X63"] = X5[:, 63].copy()
     out.update({"eps": np.array(eps), "n": np.array(n)})
     return out
 
