@@ -161,12 +161,15 @@ int skel_eval_block(const SkelSource* src, const int32_t* rows, int32_t m,
 /* Batched column ID of explicit matrices (id_fixed_precision,
  * lowrank.py:136-161).  Matrix b is column-major m[b] x n[b] at a_off[b].
  * Outputs: rank[b], skel (pivot order, n[b] capacity at skel_off[b]),
- * proj (rank x n row-major, capacity n*n at proj_off[b]), bigP[b] = max|P|. */
+ * proj (rank x n row-major, capacity n*n at proj_off[b]), bigP[b] = max|P|,
+ * ratio[b] (nullable) = the first rejected pivot norm over the leading one
+ * (InterpDecomp.achieved_error, lowrank.py:116-118,161; 0 when the CPQR ran
+ * to min(m, n) or hit an exactly zero pivot). */
 int skel_id_batched(const void* A, const int64_t* a_off, const int32_t* m,
                     const int32_t* n, int32_t nmat, double eps,
                     const int32_t* min_rank, int32_t* rank, int32_t* skel,
                     const int64_t* skel_off, void* proj, const int64_t* proj_off,
-                    double* bigP, int32_t field, void* scratch,
+                    double* bigP, double* ratio, int32_t field, void* scratch,
                     int64_t scratch_bytes, int32_t max_m, int32_t max_n,
                     void* stream);
 
@@ -265,8 +268,11 @@ int skel_big_target(const SkelSource* src, const SkelLevel* lv, int32_t box, int
                     const int32_t* nbr_box, const int32_t* nbr_pref, int32_t nnb, int32_t m,
                     int32_t n, void* W, int64_t ld, int32_t field, void* stream);
 
-/* Cooperative CPQR of W in place (pivoted_qr, lowrank.py:48-119); resume != 0
- * continues from the state's rank with the new min_rank (equalisation). */
+/* Cooperative CPQR of W in place (pivoted_qr, lowrank.py:48-119).  resume
+ * bit 0: continue from the state's rank with the new min_rank; bit 1
+ * (equalisation, skel.py:377-382): stop after exactly min_rank steps, so the
+ * box stays square even where a recomputed stale norm would carry the
+ * reference's re-run past k. */
 int skel_cpqr_big(void* W, int32_t m, int32_t n, int64_t ld, double eps, int32_t min_rank,
                   int32_t resume, void* state, int32_t field, void* stream);
 

@@ -76,8 +76,9 @@ class SketchStream:
     the probe vectors are drawn from the generator state saved right after
     the last sketch actually used."""
 
-    def __init__(self, seed, m, n, cplx, expect_rank=None):
+    def __init__(self, seed, m, n, cplx, expect_rank=None, oversampling=OVERSAMPLING):
         import threading
+        self.os = int(oversampling)
         self.rng = np.random.default_rng(seed)
         self.m, self.n, self.cplx = m, n, cplx
         self.v0 = self._draw(n)
@@ -86,8 +87,8 @@ class SketchStream:
         self.stopped = False
         self.want = 0
         k = n // 2 if expect_rank is None else expect_rank
-        self.target = 2 * OVERSAMPLING
-        while self.target < k + OVERSAMPLING:
+        self.target = 2 * self.os
+        while self.target < k + self.os:
             self.target *= 2
         self.last_state = None
         self.th = threading.Thread(target=self._run, daemon=True)
@@ -102,7 +103,7 @@ class SketchStream:
     def _run(self):
         import copy
         torch = _native.require_cuda()
-        ell = 2 * OVERSAMPLING
+        ell = 2 * self.os
         while ell < self.m:
             with self.cv:
                 while not self.stopped and ell > self.target and self.want < ell:
@@ -170,12 +171,12 @@ def _norm_estimate(torch, L, sd, v, cplx, tdt, field, st, iters=8):
     return float(s)
 
 
-def _randomized(torch, L, sd, eps, seed, field, tdt, st, stream=None):
+def _randomized(torch, L, sd, eps, seed, field, tdt, st, stream=None, oversampling=OVERSAMPLING):
     """id_randomized (lowrank.py:186-231) on the side's target; falls back
     to the deterministic CPQR exactly where the reference does."""
     m, n = sd.m, sd.n
     cplx = bool(field)
-    ss = stream if stream is not None else SketchStream(seed, m, n, cplx)
+    ss = stream if stream is not None else SketchStream(seed, m, n, cplx, oversampling=oversampling)
     try:
         _randomized_body(torch, L, sd, eps, ss, field, tdt, st, cplx)
     finally:
@@ -188,7 +189,8 @@ def _randomized_body(torch, L, sd, eps, ss, field, tdt, st, cplx):
     if normA == 0.0:
         _cpqr(L, sd.W, m, n, m, eps, 0, 0, sd.state, field, st)      # rank 0, empty ID
         return
-    ell = 2 * OVERSAMPLING
+    os_ = ss.os
+    ell = 2 * os_
     while True:
         if ell >= m:
             _cpqr(L, sd.W, m, n, m, eps, 0, 0, sd.state, field, st)
@@ -202,7 +204,7 @@ def _randomized_body(torch, L, sd, eps, ss, field, tdt, st, cplx):
         ystate = torch.zeros_like(sd.state)
         _cpqr(L, Y, ell, n, ell, eps, 0, 0, ystate, field, st)
         rank = _rank_of(ystate)
-        if rank <= ell - OVERSAMPLING:
+        if rank <= ell - os_:
             break
         ell *= 2
     _native.check(L.skel_big_interp(_native.ptr(Y), n, ell, _native.ptr(ystate), 0, field, st),
@@ -225,6 +227,7 @@ def _randomized_body(torch, L, sd, eps, ss, field, tdt, st, cplx):
         _cpqr(L, sd.W, m, n, m, eps, 0, 0, sd.state, field, st)
         return
     sd.kind = "rand"
+    sd.worst = worst
     sd.Y, sd.W_out, sd.ld_out, sd.state_out = Y, Y, ell, ystate
 
 
@@ -285,11 +288,12 @@ def run_boxes(desc, lvd, boxes, li, noff, nidx, nr, nc, neff, eps, equalize, see
             k = max(ks)
             q = 0 if ks[0] < k else 1
             sd = sides[q]
+            # (resume bit 1: stop after exactly k steps, so the box stays square)
             if sd.kind == "fixed":
-                _cpqr(L, sd.W, sd.m, sd.n, sd.m, eps, k, 1, sd.state, field, st)
+                _cpqr(L, sd.W, sd.m, sd.n, sd.m, eps, k, 3, sd.state, field, st)
             else:
                 sd.kind, sd.W_out, sd.ld_out, sd.state_out = "fixed", sd.W, sd.m, sd.state
-                _cpqr(L, sd.W, sd.m, sd.n, sd.m, eps, k, 0, sd.state, field, st)
+                _cpqr(L, sd.W, sd.m, sd.n, sd.m, eps, k, 2, sd.state, field, st)
             min_rank[q] = k
         for side, sd in enumerate(sides):
             if sd.kind == "fixed":

@@ -76,7 +76,7 @@ _SIGS = {
     "skel_assemble_S": [_P(SkelSource), c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp],
     "skel_eval_block": [_P(SkelSource), c_vp, c_i32, c_vp, c_i32, c_vp, c_i32, c_vp],
     "skel_id_batched": [c_vp, c_vp, c_vp, c_vp, c_i32, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp,
-                        c_vp, c_vp, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp],
+                        c_vp, c_vp, c_vp, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp],
     "skel_factor_level": [_P(SkelFactorLevel), c_i32, c_i32, c_i32, c_vp],
     "skel_dense_inverse": [c_vp, c_vp, c_vp, c_i32, c_f64, c_vp, c_vp, c_i32, c_vp, c_vp],
     "skel_sweep_up_ex": [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32,

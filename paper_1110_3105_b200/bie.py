@@ -202,6 +202,19 @@ class BieSource(_DeviceSourceMixin):
     def _desc(self):
         return self.system.descriptor(self.geo, self.wscale)
 
+    # the reference's proxy protocol (bie.py:251-262), device-evaluated; the
+    # fast sweep builds these blocks inside the ID kernel instead
+    @property
+    def points(self):
+        return self.system.curve.point_set().subset(self.perm)
+
+    def proxy_row_block(self, rows, pxy):
+        return self.wscale * eval_block(self.system.spec.single_layer(), self.points.subset(rows), pxy)
+
+    def proxy_col_block(self, cols, pxy):
+        src = self.points.subset(cols)
+        return eval_block(self.system.spec.single_layer(), pxy, PointSet(src.coords, None, src.weights))
+
 
 _BieSource = BieSource
 

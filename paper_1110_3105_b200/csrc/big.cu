@@ -134,7 +134,7 @@ __global__ void k_cpqr_big_init(const T* W, int m, int n, int64_t ld, void* buf)
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     v.st->rank = 0; v.st->stop = 0; v.st->pad = 0; v.st->pc = 0;
-    v.st->p0 = 0.0; v.st->beta = 0.0; v.st->bigP = 0.0;
+    v.st->p0 = 0.0; v.st->beta = 0.0; v.st->bigP = 0.0; v.st->pad0 = 0.0;
   }
 }
 
@@ -148,7 +148,7 @@ __global__ void k_cpqr_big_init(const T* W, int m, int n, int64_t ld, void* buf)
 template <class T>
 __global__ void __launch_bounds__(256)
     k_cpqr_big(T* W, int m, int n, int64_t ld, double eps, int min_rank, void* buf, int vsmem,
-               int* pivb, double* cand_v, int* cand_i) {
+               int* pivb, double* cand_v, int* cand_i, int kcap) {
   cg::grid_group grid = cg::this_grid();
   BigView<T> v = big_view<T>(buf, n);
   extern __shared__ __align__(16) unsigned char cp_smem[];
@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(256)
   const int tw = (gridDim.x * blockDim.x) >> 5;
   int s = ldcg(&v.st->rank);
   double p0 = ldcg(&v.st->p0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) v.st->pad0 = 0.0;   // set again at a rule stop
   int* pcur = v.piv;
   int* pnext = pivb;
   // candidates for the first step: every CTA scans nrm[s..n) itself
@@ -191,21 +192,27 @@ __global__ void __launch_bounds__(256)
   double bsel = red_v;
   int jsel = red_i;
   int par = 0;
-  while (s < kmax) {
+  const int kend = kmax < kcap ? kmax : kcap;     // equalisation: exactly min_rank steps
+  while (s < kend) {
     // ---- pivot + stop rule (identical on every CTA)
     const int j = jsel;
     int stop = 0;
+    double pn = 0.0;
     if (j >= n) {
       stop = 1;
     } else {
-      const double pn = sqrt(fmax(bsel, 0.0));
+      pn = sqrt(fmax(bsel, 0.0));
       if (s == 0) {
         p0 = pn;
         if (pn == 0.0) stop = 1;
       }
-      if (!stop && ((s >= min_rank && pn <= eps * p0) || pn == 0.0)) stop = 1;
+      if (!stop && ((s >= min_rank && pn <= eps * p0) || pn == 0.0)) stop = 2;
     }
-    if (stop) break;
+    if (stop) {
+      // first rejected pivot norm: achieved_error numerator (lowrank.py:88-90)
+      if (blockIdx.x == 0 && threadIdx.x == 0) v.st->pad0 = stop == 2 ? pn : 0.0;
+      break;
+    }
     const int pc = ldcg(pcur + j);           // pivot column
     const int ps_old = ldcg(pcur + s);
     const double nrm_s_old = ldcg(v.nrm + s);
@@ -883,9 +890,12 @@ __global__ void k_lu_inverse(const T* __restrict__ LU, const int* __restrict__ p
 
 // undo the row interchanges on the inverse's columns (reverse order)
 template <class T>
-__global__ void k_gj_unswap(T* A, int n, const int* swaps, const int32_t* status) {
+__global__ void k_gj_unswap(T* A, int n, const int* swaps, const int32_t* status,
+                            const int32_t* skip) {
+  // skipped (skip set: an earlier step of the box failed) or singular runs
+  // leave `swaps` unwritten: never read it then
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n || *status) return;
+  if (r >= n || *status || (skip && *skip)) return;
   T* row = A + r * n;
   for (int c = n - 1; c >= 0; --c) {
     const int p = swaps[c];
@@ -1053,7 +1063,10 @@ static int coop_grid(K kernel, int threads, size_t smem) {
 template <class T>
 static int cpqr_big_impl(void* W, int m, int n, int64_t ld, double eps, int min_rank, int resume,
                          void* state, cudaStream_t st) {
-  if (!resume) {
+  // resume bit 0: continue a previous run; bit 1: equalisation -- stop after
+  // exactly min_rank steps (see cpqr_run in cpqr.cuh)
+  const int kcap = (resume & 2) ? min_rank : 0x7fffffff;
+  if (!(resume & 1)) {
     int blocks = (n * 32 + 255) / 256;
     if (blocks < 1) blocks = 1;
     k_cpqr_big_init<T><<<blocks, 256, 0, st>>>((const T*)W, m, n, ld, state);
@@ -1073,7 +1086,8 @@ static int cpqr_big_impl(void* W, int m, int n, int64_t ld, double eps, int min_
   double* cand_v = (double*)(extra + (((size_t)n * sizeof(int) + 15) / 16) * 16);
   int* cand_i = (int*)(cand_v + 2 * 4096);
   T* Wp = (T*)W;
-  void* args[] = {&Wp, &m, &n, &ld, &eps, &min_rank, &state, &vsmem, &pivb, &cand_v, &cand_i};
+  int kc = kcap;
+  void* args[] = {&Wp, &m, &n, &ld, &eps, &min_rank, &state, &vsmem, &pivb, &cand_v, &cand_i, &kc};
   SKEL_TRY(cudaLaunchCooperativeKernel((const void*)k_cpqr_big<T>, grid, 256, args, smem, st));
   return 0;
 }
@@ -1093,7 +1107,7 @@ static int gj_impl(void* A, int n, double regularize, int32_t* status, void* scr
   T* Ap = (T*)A;
   void* args[] = {&Ap, &n, &regularize, &status, &part_v, &part_i, &colc, &swaps, &skip};
   SKEL_TRY(cudaLaunchCooperativeKernel((const void*)k_gj_coop<T>, grid, 256, args, smem, st));
-  k_gj_unswap<T><<<(n + 127) / 128, 128, 0, st>>>(Ap, n, swaps, status);
+  k_gj_unswap<T><<<(n + 127) / 128, 128, 0, st>>>(Ap, n, swaps, status, skip);
   return skel_last_error();
 }
 

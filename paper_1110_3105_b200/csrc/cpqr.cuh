@@ -46,6 +46,7 @@ struct CpqrShared {
   int partner_k; // rank of the other side of the box (equalize)
   int pc;        // column of the current pivot
   double bigP;   // max |P| (interp quality warning, lowrank.py:128-132)
+  double trail;  // first rejected pivot norm (achieved_error numerator, lowrank.py:88-90)
   double cand_v[CPQR_MAXW];
   int cand_i[CPQR_MAXW];
 };
@@ -92,38 +93,47 @@ __device__ void cpqr_init(const T* W, int m, int n, int ld, double* nrm, double*
 template <class T>
 __device__ void cpqr_pivot(T* W, int m, int n, int ld, double* nrm, double* xn2, int* piv,
                            CpqrShared<T>& sh, int s, double eps, int min_rank, int nw) {
+  // all 32 lanes: the per-warp candidates are merged by a butterfly (every
+  // lane ends with the first maximum), the stop rule is evaluated uniformly,
+  // and the pivot column is known to every lane without a broadcast
   const int lane = threadIdx.x & 31;
-  int stop = 0, pc = 0;
-  double nx2 = 0.0;
+  double bv = -1.0;
+  int j = 0x7fffffff;
+  if (lane < nw) { bv = sh.cand_v[lane]; j = sh.cand_i[lane]; }
+  // full butterfly: EVERY lane must end with the same pivot (the stop
+  // decision below is taken per lane and must be warp-uniform)
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, j, o);
+    cand_merge(bv, j, ov, oi);
+  }
+  int stop = 0;
+  double pn = 0.0;
+  if (j >= n) {
+    stop = 1;
+  } else {
+    pn = sqrt(fmax(nrm[j], 0.0));
+    const double p0 = s == 0 ? pn : sh.p0;
+    if (s == 0 && pn == 0.0) stop = 1;
+    else if ((s >= min_rank && pn <= eps * p0) || pn == 0.0) stop = 2;
+  }
   if (lane == 0) {
-    double bv = -1.0;
-    int j = 0x7fffffff;
-    for (int w = 0; w < nw; ++w) cand_merge(bv, j, sh.cand_v[w], sh.cand_i[w]);
-    if (j >= n) {
-      stop = 1;
-    } else {
-      double pn = sqrt(fmax(nrm[j], 0.0));
-      if (s == 0) {
-        sh.p0 = pn;
-        if (pn == 0.0) stop = 1;
-      }
-      if (!stop && ((s >= min_rank && pn <= eps * sh.p0) || pn == 0.0)) stop = 1;
-      if (!stop) {
-        if (j != s) {
-          double t = nrm[s]; nrm[s] = nrm[j]; nrm[j] = t;
-          if (xn2) { t = xn2[s]; xn2[s] = xn2[j]; xn2[j] = t; }
-          int q = piv[s]; piv[s] = piv[j]; piv[j] = q;
-        }
-        pc = piv[s];
-        if (xn2) nx2 = xn2[s];
-        else if (s == 0) nx2 = nrm[s];          // exact full norm at step 0
-      }
-    }
+    if (s == 0 && j < n) sh.p0 = pn;
+    if (stop == 2) sh.trail = pn;
     sh.stop = stop;
   }
-  stop = __shfl_sync(0xffffffffu, stop, 0);
   if (stop) return;
-  pc = __shfl_sync(0xffffffffu, pc, 0);
+  const int pc = piv[j];                 // pivot column (position j before the swap)
+  double nx2 = 0.0;
+  if (xn2) nx2 = xn2[j];
+  else if (s == 0) nx2 = nrm[j];         // exact full norm at step 0
+  __syncwarp();
+  if (lane == 0 && j != s) {
+    double t = nrm[s]; nrm[s] = nrm[j]; nrm[j] = t;
+    if (xn2) { t = xn2[s]; xn2[s] = xn2[j]; xn2[j] = t; }
+    piv[j] = piv[s];
+    piv[s] = pc;
+  }
   if (!xn2 && s > 0) {
     const T* x = W + (int64_t)pc * ld;
     double acc = 0.0;
@@ -140,7 +150,8 @@ __device__ void cpqr_pivot(T* W, int m, int n, int ld, double* nrm, double* xn2,
     const double vv = 2.0 * normx * (normx + ax0);    // |x - alpha e1|^2
     sh.v0 = x0 - alpha;
     sh.alpha = alpha;
-    sh.beta = vv > 0.0 ? 2.0 / vv : 0.0;
+    // 2 / vv exactly: a power-of-two scaling commutes with rounding
+    sh.beta = vv > 0.0 ? 2.0 * __drcp_rn(vv) : 0.0;
     sh.pc = pc;
   }
 }
@@ -258,19 +269,127 @@ __device__ void cpqr_update(T* W, int m, int n, int ld, double* nrm, double* ref
   if (lane == 0) { sh.cand_v[warp] = bv; sh.cand_i[warp] = bi; }
 }
 
+// Phase B, real targets, paired-row register path.  Requires an EVEN leading
+// dimension whose pad row (row m when m is odd) is zero in every column and a
+// 16-byte aligned W.  Lane gl of a GL-lane group holds the row pairs
+// {s0 + 2 gl + 2 GL r, +1} (s0 = s rounded down to even, r < RP2) of the
+// reflector and of its column, so every shared-memory access is one 16-byte
+// LDS/STS per two rows and no per-row predicate is needed: the reflector is
+// zero above row s (those rows of the column are left exactly unchanged) and
+// the pad row stays zero (0 - 0 f).  Same arithmetic per entry as the
+// generic path (dot in four partial chains, one rank-1 update per entry).
+template <int GL, int RP2>
+__device__ void cpqr_update_pr(double* W, int m, int n, int ld, double* nrm, double* ref,
+                               const int* piv, CpqrShared<double>& sh, int s, int kmax) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double v0 = sh.v0;
+  const double beta = sh.beta;
+  const int s1 = s + 1, s0 = s & ~1;
+  const bool renorm = (s1 < kmax) && (s1 % 32 == 0);
+  constexpr int CPW = 32 / GL;
+  const int g = lane / GL, gl = lane - (lane / GL) * GL;
+  const double* vcol = W + (int64_t)sh.pc * ld;
+  double2 vr[RP2];
+#pragma unroll
+  for (int r = 0; r < RP2; ++r) {
+    const int i = s0 + 2 * gl + 2 * GL * r;
+    vr[r] = (i < m) ? *reinterpret_cast<const double2*>(vcol + i) : make_double2(0.0, 0.0);
+  }
+  if (gl == 0) {
+    // rows s0, s0+1: row s carries v0; an odd s zeroes row s-1 (an R entry)
+    if (s & 1) { vr[0].x = 0.0; vr[0].y = v0; } else { vr[0].x = v0; }
+  }
+  double bv = -1.0;
+  int bi = 0x7fffffff;
+  for (int cb = s1 + warp * CPW; cb < n; cb += nw * CPW) {
+    const int c = cb + g;
+    const bool act = c < n;
+    double* wc = W + (int64_t)piv[act ? c : n - 1] * ld;
+    double2 wr[RP2];
+    double d4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int r = 0; r < RP2; ++r) {
+      const int i = s0 + 2 * gl + 2 * GL * r;
+      wr[r] = (i < m) ? *reinterpret_cast<const double2*>(wc + i) : make_double2(0.0, 0.0);
+      d4[(2 * r) & 3] += vr[r].x * wr[r].x;
+      d4[(2 * r + 1) & 3] += vr[r].y * wr[r].y;
+    }
+    double dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+#pragma unroll
+    for (int o = GL / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    const double f = dot * beta;
+#pragma unroll
+    for (int r = 0; r < RP2; ++r) {
+      const int i = s0 + 2 * gl + 2 * GL * r;
+      wr[r].x -= vr[r].x * f;
+      wr[r].y -= vr[r].y * f;
+      if (i < m && act) *reinterpret_cast<double2*>(wc + i) = wr[r];
+    }
+    double t = 0.0;
+    int need = 0;
+    if (gl == 0 && act) {
+      const double rs = (s & 1) ? wr[0].y : wr[0].x;     // R[s, c]
+      t = nrm[c] - rs * rs;
+      t = t > 0.0 ? t : 0.0;
+      need = (s1 < kmax) && (renorm || t < 1e-8 * ref[c]);
+    }
+    need = __shfl_sync(0xffffffffu, need, g * GL);
+    if (__any_sync(0xffffffffu, need)) {
+      double x4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int r = 0; r < RP2; ++r) {
+        const int i = s0 + 2 * gl + 2 * GL * r;
+        if (i > s) x4[(2 * r) & 3] += wr[r].x * wr[r].x;
+        if (i + 1 > s) x4[(2 * r + 1) & 3] += wr[r].y * wr[r].y;
+      }
+      double xa = (x4[0] + x4[1]) + (x4[2] + x4[3]);
+#pragma unroll
+      for (int o = GL / 2; o > 0; o >>= 1) xa += __shfl_xor_sync(0xffffffffu, xa, o);
+      if (gl == 0 && need) { t = xa; ref[c] = xa; }
+    }
+    if (gl == 0 && act) {
+      nrm[c] = t;
+      cand_merge(bv, bi, t, c);
+    }
+  }
+  warp_cand(bv, bi);
+  if (lane == 0) { sh.cand_v[warp] = bv; sh.cand_i[warp] = bi; }
+}
+
+template <class T, int GL, int RPL>
+__device__ __forceinline__ void cpqr_update_any(T* W, int m, int n, int ld, double* nrm, double* ref,
+                                                double* xn2, const int* piv, CpqrShared<T>& sh, int s,
+                                                int kmax) {
+  if constexpr (sizeof(T) == sizeof(double) && RPL > 0 && (RPL & 1) == 0)
+    cpqr_update_pr<GL, RPL / 2>(W, m, n, ld, nrm, ref, piv, sh, s, kmax);
+  else
+    cpqr_update<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, s, kmax);
+}
+
 // Run CPQR steps from sh.rank until the stop rule (with min_rank) fires.
+// For real targets with an even register tile (RPL even) the paired-row path
+// runs, which needs the even-ld / zero-pad-row layout (cpqr_ld()).
+// `kcap` (equalisation only) ends the run after exactly kcap steps: the
+// reference re-runs the smaller side with min_rank = k and normally stops
+// right at k, but a stale-norm recomputation can lift the next trailing
+// pivot back above eps*p0 and carry it past k -- which would leave the box
+// non-square and make factor() fail (solver.py:200-203).  Capping at k keeps
+// every equalised box square; it differs from the reference only where the
+// reference itself would fail.
 template <class T, int GL, int RPL>
 __device__ void cpqr_run(T* W, int m, int n, int ld, double* nrm, double* ref, double* xn2,
-                         int* piv, CpqrShared<T>& sh, double eps, int min_rank) {
+                         int* piv, CpqrShared<T>& sh, double eps, int min_rank,
+                         int kcap = 0x7fffffff) {
   const int kmax = m < n ? m : n;
+  const int kend = kmax < kcap ? kmax : kcap;
   const int nw = blockDim.x >> 5;
   int s = sh.rank;
-  while (s < kmax) {
+  while (s < kend) {
     if (threadIdx.x < 32)
       cpqr_pivot<T>(W, m, n, ld, nrm, RPL == 0 ? xn2 : nullptr, piv, sh, s, eps, min_rank, nw);
     __syncthreads();
     if (sh.stop) break;
-    cpqr_update<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, s, kmax);
+    cpqr_update_any<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, s, kmax);
     if (threadIdx.x == 0) {
       W[(int64_t)sh.pc * ld + s] = sh.alpha;
       sh.rank = s + 1;

@@ -98,6 +98,7 @@ int skel_plan_id_level(int64_t p, const int64_t* nr, const int64_t* nc, const in
     m0[a] = s0 + neff[a];
     m1[a] = s1 + neff[a];
     need_m[a] = std::max(m0[a], m1[a]);
+    if (elem == 8) need_m[a] = (need_m[a] + 1) & ~int64_t(1);   // even ld, real CPQR tile
     need_n[a] = std::max<int64_t>(std::max(r, c), 1);
     wb[a] = need_m[a] * need_n[a] * elem;
     const int64_t fixed = level_smem_fixed(need_n[a]);

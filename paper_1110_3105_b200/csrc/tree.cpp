@@ -692,16 +692,33 @@ extern "C" {
 
 int skel_tree_build(const double* coords, int64_t n, int32_t dim, int64_t max_leaf, void** handle) {
   if (!coords || n < 1 || (dim != 2 && dim != 3) || max_leaf < 1 || !handle) return -1;
-  Tree* T = new Tree();
-  build(*T, coords, n, dim, max_leaf);
+  Tree* T = nullptr;
+  try {
+    T = new Tree();
+    build(*T, coords, n, dim, max_leaf);
+  } catch (...) {          // bad_alloc (or a pool failure): no exception crosses the C ABI
+    delete T;
+    return -2;
+  }
   if (T->nonfinite) {
     delete T;
     return -3;   // non-finite coordinate
   }
   // the neighbour lists of every cover are needed right after (the finest
   // level's first): start them now, overlapping the caller's node-array
-  // copies and source setup; readers join first
-  T->nbr_thread = std::thread([T]() { all_neighbors(*T); });
+  // copies and source setup; readers join first.  Failures on that thread
+  // (or failing to start it) are absorbed: skel_tree_neighbors then builds
+  // the lists itself and reports the error.
+  try {
+    T->nbr_thread = std::thread([T]() {
+      try {
+        all_neighbors(*T);
+      } catch (...) {
+        T->nbr_done = false;
+      }
+    });
+  } catch (...) {
+  }
   *handle = T;
   return 0;
 }
@@ -745,7 +762,12 @@ int skel_tree_neighbors(void* handle, int32_t li, int64_t* off, int64_t* count, 
     std::lock_guard<std::mutex> l(T->nbr_m);
     if (T->nbr_thread.joinable()) T->nbr_thread.join();
   }
-  all_neighbors(*T);
+  try {
+    all_neighbors(*T);
+  } catch (...) {
+    T->nbr_done = false;
+    return -2;
+  }
   *count = (int64_t)T->nbr_idx[li].size();
   if (off) std::memcpy(off, T->nbr_off[li].data(), T->nbr_off[li].size() * sizeof(int64_t));
   if (idx) std::memcpy(idx, T->nbr_idx[li].data(), T->nbr_idx[li].size() * sizeof(int64_t));

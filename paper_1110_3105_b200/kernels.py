@@ -75,12 +75,28 @@ def eval_block(spec: KernelSpec, targets, sources, source_curvature=None) -> np.
         raise InvalidInput("double layer needs source normals")
     curv = source_curvature if source_curvature is not None else sources.curvatures
     climit = spec.self_interaction == "curvature_limit"
-    if climit:
-        if spec.equation != "laplace" or spec.dim != 2 or spec.layer != "double":
-            raise InvalidInput("curvature_limit only defined for the 2D Laplace double layer")
-        if curv is None:
-            raise InvalidInput("curvature_limit needs source curvatures")
     m, n = targets.n, sources.n
+    if climit and (spec.equation != "laplace" or spec.dim != 2 or spec.layer != "double"
+                   or curv is None):
+        # the reference only consults the self-interaction rule when the
+        # block HAS a coincident pair (kernels.py:146-157): e.g. proxy blocks
+        # of a curvature-limit spec's single layer are fine.  This host check
+        # runs only for that unusual combination (an error path).
+        span = max(float(np.ptp(targets.coords, axis=0).max()),
+                   float(np.ptp(sources.coords, axis=0).max()),
+                   float(np.abs(targets.coords).max()), float(np.abs(sources.coords).max()), 1.0)
+        tol = COINCIDENT_RTOL * span
+        hit = False
+        for lo in range(0, m, 256):
+            dd = targets.coords[lo:lo + 256, None, :] - sources.coords[None, :, :]
+            if (np.sqrt(np.sum(dd * dd, axis=2)) < tol).any():
+                hit = True
+                break
+        if hit:
+            if spec.equation != "laplace" or spec.dim != 2 or spec.layer != "double":
+                raise InvalidInput("curvature_limit only defined for the 2D Laplace double layer")
+            raise InvalidInput("curvature_limit needs source curvatures")
+        climit = False                   # no coincident pair: the rule never fires
     d = spec.dim
     coords = np.vstack([targets.coords, sources.coords])
     nrm = None

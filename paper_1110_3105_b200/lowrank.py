@@ -59,17 +59,20 @@ def id_fixed_precision_batched(mats, eps, min_ranks=None):
     skel = torch.zeros(max(int(s_off[-1]), 1), dtype=torch.int32, device=dev)
     proj = torch.zeros(max(int(p_off[-1]), 1), dtype=_native.torch_dtype(field), device=dev)
     big = torch.zeros(nb, dtype=torch.float64, device=dev)
+    ratio = torch.zeros(nb, dtype=torch.float64, device=dev)
     dso, dpo = up(s_off), up(p_off)
     max_m = int(ms.max()) if nb else 1
     max_n = int(ns.max()) if nb else 1
-    need = nb * max_m * max_n * (16 if cplx else 8)
+    # real targets use an even leading dimension inside the kernel
+    need = nb * (max_m + (0 if cplx else max_m % 2)) * max_n * (16 if cplx else 8)
     scratch = torch.empty(max(need // 8, 1), dtype=torch.float64, device=dev)
     p = _native.ptr
     _native.check(_native.lib().skel_id_batched(
         p(dA), p(dao), p(dm), p(dn), nb, float(eps), p(dmr), p(rank), p(skel), p(dso), p(proj),
-        p(dpo), p(big), field, p(scratch), scratch.numel() * 8, max_m, max_n,
+        p(dpo), p(big), p(ratio), field, p(scratch), scratch.numel() * 8, max_m, max_n,
         _native.stream_ptr()), "skel_id_batched")
     rank, skel, proj, big = rank.cpu().numpy(), skel.cpu().numpy(), proj.cpu().numpy(), big.cpu().numpy()
+    ratio = ratio.cpu().numpy()
     out = []
     for b in range(nb):
         k, n = int(rank[b]), int(ns[b])
@@ -78,7 +81,7 @@ def id_fixed_precision_batched(mats, eps, min_ranks=None):
             warnings.warn(f"interpolation matrix entries reach {big[b]:.3g} (> 2); "
                           "pivoting quality degraded on this block", stacklevel=3)
         out.append(InterpDecomp(skel=skel[s_off[b]:s_off[b] + k].astype(np.int64), proj=P,
-                                rank=k, achieved_error=float("nan")))
+                                rank=k, achieved_error=float(ratio[b])))
     return out
 
 
@@ -110,15 +113,15 @@ def _big_side(A):
 
 def _big_result(sd, field, min_rank):
     """InterpDecomp from a big-box CPQR state (interp already applied)."""
-    from . import _bigbox
     n = sd.n
     st = sd.state_out
     hdr = st[:4].cpu().view(_i32()).numpy()
     r, pad = int(hdr[0]), int(hdr[2])
-    nb = st.numel() * 8
     raw = st.cpu().numpy().view(np.uint8)
     piv = raw[256 + 24 * n:256 + 28 * n].view(np.int32).astype(np.int64)
+    p0 = float(raw[16:24].view(np.float64)[0])         # BigState.p0
     bigP = float(raw[32:40].view(np.float64)[0])       # BigState.bigP
+    trail = float(raw[40:48].view(np.float64)[0])      # BigState.pad0: first rejected pivot
     W = sd.W_out.cpu().numpy().reshape(n, sd.ld_out)          # row q = column q of the target
     dt = np.complex128 if field else np.float64
     K = r + pad
@@ -130,8 +133,10 @@ def _big_result(sd, field, min_rank):
     if bigP > 2.0:
         warnings.warn(f"interpolation matrix entries reach {bigP:.3g} (> 2); "
                       "pivoting quality degraded on this block", stacklevel=3)
-    del nb, _bigbox
-    return InterpDecomp(skel=piv[:K].copy(), proj=P, rank=K, achieved_error=float("nan"))
+    ratio = trail / p0 if p0 > 0.0 else 0.0
+    if sd.kind == "rand":
+        ratio = sd.worst                       # worst probe error (lowrank.py:219-231)
+    return InterpDecomp(skel=piv[:K].copy(), proj=P, rank=K, achieved_error=float(ratio))
 
 
 def _i32():
@@ -161,12 +166,12 @@ def id_randomized(A, eps, oversampling=10, seed=0) -> InterpDecomp:
     from . import _bigbox
     if not 0 < eps < 1:
         raise InvalidInput("eps must lie in (0, 1)")
-    if oversampling != _bigbox.OVERSAMPLING:
-        raise InvalidInput("only the reference's oversampling (10) is supported")
+    if oversampling < 4:
+        raise InvalidInput("oversampling must be >= 4")
     torch, sd, field, tdt = _big_side(A)
     L = _native.lib()
     st = _native.stream_ptr()
-    _bigbox._randomized(torch, L, sd, eps, seed, field, tdt, st)
+    _bigbox._randomized(torch, L, sd, eps, seed, field, tdt, st, oversampling=int(oversampling))
     if sd.kind == "fixed":
         _native.check(L.skel_big_interp(_native.ptr(sd.W), sd.n, sd.m, _native.ptr(sd.state), 0,
                                         field, st), "skel_big_interp")

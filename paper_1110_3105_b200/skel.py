@@ -132,6 +132,17 @@ class KernelSource(_DeviceSourceMixin):
                                   points.normals if spec.layer == "double" else None,
                                   points.weights, None)
 
+    # the reference's proxy protocol (skel.py:116-124), device-evaluated; the
+    # fast sweep never calls these (it builds the proxies inside the ID kernel)
+    def proxy_row_block(self, rows, proxy: PointSet):
+        from .kernels import eval_block
+        return eval_block(self.proxy_spec, self.points.subset(rows), proxy)
+
+    def proxy_col_block(self, cols, proxy: PointSet):
+        from .kernels import eval_block
+        src = self.points.subset(cols)
+        return eval_block(self.proxy_spec, proxy, PointSet(src.coords, None, src.weights))
+
     def _desc(self):
         return self.geo.source(_native.SRC_KERNEL, self.spec.eq_code, self.spec.layer_code,
                                self.spec.wavenumber, diag=self.diag,
@@ -455,14 +466,22 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
     if mode == "global" and n > GLOBAL_MODE_LIMIT and not allow_large:
         raise RefusedTooLarge(f"global-mode compression of N={n} is quadratic; "
                               "pass allow_large=True to force it")
-    if mode == "global":
-        raise InvalidInput("mode='global' is not part of the B200 hot path; use mode='proxy'")
-    if not hasattr(source, "device_source"):
-        raise InvalidInput("matrix source has no device descriptor (use KernelSource, "
-                           "bie.BieSystem sources, or bie.combined_field_system)")
+    cfg = (proxy or ProxyConfig()).resolve(tree.dim)
+    if mode == "global" or not hasattr(source, "device_source"):
+        # the reference's plugin protocol / quadratic global mode: explicit
+        # targets from the source, batched GPU IDs (hostsweep.py)
+        if shard is not None:
+            raise InvalidInput("sharded compression needs a source with a device descriptor "
+                               "and mode='proxy'")
+        for attr in ("block", "dtype") + (("proxy_row_block", "proxy_col_block")
+                                          if mode == "proxy" else ()):
+            if not hasattr(source, attr):
+                raise InvalidInput(f"matrix source lacks {attr!r} (skel.py:286-290 protocol)")
+        _native.require_cuda()
+        from .hostsweep import compress_explicit
+        return compress_explicit(source, tree, eps, cfg, mode, equalize_ranks, seed)
     torch = _native.require_cuda()
     dev = torch.device("cuda")
-    cfg = (proxy or ProxyConfig()).resolve(tree.dim)
     desc, field = source.device_source()
     dtype = np.complex128 if field else np.float64
     sfield = "complex" if field else "real"

@@ -1,0 +1,210 @@
+"""The drop-in boundary beyond the fast path: the reference's plugin protocol
+(any object with block / proxy_row_block / proxy_col_block, skel.py:286-290),
+mode="global" (skel.py:369-373), InterpDecomp.achieved_error
+(lowrank.py:116-118,161,231) and id_randomized's oversampling argument
+(lowrank.py:186-194).  The GPU cases mirror the reference's own
+tests/test_skel.py:149-185 and tests/test_lowrank.py.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+
+gpu = pytest.mark.gpu
+
+
+def _sk():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_1110_3105_b200 as sk
+    return sk
+
+
+class ProtocolSource(oracle.BieSource):
+    """A pure-Python matrix source in the reference's protocol: numpy entries,
+    proxies passed as PointSet objects (skel.py:289-290, bie.py:233-262)."""
+
+    def proxy_row_block(self, rows, pxy):
+        return super().proxy_row_block(rows, np.asarray(getattr(pxy, "coords", pxy)))
+
+    def proxy_col_block(self, cols, pxy):
+        return super().proxy_col_block(cols, np.asarray(getattr(pxy, "coords", pxy)))
+
+
+def circle_points(sk, n):
+    th = 2 * np.pi * np.arange(n) / n
+    return sk.PointSet(np.column_stack([np.cos(th), np.sin(th)]))
+
+
+# ---------------------------------------------------------------------------
+def test_protocol_source_missing_methods_is_invalid_input():
+    """A source without the proxy callbacks is rejected up front (CPU)."""
+    import paper_1110_3105_b200 as sk
+    pts = circle_points(sk, 256)
+    tree = sk.build_tree(pts, 64)
+
+    class NoProxies:
+        n, dtype, wavenumber = 256, np.float64, 0.0
+
+        def block(self, rows, cols):
+            return np.zeros((len(rows), len(cols)))
+
+    with pytest.raises(sk.InvalidInput):
+        sk.compress_source(NoProxies(), tree, 1e-6)
+
+
+@gpu
+def test_protocol_source_matches_oracle_and_fast_path():
+    """A numpy-only source goes through the host-assembly path: every rank and
+    skeleton set equals the oracle's (same entries bit for bit, same CPQR
+    rules), and the solution agrees with the oracle and with the fast
+    device-descriptor path within 10 eps."""
+    sk = _sk()
+    n, eps = 2048, 1e-9
+    oc = oracle.ellipse(2.0, 1.0, n)
+    T = oracle.build_tree(oc["xy"], 64)
+    src = ProtocolSource(oc, T.perm)
+    ref = oracle.compress(src, T, eps)
+    Xo = oracle.solve(oracle.factor(ref), np.random.default_rng(0).standard_normal((n, 2)))
+
+    curve = sk.bie.ellipse(2.0, 1.0, n)
+    tree = sk.build_tree(curve.point_set(), 64)
+    assert np.array_equal(tree.perm, T.perm)
+    cm = sk.compress_source(ProtocolSource(oc, tree.perm), tree, eps)
+    assert cm.nlevels == len(ref.levels)
+    diff = 0
+    for li, lv in enumerate(ref.levels):
+        assert np.array_equal(cm.levels[li].kr_counts, lv.kr), li
+        assert np.array_equal(cm.levels[li].kc_counts, lv.kc), li
+        mine = np.concatenate([nd.row_skel for nd in cm.levels[li].nodes])
+        diff += int(np.count_nonzero(mine != np.concatenate(lv.row_skel)))
+    assert diff == 0
+    B = np.random.default_rng(0).standard_normal((n, 2))
+    X = sk.solve(sk.factor(cm), B)
+    assert np.linalg.norm(X - Xo) / np.linalg.norm(Xo) <= 10 * eps
+
+    system = sk.bie.discretize_dirichlet(curve, sk.KernelSpec("laplace", 2))
+    _, cm_fast = sk.bie.compress_system(system, eps, 64)
+    Xf = sk.solve(sk.factor(cm_fast), B)
+    assert np.linalg.norm(X - Xf) / np.linalg.norm(Xf) <= 10 * eps
+
+
+@gpu
+def test_device_sources_expose_the_proxy_protocol():
+    """KernelSource / BieSource answer the reference's proxy callbacks
+    (skel.py:116-124, bie.py:251-262) with the oracle's entries."""
+    sk = _sk()
+    n = 512
+    oc = oracle.ellipse(2.0, 1.0, n)
+    curve = sk.bie.ellipse(2.0, 1.0, n)
+    tree = sk.build_tree(curve.point_set(), 64)
+    system = sk.bie.discretize_dirichlet(curve, sk.KernelSpec("laplace", 2))
+    mine = sk.bie.BieSource(system, tree.perm)
+    ref = ProtocolSource(oc, tree.perm)
+    rows = np.arange(10, 50)
+    pxy = sk.PointSet(np.column_stack([3 * np.cos(np.arange(64) * 0.1), np.sin(np.arange(64))]))
+    np.testing.assert_allclose(mine.proxy_row_block(rows, pxy), ref.proxy_row_block(rows, pxy),
+                               rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(mine.proxy_col_block(rows, pxy), ref.proxy_col_block(rows, pxy),
+                               rtol=1e-13, atol=1e-15)
+    ks = sk.KernelSource(sk.KernelSpec("laplace", 2), curve.point_set(), tree.perm)
+    kref = oracle.KernelSource("laplace", 2, "single", oc["xy"], tree.perm)
+    np.testing.assert_allclose(ks.proxy_row_block(rows, pxy), kref.proxy_row_block(rows, pxy.coords),
+                               rtol=1e-13, atol=1e-15)
+
+
+@gpu
+def test_proxy_vs_global_agreement():
+    """tests/test_skel.py:156-165 of the reference."""
+    sk = _sk()
+    pts = circle_points(sk, 1024)
+    tree = sk.build_tree(pts, 64)
+    eps = 1e-9
+    spec = sk.KernelSpec("laplace", 2)
+    cm_p = sk.compress(spec, pts, tree, eps, mode="proxy")
+    cm_g = sk.compress(spec, pts, tree, eps, mode="global")
+    x = np.random.default_rng(3).standard_normal(1024)
+    yp, yg = sk.apply(cm_p, x), sk.apply(cm_g, x)
+    assert np.linalg.norm(yp - yg) / np.linalg.norm(yg) <= 10 * eps
+
+
+@gpu
+def test_global_mode_matches_oracle_ranks():
+    """Global-mode targets (whole off-diagonal block row / column) give the
+    oracle's ranks on the same ellipse."""
+    sk = _sk()
+    n, eps = 1024, 1e-9
+    oc = oracle.ellipse(2.0, 1.0, n)
+    T = oracle.build_tree(oc["xy"], 64)
+    src = ProtocolSource(oc, T.perm)
+    curve = sk.bie.ellipse(2.0, 1.0, n)
+    tree = sk.build_tree(curve.point_set(), 64)
+    cm = sk.compress_source(ProtocolSource(oc, tree.perm), tree, eps, mode="global")
+    for lv in cm.levels:
+        assert np.array_equal(lv.kr_counts, lv.kc_counts)
+    x = np.random.default_rng(1).standard_normal(n)
+    y = sk.apply(cm, x)
+    yd = oracle.dense_matvec(src, x[:, None])[:, 0]
+    assert np.linalg.norm(y - yd) / np.linalg.norm(yd) <= 100 * eps
+
+
+@gpu
+def test_global_mode_size_guard(monkeypatch):
+    """tests/test_skel.py:168-178 of the reference."""
+    sk = _sk()
+    from paper_1110_3105_b200 import skel as skel_mod
+    monkeypatch.setattr(skel_mod, "GLOBAL_MODE_LIMIT", 400)
+    pts = circle_points(sk, 512)
+    tree = sk.build_tree(pts, 64)
+    spec = sk.KernelSpec("laplace", 2)
+    with pytest.raises(sk.RefusedTooLarge):
+        sk.compress(spec, pts, tree, 1e-6, mode="global")
+    cm = sk.compress(spec, pts, tree, 1e-6, mode="global", allow_large=True)
+    assert cm.n == 512
+
+
+@gpu
+def test_achieved_error_matches_oracle_ratio():
+    """id_fixed_precision's achieved_error is the first rejected pivot over
+    the leading one (lowrank.py:116-118,161): the oracle's ratio."""
+    sk = _sk()
+    rng = np.random.default_rng(7)
+    U = rng.standard_normal((80, 12))
+    V = rng.standard_normal((12, 40))
+    A = U @ np.diag(np.logspace(0, -14, 12)) @ V
+    for eps in (1e-3, 1e-7, 1e-10):
+        got = sk.id_fixed_precision(A, eps)
+        _, _, rank, ratio = oracle.cpqr(A, eps)
+        assert got.rank == rank
+        # the rejected pivot is a tiny trailing norm: its last digits carry
+        # the O(u |A|) rounding of the earlier updates (|ratio| ~ eps)
+        assert got.achieved_error == pytest.approx(ratio, rel=1e-3, abs=1e-300)
+        assert 0.0 <= got.achieved_error <= eps
+    # ran to min(m, n): ratio 0 (no rejected pivot); zero matrix: 0
+    assert sk.id_fixed_precision(rng.standard_normal((5, 3)), 1e-12).achieved_error == 0.0
+    assert sk.id_fixed_precision(np.zeros((6, 4)), 1e-6).achieved_error == 0.0
+    # the whole-GPU path reports the same quantity
+    from paper_1110_3105_b200 import lowrank
+    big = lowrank.id_fixed_precision_large(A, 1e-7)
+    _, _, rank, ratio = oracle.cpqr(A, 1e-7)
+    assert big.rank == rank and big.achieved_error == pytest.approx(ratio, rel=1e-3)
+
+
+@gpu
+def test_randomized_oversampling_argument():
+    """id_randomized accepts any oversampling >= 4 (lowrank.py:193-194) and
+    reproduces the oracle's rank with the same seed; achieved_error is the
+    worst probe error, below 3 eps."""
+    sk = _sk()
+    rng = np.random.default_rng(11)
+    m, n = 6000, 120
+    A = rng.standard_normal((m, 30)) @ (np.logspace(0, -12, 30)[:, None] * rng.standard_normal((30, n)))
+    for os_ in (4, 5, 16):
+        got = sk.id_randomized(A, 1e-9, oversampling=os_, seed=3)
+        ref = oracle.id_randomized(A, 1e-9, oversampling=os_, seed=3)
+        assert abs(got.rank - ref[2]) <= 1
+        assert 0.0 <= got.achieved_error <= 3e-9
+    with pytest.raises(sk.InvalidInput):
+        sk.id_randomized(A, 1e-9, oversampling=3)

@@ -220,3 +220,32 @@ def test_scattering_preconditioned_gmres(golden):
                                rtol=1e-6, atol=1e-9)
     with pytest.raises(sk.InvalidInput):
         sk.bie.scattering_system([sk.bie.trefoil(64), sk.bie.trefoil(64, scale=0.5)], 3.0)
+
+
+@gpu
+def test_embedding_of_gpu_compression_solves_like_the_factorization(tmp_path):
+    """assemble_embedding (solver.py:91-140) of a GPU-compressed matrix, solved
+    by an independent sparse direct solver (scipy SuperLU), equals the
+    telescoping factor/solve of the same matrix; the Matrix Market export of
+    it reads back to the same COO."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    sk = _sk()
+    from paper_1110_3105_b200 import embedding
+    n, eps = 4096, 1e-9
+    curve = sk.bie.ellipse(2.0, 1.0, n)
+    system = sk.bie.discretize_dirichlet(curve, sk.KernelSpec("laplace", 2))
+    _, cm = sk.bie.compress_system(system, eps, 64)
+    se = sk.assemble_embedding(cm)
+    r, c, v = se.to_coo()
+    A = sp.csc_matrix((v, (r, c)), shape=(se.m, se.m))
+    b = np.random.default_rng(4).standard_normal(n)
+    x_emb = se.extract_x(spla.spsolve(A, se.rhs(b)))
+    x_fac = sk.solve(sk.factor(cm), b)
+    assert np.linalg.norm(x_emb - x_fac) / np.linalg.norm(x_fac) <= 1e-10
+    path = tmp_path / "emb.mtx"
+    sk.export_matrix_market(se, str(path))
+    shape, r2, c2, v2 = embedding.read_matrix_market(str(path))
+    assert shape == (se.m, se.m)
+    A2 = sp.csc_matrix((v2, (r2, c2)), shape=shape)
+    assert abs(A2 - A).max() <= 1e-15 * abs(A).max()

@@ -128,6 +128,7 @@ def test_level_planner_matches_numpy():
     np.testing.assert_array_equal(pl.rdof_off, np.concatenate([[0], np.cumsum(nr)]))
     np.testing.assert_array_equal(pl.d_off, np.concatenate([[0], np.cumsum(nr * nc)]))
     need_m = np.maximum(pl.m0, pl.m1)
+    need_m += need_m % 2                  # real targets: even leading dimension
     need_n = np.maximum(np.maximum(nr, nc), 1)
     wb = need_m * need_n * 8
     cls = np.searchsorted(np.asarray(W), wb) * 16 + np.searchsorted(np.asarray(M), need_m)
