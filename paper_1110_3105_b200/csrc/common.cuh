@@ -101,6 +101,21 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+// One-instruction bulk prefetch of a contiguous global range into L2 by the
+// TMA unit (cp.async.bulk.prefetch.L2, sm_90+): the range is widened to
+// 16-byte boundaries (its ends may touch a neighbouring block of the same
+// slab, which is harmless for a prefetch) and split in <= 1 MB pieces.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, size_t bytes) {
+  if (bytes == 0) return;
+  uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  while (a < e) {
+    const uint32_t n = (uint32_t)((e - a) < (1u << 20) ? (e - a) : (1u << 20));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a), "r"(n) : "memory");
+    a += n;
+  }
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 

@@ -58,9 +58,13 @@ __device__ __forceinline__ zc sk_unit_phase(zc x0, double a) { return zc(x0.re /
 __device__ __forceinline__ void cand_merge(double& bv, int& bi, double ov, int oi) {
   if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
 }
+// FROM: only lanes that are multiples of FROM hold candidates (column-group
+// leaders), so the butterfly stops there -- log2(32/FROM) dependent shuffle
+// rounds instead of five; lane 0 ends with the warp's first maximum.
+template <int FROM = 1>
 __device__ __forceinline__ void warp_cand(double& bv, int& bi) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = 16; o >= FROM; o >>= 1) {
     double ov = __shfl_xor_sync(0xffffffffu, bv, o);
     int oi = __shfl_xor_sync(0xffffffffu, bi, o);
     cand_merge(bv, bi, ov, oi);
@@ -97,16 +101,14 @@ __device__ void cpqr_pivot(T* W, int m, int n, int ld, double* nrm, double* xn2,
   // lane ends with the first maximum), the stop rule is evaluated uniformly,
   // and the pivot column is known to every lane without a broadcast
   const int lane = threadIdx.x & 31;
+  // every lane merges the (<= 16) per-warp candidates itself: independent
+  // shared-memory loads and a short compare chain, no dependent shuffle
+  // rounds, and the pivot is warp-uniform (the stop decision below is taken
+  // per lane)
   double bv = -1.0;
   int j = 0x7fffffff;
-  if (lane < nw) { bv = sh.cand_v[lane]; j = sh.cand_i[lane]; }
-  // full butterfly: EVERY lane must end with the same pivot (the stop
-  // decision below is taken per lane and must be warp-uniform)
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, j, o);
-    cand_merge(bv, j, ov, oi);
-  }
+#pragma unroll 4
+  for (int w = 0; w < nw; ++w) cand_merge(bv, j, sh.cand_v[w], sh.cand_i[w]);
   int stop = 0;
   double pn = 0.0;
   if (j >= n) {
@@ -232,7 +234,7 @@ __device__ void cpqr_update(T* W, int m, int n, int ld, double* nrm, double* ref
         cand_merge(bv, bi, t, c);
       }
     }
-    warp_cand(bv, bi);
+    warp_cand<GL>(bv, bi);
   } else {
     for (int c = s1 + warp; c < n; c += nw) {
       T* wc = W + (int64_t)piv[c] * ld;
@@ -352,7 +354,7 @@ __device__ void cpqr_update_pr(double* W, int m, int n, int ld, double* nrm, dou
       cand_merge(bv, bi, t, c);
     }
   }
-  warp_cand(bv, bi);
+  warp_cand<GL>(bv, bi);
   if (lane == 0) { sh.cand_v[warp] = bv; sh.cand_i[warp] = bi; }
 }
 

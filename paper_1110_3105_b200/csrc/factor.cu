@@ -25,6 +25,16 @@ __device__ __forceinline__ void cp_async_block_one(T* dst, const T* src) {
     cp_async8(reinterpret_cast<double*>(dst) + w, reinterpret_cast<const double*>(src) + w);
 }
 
+// 1/x correctly rounded (the reciprocal is the only division of a GJ step)
+__device__ __forceinline__ double fac_recip(double x) { return __drcp_rn(x); }
+__device__ __forceinline__ zc fac_recip(zc x) { return zc(1.0) / x; }
+
+// first-maximum merge (ties -> lower index), LAPACK i?amax order
+__device__ __forceinline__ void fac_cmerge(double& bv, int& bi, double ov, int oi) {
+  if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+}
+#define cmerge fac_cmerge
+
 template <class T>
 struct FacShared {
   int status;
@@ -147,6 +157,159 @@ __device__ int sm_invert(T* A, int lda, int p, T* scratch, int* ipiv, FacShared<
   return 0;
 }
 
+// Gauss-Jordan inverse, same pivots and the same per-entry arithmetic as
+// sm_invert (bit-identical result), restructured so no step has a
+// single-warp serial phase:
+//   (1) every thread merges the per-warp pivot candidates of column kk
+//       (written during the previous step's elimination) and forms 1/pivot;
+//   (2) all threads stage the scaled pivot row, the old row kk (it moves to
+//       row pr) and column kk after the exchange;            -- barrier
+//   (3) warp w eliminates rows i = w (mod warps), lanes over columns (the
+//       pivot row in CPL registers per lane), the lane that owns column kk+1
+//       folds the new |a_i,kk+1| (rows > kk) into the warp's candidate for
+//       the next step.                                          -- barrier
+// Two barriers per step as before, but the pivot search rides on the
+// elimination and the row exchange is a staged copy (no warp-0 column scan,
+// no flat (i, j) index walk).  p <= 32 * CPL.
+template <class T, int CPL>
+__device__ int sm_invert_rows(T* A, int lda, int p, T* scratch, int* ipiv, FacShared<T>& sh) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  T* rowp = scratch;
+  T* rowk = scratch + p;
+  T* colk = scratch + 2 * p;
+  {
+    double bv = -1.0;
+    int bi = p;
+    for (int i = tid; i < p; i += nt) cmerge(bv, bi, sk_pivabs(A[(int64_t)i * lda]), i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      cmerge(bv, bi, ov, oi);
+    }
+    if (lane == 0) { sh.red[warp] = bv; sh.red_i[warp] = bi; }
+  }
+  __syncthreads();
+  for (int kk = 0; kk < p; ++kk) {
+    // per-warp candidates: lanes < nw load one each, a log2(nw)-round
+    // butterfly, then lane 0's result is broadcast (warp-uniform pivot)
+    double best = -1.0;
+    int pr = p;
+    if (lane < nw) { best = sh.red[lane]; pr = sh.red_i[lane]; }
+    for (int o = 1; o < nw; o <<= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, pr, o);
+      cmerge(best, pr, ov, oi);
+    }
+    best = __shfl_sync(0xffffffffu, best, 0);
+    pr = __shfl_sync(0xffffffffu, pr, 0);
+    if (!(best > 0.0) || pr >= p) return 1;          // exact zero pivot (uniform)
+    const T inv = fac_recip(A[(int64_t)pr * lda + kk]);
+    const T akk = A[(int64_t)kk * lda + kk];
+    for (int j = tid; j < p; j += nt) {
+      const T vp = A[(int64_t)pr * lda + j];
+      rowp[j] = (j == kk) ? inv : vp * inv;
+      rowk[j] = A[(int64_t)kk * lda + j];
+      colk[j] = (j == pr) ? akk : A[(int64_t)j * lda + kk];
+    }
+    if (tid == 0) ipiv[kk] = pr;
+    __syncthreads();
+    T rp[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int j = lane + 32 * c;
+      rp[c] = j < p ? rowp[j] : T(0.0);
+    }
+    const int jn = kk + 1;
+    double bv = -1.0;
+    int bi = p;
+    for (int i = warp; i < p; i += nw) {
+      T* Ai = A + (int64_t)i * lda;
+      if (i == kk) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int j = lane + 32 * c;
+          if (j < p) Ai[j] = rp[c];
+        }
+        continue;
+      }
+      const T* src = (i == pr) ? rowk : Ai;
+      const T f = colk[i];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int j = lane + 32 * c;
+        if (j < p) {
+          const T a = (j == kk) ? T(0.0) : src[j];
+          Ai[j] = a - f * rp[c];
+        }
+      }
+      // the owner lane of column kk+1 re-reads its own fresh store
+      if (lane == (jn & 31) && jn < p && i > kk) cmerge(bv, bi, sk_pivabs(Ai[jn]), i);
+    }
+    if (jn < p && lane == (jn & 31)) { sh.red[warp] = bv; sh.red_i[warp] = bi; }
+    __syncthreads();
+  }
+  for (int i = tid; i < p; i += nt) {
+    T* Ai = A + (int64_t)i * lda;
+    for (int kk = p - 1; kk >= 0; --kk) {
+      const int pr = ipiv[kk];
+      if (pr != kk) {
+        const T t = Ai[kk];
+        Ai[kk] = Ai[pr];
+        Ai[pr] = t;
+      }
+    }
+  }
+  __syncthreads();
+  return 0;
+}
+
+template <class T>
+__device__ int sm_invert_any(T* A, int lda, int p, T* scratch, int* ipiv, FacShared<T>& sh) {
+  if (p <= 32) return sm_invert_rows<T, 1>(A, lda, p, scratch, ipiv, sh);
+  if (p <= 64) return sm_invert_rows<T, 2>(A, lda, p, scratch, ipiv, sh);
+  if (p <= 96) return sm_invert_rows<T, 3>(A, lda, p, scratch, ipiv, sh);
+  if (p <= 128) return sm_invert_rows<T, 4>(A, lda, p, scratch, ipiv, sh);
+  return sm_invert<T>(A, lda, p, scratch, ipiv, sh);
+}
+
+// C (p x q) = [C -] A (p x r) B (r x q), row-major in shared memory, on the
+// FP64 tensor pipe: each warp owns 8 x 8 output tiles and runs the k-loop as
+// mma.sync.m8n8k4.f64 (A fragment A[i0+g][k0+t], B fragment B[k0+t][j0+g],
+// accumulator C[i0+g][j0+2t .. +1]); edges are zero-filled in the fragment
+// loads, so p, q, r need no padding.
+__device__ __forceinline__ void fac_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <bool SUB>
+__device__ void sm_gemm_dmma(double* C, int ldc, const double* A, int lda, const double* B, int ldb,
+                             int p, int q, int r) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int tp = (p + 7) >> 3, tq = (q + 7) >> 3;
+  for (int tile = warp; tile < tp * tq; tile += nw) {
+    const int i0 = (tile / tq) * 8, j0 = (tile % tq) * 8;
+    const int ia = i0 + g, jb = j0 + g;
+    double d0 = 0.0, d1 = 0.0;
+    const double* ar = A + (int64_t)(ia < p ? ia : 0) * lda;
+    for (int k0 = 0; k0 < r; k0 += 4) {
+      const int k = k0 + t;
+      const double av = (ia < p && k < r) ? ar[k] : 0.0;
+      const double bv = (jb < q && k < r) ? B[(int64_t)k * ldb + jb] : 0.0;
+      fac_dmma(d0, d1, av, bv);
+    }
+    const int jc = j0 + 2 * t;
+    if (ia < p) {
+      double* c = C + (int64_t)ia * ldc;
+      if (jc < q) c[jc] = SUB ? c[jc] - d0 : d0;
+      if (jc + 1 < q) c[jc + 1] = SUB ? c[jc + 1] - d1 : d1;
+    }
+  }
+}
+
 // C (p x q, ldc) = [C -] A (p x r) * B (r x q), row-major, TS x TS register
 // tiles (the caller picks TS so that enough threads get a tile).
 template <class T, bool SUB, int TS>
@@ -186,6 +349,12 @@ __device__ void sm_gemm_t(T* C, int ldc, const T* A, int lda, const T* B, int ld
 template <class T, bool SUB>
 __device__ void sm_gemm(T* C, int ldc, const T* A, int lda, const T* B, int ldb, int p, int q,
                         int r) {
+  if constexpr (sizeof(T) == sizeof(double)) {
+    // real blocks: DMMA (the dense block contractions of solver.py:243-261)
+    sm_gemm_dmma<SUB>(reinterpret_cast<double*>(C), ldc, reinterpret_cast<const double*>(A), lda,
+                      reinterpret_cast<const double*>(B), ldb, p, q, r);
+    return;
+  }
   const int nt = blockDim.x;
   if (((p + 3) >> 2) * ((q + 3) >> 2) >= nt) sm_gemm_t<T, SUB, 4>(C, ldc, A, lda, B, ldb, p, q, r);
   else if (((p + 1) >> 1) * ((q + 1) >> 1) >= nt / 2) sm_gemm_t<T, SUB, 2>(C, ldc, A, lda, B, ldb, p, q, r);
@@ -268,7 +437,7 @@ __global__ void __launch_bounds__(NT, ((NT == 256 && sizeof(T) == sizeof(double)
     __syncthreads();
   }
   double nA = sm_norm1<T>(A, n, n, n, sh);
-  int bad = sm_invert<T>(A, n, n, colk, ipiv, sh);
+  int bad = sm_invert_any<T>(A, n, n, colk, ipiv, sh);
   if (bad) {
     if (threadIdx.x == 0) { F.status[a] = 1; F.rcond_d[a] = 0.0; F.rcond_m[a] = 0.0; }
     return;
@@ -291,7 +460,7 @@ __global__ void __launch_bounds__(NT, ((NT == 256 && sizeof(T) == sizeof(double)
     for (int i = threadIdx.x; i < k; i += blockDim.x) M[(int64_t)i * k + i] += T(F.regularize);
     __syncthreads();
   }
-  bad = sm_invert<T>(M, k, k, colk, ipiv, sh);
+  bad = sm_invert_any<T>(M, k, k, colk, ipiv, sh);
   if (bad) {
     if (threadIdx.x == 0) { F.status[a] = 2; F.rcond_d[a] = rcd; F.rcond_m[a] = 0.0; }
     return;
@@ -359,7 +528,7 @@ __global__ void __launch_bounds__(1024) k_dense_inverse(T* Ag, int K, double reg
     __syncthreads();
   }
   double nA = sm_norm1<T>(A, K, K, K, sh);
-  int bad = sm_invert<T>(A, K, K, colk, ipiv, sh);
+  int bad = sm_invert_any<T>(A, K, K, colk, ipiv, sh);
   if (bad) {
     if (threadIdx.x == 0) { *status = 1; *rcond = 0.0; }
     return;

@@ -549,6 +549,9 @@ def _sweep_work(rec, d, Rn, field, up):
 
 _GRAPH_CACHE = 4
 _GRAPH_MAX_R = 64
+# SKEL_SOLVE_GRAPH=0: never capture / replay (profiling: ncu times every
+# sweep launch of an eager solve, but not kernel nodes of a replayed graph)
+_NO_GRAPH = __import__("os").environ.get("SKEL_SOLVE_GRAPH", "1") == "0"
 
 
 def _device_rhs(fi: FactoredInverse, B):
@@ -604,7 +607,7 @@ def solve_device(fi: FactoredInverse, B, graph: bool = True, _private: bool = Fa
 
 def _solve_graph(fi, B, graph, private, user, weakref):
     torch = _native.require_cuda()
-    if (not graph or _profile.enabled or torch.cuda.is_current_stream_capturing()
+    if (not graph or _NO_GRAPH or _profile.enabled or torch.cuda.is_current_stream_capturing()
             or fi.shard is not None or B.shape[1] > _GRAPH_MAX_R):
         # many RHS: launch overhead is noise next to the sweeps, and the
         # graph's output copy would not be (8.6 GB at 2^20 x 1024)
