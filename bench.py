@@ -254,6 +254,10 @@ def run_ours(args):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         backend = os.environ.get("SKEL_DIST_BACKEND", "nccl")   # gloo: code-path checks only
         if backend == "nccl":
+            # communicator init lines (nRanks, NVLS / P2P transport) on stderr,
+            # so the rank count of the NCCL job is checkable from the logs
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
@@ -501,6 +505,10 @@ def run_ours(args):
                                     f"subtree-sharded factor over {ws} ranks below split level "
                                     f"{cm.shard.split}, replicated above; box-sharded solve"),
                     "levels": cm.nlevels, "S": list(cm.S_shape()),
+                    "collectives": (None if dist is None else
+                                    {"backend": dist.get_backend(), "world": dist.get_world_size(),
+                                     "per_sharded_level": "all_gather(owned kr|kc|flags) + "
+                                                          "all_gather(owned skeleton lists) x2"}),
                     "factor_bytes_per_point": fi.factor_bytes() / n},
             "solve": {"R": R, "nrhs_per_s": n * R / solve_s, "ms": solve_s * 1e3,
                       "solves_per_step": SOLVES_PER_STEP,

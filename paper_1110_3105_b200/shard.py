@@ -8,11 +8,12 @@ one contiguous range per level and every box's children are local.  Per
 level below (and at) the split, each rank compresses and factors only its own
 boxes; the only exchanges are
 
-  * after every sharded level: the per-box ranks (p ints) and the compacted
-    skeleton lists (integer all-reduce, non-owned entries zero) -- neighbour
-    boxes of a rank's boxes may live on another rank;
+  * after every sharded level: the per-box ranks / flags (p ints each) and
+    the compacted skeleton lists -- neighbour boxes of a rank's boxes may
+    live on another rank.  Each is an all_gather of the rank's OWNED
+    contiguous range only (no zero-padded full-size reduction);
   * after the split level: the Lambda blocks of the split cover (the parents
-    above it need them), a float all-reduce of one small slab;
+    above it need them), an all_gather of the owned part of one small slab;
   * in the solve: the split-level vector after the up-sweep and the solution
     rows after the down-sweep.
 
@@ -100,6 +101,21 @@ class ShardPlan:
         bd = self.bounds(off, li)
         lo, hi = bd[self.rank]
         return self.all_gather_var(t[lo:hi], bd, t)
+
+    def gather_boxes(self, t, li, nseg=1):
+        """``t`` holds ``nseg`` consecutive per-box segments over the level-li
+        boxes (e.g. kr | kc | flags); every segment's owned box range is
+        all-gathered into place with ONE collective."""
+        import torch
+        p = t.numel() // nseg
+        v = t.view(nseg, p)
+        bd = [self.box_range(li, q) for q in range(self.world)]
+        b0, b1 = bd[self.rank]
+        local = v[:, b0:b1].t().contiguous()
+        full = torch.empty((p, nseg), dtype=t.dtype, device=t.device)
+        self.all_gather_var(local, bd, full)
+        v.copy_(full.t())
+        return t
 
     def sharded(self, li):
         return li <= self.split

@@ -637,7 +637,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         _ht and _ht.mark("launch")
         join(streams)
         if mine is not None:
-            shard.all_reduce(kk)          # non-owned entries are zero on each rank
+            shard.gather_boxes(kk, li, 3)   # kr | kc | flags of the owned boxes, everywhere
         _ht and _ht.mark("big+join")
         kk_h = kk.cpu().numpy()
         _ht and _ht.mark("kk-wait")
@@ -674,9 +674,9 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             csk = torch.empty(max(int(kco[-1]), 1), dtype=torch.int32, device=dev)
             klen_r, klen_c = t2["kr"], t2["kc"]
         else:
-            # each rank compacts its own boxes' skeletons; the sum over ranks
-            # (one integer all-reduce of both lists) is the full list
-            sk = torch.zeros(max(int(kro[-1]) + int(kco[-1]), 1), dtype=torch.int32, device=dev)
+            # each rank compacts its own boxes' skeletons; all-gathering the
+            # owned ranges of both lists gives every rank the full lists
+            sk = torch.empty(max(int(kro[-1]) + int(kco[-1]), 1), dtype=torch.int32, device=dev)
             rsk, csk = sk[:int(kro[-1])], sk[int(kro[-1]):]
             pk3 = Packer()
             pk3.add("kr", (kr * own).astype(np.int32)).add("kc", (kc * own).astype(np.int32))
@@ -688,7 +688,8 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         _native.check(L.skel_compact_i32(p, p_(t["cdof_off"]), p_(klen_c), p_(t2["kc_off"]),
                                          p_(cskel), p_(csk), st), "skel_compact_i32")
         if mine is not None:
-            shard.all_reduce(sk)
+            shard.gather_rows(rsk, kro, li)
+            shard.gather_rows(csk, kco, li)
         rsk, csk = rsk[:int(kro[-1])], csk[:int(kco[-1])]
         # L is stored nr x kr inside an nr x nr slot, R kc x nc inside nc x nc
         dl = DevLevel(li, nr, nc, kr, kc, d_off, l_off, r_off, Dt, Lt, Rt, rsk, csk, child_off,

@@ -368,7 +368,7 @@ class FactorRun:
             if streams:
                 join(streams)
             if gather_lam:
-                self.shard.all_reduce(Lam)       # the split cover's Lambdas, everywhere
+                self.shard.gather_rows(Lam, lam_off, li)   # the split cover's Lambdas, everywhere
         self.levels.append(((sq_bad, lam_bad, n, k), fl, status, rcd, rcm, dl))
 
     def finish(self, cm):
@@ -379,11 +379,12 @@ class FactorRun:
             torch.cuda.current_stream().wait_event(ev)
         warns = []
         flevels = []
-        for (_, fl, status, rcd, rcm, _) in self.levels:
+        for li, (_, fl, status, rcd, rcm, _) in enumerate(self.levels):
             if fl.mine is not None:
-                self.shard.all_reduce(status, "max")
-                self.shard.all_reduce(rcd, "min")
-                self.shard.all_reduce(rcm, "min")
+                # the owned boxes' status / rcond estimates, everywhere
+                self.shard.gather_boxes(status, li)
+                self.shard.gather_boxes(rcd, li)
+                self.shard.gather_boxes(rcm, li)
         # every level's status / rcond in one device->host copy
         if self.levels:
             cat_s = torch.cat([x[2] for x in self.levels]).cpu().numpy()

@@ -2,7 +2,8 @@
 process per rank, backend gloo).
 
   plan  <out>          CPU only: build the tree, the ShardPlan, check the
-                       ownership invariants across ranks and an all-reduce.
+                       ownership invariants across ranks, the all-reduce and
+                       the owned-range all-gathers.
   solve <out> <n> <eps> GPU: sharded compress -> factor -> solve / apply of
                        the 2D Laplace BIE (every rank on cuda:0 when only
                        one device is visible; the exchange is host-side
@@ -69,6 +70,15 @@ def plan(out):
     sp.gather_rows(v, off, 0)
     want = np.repeat(sp.owners[0], np.diff(off)).astype(np.float64)
     assert np.array_equal(v[:, 0].numpy(), want) and np.array_equal(v[:, 1].numpy(), want)
+    # per-box segments (kr | kc | flags layout): owned ranges gathered in place
+    p1 = covers[1].size
+    kk = torch.full((3 * p1,), -7, dtype=torch.int32)
+    c0, c1 = sp.box_range(1, rank)
+    for sgi in range(3):
+        kk[sgi * p1 + c0:sgi * p1 + c1] = torch.arange(c0, c1, dtype=torch.int32) * 10 + sgi
+    sp.gather_boxes(kk, 1, 3)
+    want = (np.arange(p1)[None, :] * 10 + np.arange(3)[:, None]).reshape(-1)
+    assert np.array_equal(kk.numpy(), want)
     if rank == 0:
         np.savez(out, split=sp.split, owners=own_all, per=per)
     dist.barrier()
