@@ -12,7 +12,8 @@ import re
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libskel_sm100.so")
+# SKEL_LIB: developer A/B of two builds of the same library (tools/); no fallback either way
+LIB_PATH = os.environ.get("SKEL_LIB") or os.path.join(_HERE, "libskel_sm100.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "skel_b200.h")
 
 c_i32 = ctypes.c_int32
