@@ -273,6 +273,227 @@ __device__ int sm_invert_any(T* A, int lda, int p, T* scratch, int* ipiv, FacSha
   return sm_invert<T>(A, lda, p, scratch, ipiv, sh);
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident Gauss-Jordan inverse with panel look-ahead (real blocks,
+// 8-warp CTAs, p <= 32 * RPL and p <= 8 * CW).  Same pivots and the same
+// per-entry arithmetic as sm_invert / sm_invert_rows (a - f * r with the
+// scaled pivot row, 1/pivot by __drcp_rn): the result is bit-identical.
+//
+// Layout: warp w owns the CW contiguous columns [w CW, (w+1) CW), lane l the
+// rows l, l + 32, ...: the whole matrix lives in registers (RPL x CW doubles
+// per thread) for the duration of the inversion.  A Gauss-Jordan step needs,
+// besides a warp's own columns, only the pivot row index and column kk (the
+// multipliers): the warp that owns a panel of CW columns therefore runs its
+// CW steps ALONE, ahead of everybody (pivot search by a warp butterfly, pivot
+// row entries by shuffles: no shared memory, no CTA barrier), publishing per
+// step the pivot row index and the raw column kk; after one barrier the other
+// seven warps replay the CW steps on their own columns.  Two CTA barriers per
+// CW steps instead of two per step, no per-step shared-memory traffic for the
+// matrix, and the row exchange is a register patch on two lanes.
+//   pubf: CW * p doubles (raw column kk of each step of the current panel)
+//   sh.red_i[u]: pivot row of step u; sh.piv_row < 0: exact zero pivot
+// One Gauss-Jordan step on a warp's own columns.  UO >= 0: this warp owns
+// column kk = column slot UO of its tile (compile-time), fr = that column.
+// KS / PS: register slots (row / 32) of rows kk and pr, compile-time so the
+// two special rows are patched with two predicated moves per column (PS < 0:
+// pr == kk, no exchange): row kk <- r, row pr <- old row kk - akk r (the
+// exchange of sm_invert); every other entry is t - f r.
+template <int RPL, int CW, int UO, int KS, int PS>
+__device__ __forceinline__ void gj_la_step_v(double (&t)[RPL][CW], int lane, int kk, int pr,
+                                             const double (&fr)[RPL], double pivv, double akk) {
+  const double inv = fac_recip(pivv);
+  const bool isk = lane == (kk & 31);
+  const bool isp = PS >= 0 && lane == (pr & 31);
+#pragma unroll
+  for (int c = 0; c < CW; ++c) {
+    const double vp = __shfl_sync(0xffffffffu, t[PS >= 0 ? PS : KS][c], pr & 31);   // A[pr][j]
+    const double rp = (c == UO) ? inv : vp * inv;
+    double pv = 0.0;
+    if constexpr (PS >= 0) {
+      double vk = __shfl_sync(0xffffffffu, t[KS][c], kk & 31);                       // A[kk][j]
+      if (c == UO) vk = 0.0;
+      pv = vk - akk * rp;                                      // row pr after the exchange
+    }
+#pragma unroll
+    for (int a = 0; a < RPL; ++a) {
+      const double aa = (c == UO) ? 0.0 : t[a][c];
+      t[a][c] = aa - fr[a] * rp;
+    }
+    if constexpr (PS >= 0) {
+      if (isp) t[PS][c] = pv;
+    }
+    if (isk) t[KS][c] = rp;
+  }
+}
+
+template <int RPL, int CW, int UO>
+__device__ __forceinline__ void gj_la_step(double (&t)[RPL][CW], int lane, int kk, int pr,
+                                           const double (&fr)[RPL], double pivv, double akk) {
+  // kk, pr are CTA-uniform: the slot dispatch is a uniform branch
+  if constexpr (RPL == 1) {
+    if (pr == kk) gj_la_step_v<RPL, CW, UO, 0, -1>(t, lane, kk, pr, fr, pivv, akk);
+    else gj_la_step_v<RPL, CW, UO, 0, 0>(t, lane, kk, pr, fr, pivv, akk);
+  } else {
+    static_assert(RPL <= 2, "slot dispatch covers two row slots");
+    const int ks = kk >> 5, ps = pr >> 5;
+    if (pr == kk) {
+      if (ks == 0) gj_la_step_v<RPL, CW, UO, 0, -1>(t, lane, kk, pr, fr, pivv, akk);
+      else gj_la_step_v<RPL, CW, UO, 1, -1>(t, lane, kk, pr, fr, pivv, akk);
+    } else if (ks == 0) {
+      if (ps == 0) gj_la_step_v<RPL, CW, UO, 0, 0>(t, lane, kk, pr, fr, pivv, akk);
+      else gj_la_step_v<RPL, CW, UO, 0, 1>(t, lane, kk, pr, fr, pivv, akk);
+    } else {
+      // pr >= kk >= 32: both rows live in slot 1
+      gj_la_step_v<RPL, CW, UO, 1, 1>(t, lane, kk, pr, fr, pivv, akk);
+    }
+  }
+}
+
+// Pivot search of one column held one row per (lane, slot): first maximum of
+// |x| over rows kk <= i < p (LAPACK i?amax order), by two 32-bit warp
+// reductions on the bit pattern of |x| (monotone for non-negative doubles)
+// and a ballot for the lowest row.  Returns p when the column is exactly zero
+// (or all NaN, which the comparison-based search never selects either).
+template <int RPL>
+__device__ __forceinline__ int gj_la_pivot(const double (&col)[RPL], int lane, int kk, int p) {
+  unsigned long long key = 0ull;
+  int slot = 0;
+#pragma unroll
+  for (int a = 0; a < RPL; ++a) {
+    const int i = lane + 32 * a;
+    const double v = fabs(col[a]);
+    unsigned long long k = (i >= kk && i < p && v == v) ? (unsigned long long)__double_as_longlong(v) : 0ull;
+    if (k > key) { key = k; slot = a; }
+  }
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  if ((mh | ml) == 0u) return p;
+  const bool hit = hi == mh && lo == ml;
+  int best = p;
+#pragma unroll
+  for (int a = 0; a < RPL; ++a) {
+    const unsigned b = __ballot_sync(0xffffffffu, hit && slot == a);
+    if (best == p && b) best = 32 * a + (__ffs(b) - 1);
+  }
+  return best;
+}
+
+// The panel owner's CW steps, unrolled at compile time (the pivot column of
+// step U is column slot U of the owner's tile).
+template <int RPL, int CW, int U>
+__device__ __forceinline__ void gj_la_owner(double (&t)[RPL][CW], int lane, int kk0, int nst, int p,
+                                            double* pubf, int* ipiv, FacShared<double>& sh) {
+  if constexpr (U < CW) {
+    if (U >= nst) return;
+    const int kk = kk0 + U;
+    double col[RPL];
+#pragma unroll
+    for (int a = 0; a < RPL; ++a) col[a] = t[a][U];
+    const int pr = gj_la_pivot<RPL>(col, lane, kk, p);
+    if (pr >= p) {                                  // exact zero pivot (warp-uniform)
+      if (lane == 0) sh.piv_row = -1;
+      return;
+    }
+#pragma unroll
+    for (int a = 0; a < RPL; ++a) {
+      const int i = lane + 32 * a;
+      if (i < p) pubf[U * p + i] = col[a];
+    }
+    if (lane == 0) { sh.red_i[U] = pr; ipiv[kk] = pr; }
+    // pivot and old diagonal entry of column kk, from their owner lanes
+    double psel = col[0], ksel = col[0];
+#pragma unroll
+    for (int a = 1; a < RPL; ++a) {
+      psel = (a == (pr >> 5)) ? col[a] : psel;
+      ksel = (a == (kk >> 5)) ? col[a] : ksel;
+    }
+    const double pivv = __shfl_sync(0xffffffffu, psel, pr & 31);
+    const double akk = __shfl_sync(0xffffffffu, ksel, kk & 31);
+    gj_la_step<RPL, CW, U>(t, lane, kk, pr, col, pivv, akk);
+    gj_la_owner<RPL, CW, U + 1>(t, lane, kk0, nst, p, pubf, ipiv, sh);
+  }
+}
+
+template <int RPL, int CW>
+__device__ int sm_invert_la(double* A, int lda, int p, double* pubf, int* ipiv, FacShared<double>& sh) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int j0 = warp * CW;
+  double t[RPL][CW];
+#pragma unroll
+  for (int a = 0; a < RPL; ++a) {
+    const int i = lane + 32 * a;
+#pragma unroll
+    for (int c = 0; c < CW; ++c)
+      t[a][c] = (i < p && j0 + c < p) ? A[(int64_t)i * lda + j0 + c] : 0.0;
+  }
+  if (tid == 0) sh.piv_row = 0;
+  __syncthreads();
+  const int npanel = (p + CW - 1) / CW;
+  for (int P = 0; P < npanel; ++P) {
+    const int kk0 = P * CW;
+    const int nst = (p - kk0) < CW ? (p - kk0) : CW;
+    if (warp == P) gj_la_owner<RPL, CW, 0>(t, lane, kk0, nst, p, pubf, ipiv, sh);
+    __syncthreads();
+    if (sh.piv_row < 0) return 1;
+    if (warp != P) {
+      for (int u = 0; u < nst; ++u) {
+        const int kk = kk0 + u;
+        const int pr = sh.red_i[u];
+        const double* fu = pubf + u * p;
+        double fr[RPL];
+#pragma unroll
+        for (int a = 0; a < RPL; ++a) {
+          const int i = lane + 32 * a;
+          fr[a] = i < p ? fu[i] : 0.0;
+        }
+        gj_la_step<RPL, CW, -1>(t, lane, kk, pr, fr, fu[pr], fu[kk]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < RPL; ++a) {
+    const int i = lane + 32 * a;
+#pragma unroll
+    for (int c = 0; c < CW; ++c)
+      if (i < p && j0 + c < p) A[(int64_t)i * lda + j0 + c] = t[a][c];
+  }
+  __syncthreads();
+  // undo the row interchanges as column interchanges, last first
+  for (int i = tid; i < p; i += blockDim.x) {
+    double* Ai = A + (int64_t)i * lda;
+    for (int kk = p - 1; kk >= 0; --kk) {
+      const int pr = ipiv[kk];
+      if (pr != kk) {
+        const double tt = Ai[kk];
+        Ai[kk] = Ai[pr];
+        Ai[pr] = tt;
+      }
+    }
+  }
+  __syncthreads();
+  return 0;
+}
+
+// pub_cap: doubles available at `pub` for the look-ahead path (0 = use the
+// barrier-per-step kernels with the 3p scratch)
+template <class T>
+__device__ int sm_invert_fast(T* A, int lda, int p, T* scratch, T* pub, int64_t pub_cap, int* ipiv,
+                              FacShared<T>& sh) {
+  if constexpr (sizeof(T) == sizeof(double)) {
+    if (blockDim.x == 256) {
+      if (p <= 32 && pub_cap >= 4 * (int64_t)p)
+        return sm_invert_la<1, 4>(reinterpret_cast<double*>(A), lda, p, reinterpret_cast<double*>(pub),
+                                  ipiv, sh);
+      if (p <= 64 && pub_cap >= 8 * (int64_t)p)
+        return sm_invert_la<2, 8>(reinterpret_cast<double*>(A), lda, p, reinterpret_cast<double*>(pub),
+                                  ipiv, sh);
+    }
+  }
+  return sm_invert_any<T>(A, lda, p, scratch, ipiv, sh);
+}
+
 // C (p x q) = [C -] A (p x r) B (r x q), row-major in shared memory, on the
 // FP64 tensor pipe: each warp owns 8 x 8 output tiles and runs the k-loop as
 // mma.sync.m8n8k4.f64 (A fragment A[i0+g][k0+t], B fragment B[k0+t][j0+g],
@@ -368,7 +589,29 @@ __device__ void copy_out(T* dst, const T* src, int64_t cnt) {
 
 template <class T>
 static __host__ __device__ inline size_t fac_elems(int n, int k) {
-  return (size_t)n * n + 4 * (size_t)n * k + (size_t)k * k + 3 * (size_t)n;
+  // A and M are held with odd leading dimensions (n | 1, k | 1: the row-per-
+  // lane register loads of sm_invert_la are then bank-conflict free)
+  return (size_t)n * n + 4 * (size_t)n * k + (size_t)k * k + 4 * (size_t)n + (size_t)k;
+}
+
+// global (contiguous rows of q) <-> shared (row stride ld) block copies
+template <class T>
+__device__ __forceinline__ void cp_async_block_2d(T* dst, int ld, const T* src, int p, int q) {
+  constexpr int W = sizeof(T) / 8;
+  for (int e = threadIdx.x; e < p * q; e += blockDim.x) {
+    const int i = e / q, j = e - i * q;
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      cp_async8(reinterpret_cast<double*>(dst + (int64_t)i * ld + j) + w,
+                reinterpret_cast<const double*>(src + e) + w);
+  }
+}
+template <class T>
+__device__ void copy_out_2d(T* dst, const T* src, int ld, int p, int q) {
+  for (int e = threadIdx.x; e < p * q; e += blockDim.x) {
+    const int i = e / q, j = e - i * q;
+    dst[e] = src[(int64_t)i * ld + j];
+  }
 }
 
 template <class T, bool GW, int NT>
@@ -387,25 +630,26 @@ __global__ void __launch_bounds__(NT, ((NT == 256 && sizeof(T) == sizeof(double)
     if (threadIdx.x == 0) { F.status[a] = 0; F.rcond_d[a] = 1.0; F.rcond_m[a] = 1.0; }
     return;
   }
+  const int lda = n | 1, ldm = k | 1;
   T* A = base;
-  T* Lb = A + (size_t)n * n;
+  T* Lb = A + (size_t)n * lda;
   T* Rb = Lb + (size_t)n * k;
   T* X = Rb + (size_t)k * n;
   T* Y = X + (size_t)n * k;
   T* M = Y + (size_t)k * n;
-  T* colk = M + (size_t)k * k;
+  T* colk = M + (size_t)k * ldm;
 
   const T* D = reinterpret_cast<const T*>(F.D) + F.d_off[a];
   const T* Lg = reinterpret_cast<const T*>(F.L) + F.l_off[a];
   const T* Rg = reinterpret_cast<const T*>(F.R) + F.r_off[a];
   if constexpr (!GW) {
-    cp_async_block<T>(A, D, (int64_t)n * n);
+    cp_async_block_2d<T>(A, lda, D, n, n);
     cp_async_block<T>(Lb, Lg, (int64_t)n * k);
     cp_async_block<T>(Rb, Rg, (int64_t)n * k);
     cp_async_commit();
     cp_async_wait<0>();
   } else {
-    for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) A[e] = D[e];
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) A[(int64_t)(e / n) * lda + e % n] = D[e];
     for (int64_t e = threadIdx.x; e < (int64_t)n * k; e += blockDim.x) {
       Lb[e] = Lg[e];
       Rb[e] = Rg[e];
@@ -421,8 +665,8 @@ __global__ void __launch_bounds__(NT, ((NT == 256 && sizeof(T) == sizeof(double)
       const T* lam = reinterpret_cast<const T*>(F.prev_lam) + F.prev_lam_off[c];
       for (int e = threadIdx.x; e < kc * kc; e += blockDim.x) {
         int i = e / kc, j = e - i * kc;
-        if constexpr (!GW) cp_async_block_one(A + (int64_t)(ro + i) * n + ro + j, lam + e);
-        else A[(int64_t)(ro + i) * n + ro + j] = lam[e];
+        if constexpr (!GW) cp_async_block_one(A + (int64_t)(ro + i) * lda + ro + j, lam + e);
+        else A[(int64_t)(ro + i) * lda + ro + j] = lam[e];
       }
       ro += kc;
     }
@@ -433,48 +677,50 @@ __global__ void __launch_bounds__(NT, ((NT == 256 && sizeof(T) == sizeof(double)
   }
   __syncthreads();
   if (F.regularize != 0.0) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) A[(int64_t)i * n + i] += T(F.regularize);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) A[(int64_t)i * lda + i] += T(F.regularize);
     __syncthreads();
   }
-  double nA = sm_norm1<T>(A, n, n, n, sh);
-  int bad = sm_invert_any<T>(A, n, n, colk, ipiv, sh);
+  double nA = sm_norm1<T>(A, lda, n, n, sh);
+  // look-ahead publication buffer: X is not live before X = D^-1 L
+  int bad = sm_invert_fast<T>(A, lda, n, colk, X, (int64_t)n * k, ipiv, sh);
   if (bad) {
     if (threadIdx.x == 0) { F.status[a] = 1; F.rcond_d[a] = 0.0; F.rcond_m[a] = 0.0; }
     return;
   }
-  double nAi = sm_norm1<T>(A, n, n, n, sh);
+  double nAi = sm_norm1<T>(A, lda, n, n, sh);
   const double rcd = (nA * nAi > 0.0) ? 1.0 / (nA * nAi) : 0.0;
   T* Dd = reinterpret_cast<T*>(F.Dd) + F.dd_off[a];
   if (k == 0) {
-    copy_out<T>(Dd, A, (int64_t)n * n);
+    copy_out_2d<T>(Dd, A, lda, n, n);
     if (threadIdx.x == 0) { F.status[a] = 0; F.rcond_d[a] = rcd; F.rcond_m[a] = 1.0; }
     return;
   }
-  sm_gemm<T, false>(X, k, A, n, Lb, k, n, k, n);    // X = D^-1 L
-  sm_gemm<T, false>(Y, n, Rb, n, A, n, k, n, n);    // Y = R D^-1
+  sm_gemm<T, false>(X, k, A, lda, Lb, k, n, k, n);    // X = D^-1 L
+  sm_gemm<T, false>(Y, n, Rb, n, A, lda, k, n, n);    // Y = R D^-1
   __syncthreads();
-  sm_gemm<T, false>(M, k, Rb, n, X, k, k, k, n);    // M = R X
+  sm_gemm<T, false>(M, ldm, Rb, n, X, k, k, k, n);    // M = R X
   __syncthreads();
-  double nM = sm_norm1<T>(M, k, k, k, sh);
+  double nM = sm_norm1<T>(M, ldm, k, k, sh);
   if (F.regularize != 0.0) {
-    for (int i = threadIdx.x; i < k; i += blockDim.x) M[(int64_t)i * k + i] += T(F.regularize);
+    for (int i = threadIdx.x; i < k; i += blockDim.x) M[(int64_t)i * ldm + i] += T(F.regularize);
     __syncthreads();
   }
-  bad = sm_invert_any<T>(M, k, k, colk, ipiv, sh);
+  // L is dead between X = D^-1 L and Ld = X Lam: its slot is the publication buffer
+  bad = sm_invert_fast<T>(M, ldm, k, colk, Lb, (int64_t)n * k, ipiv, sh);
   if (bad) {
     if (threadIdx.x == 0) { F.status[a] = 2; F.rcond_d[a] = rcd; F.rcond_m[a] = 0.0; }
     return;
   }
-  double nMi = sm_norm1<T>(M, k, k, k, sh);
-  sm_gemm<T, false>(Rb, n, M, k, Y, n, k, n, k);    // Rd = Lam RD
-  sm_gemm<T, false>(Lb, k, X, k, M, k, n, k, k);    // Ld = X Lam
+  double nMi = sm_norm1<T>(M, ldm, k, k, sh);
+  sm_gemm<T, false>(Rb, n, M, ldm, Y, n, k, n, k);    // Rd = Lam RD
+  sm_gemm<T, false>(Lb, k, X, k, M, ldm, n, k, k);    // Ld = X Lam
   __syncthreads();
-  sm_gemm<T, true>(A, n, X, k, Rb, n, n, n, k);     // Dd = D^-1 - X Rd
+  sm_gemm<T, true>(A, lda, X, k, Rb, n, n, n, k);     // Dd = D^-1 - X Rd
   __syncthreads();
-  copy_out<T>(Dd, A, (int64_t)n * n);
+  copy_out_2d<T>(Dd, A, lda, n, n);
   copy_out<T>(reinterpret_cast<T*>(F.Ld) + F.ld_off[a], Lb, (int64_t)n * k);
   copy_out<T>(reinterpret_cast<T*>(F.Rd) + F.rd_off[a], Rb, (int64_t)k * n);
-  copy_out<T>(reinterpret_cast<T*>(F.Lam) + F.lam_off[a], M, (int64_t)k * k);
+  copy_out_2d<T>(reinterpret_cast<T*>(F.Lam) + F.lam_off[a], M, ldm, k, k);
   if (threadIdx.x == 0) {
     F.status[a] = 0;
     F.rcond_d[a] = rcd;

@@ -160,7 +160,7 @@ int skel_plan_factor_level(int64_t p, const int64_t* nr, const int64_t* nc, cons
     lam_off[a + 1] = lam_off[a] + k[a] * k[a];
     noff[a + 1] = noff[a] + n[a];
     koff[a + 1] = koff[a] + k[a];
-    need[a] = (n[a] * n[a] + 4 * n[a] * k[a] + k[a] * k[a] + 3 * n[a]) * elem;
+    need[a] = (n[a] * n[a] + 4 * n[a] * k[a] + k[a] * k[a] + 4 * n[a] + k[a]) * elem;   // fac_elems (factor.cu)
     const bool bg = no >= big_n;
     big[a] = (uint8_t)(no > 0 && bg);
     cls[a] = (no > 0 && !bg) ? lower_bound_idx(fcls, n_fcls, need[a]) : -1;
@@ -173,7 +173,7 @@ int skel_plan_factor_level(int64_t p, const int64_t* nr, const int64_t* nc, cons
   }
   merged[0] = 0;
   if (p <= small_level && any_fit &&
-      (fn * fn + 4 * fn * fk + fk * fk + 3 * fn) * elem + 1024 + 4 * fn <= optin) {
+      (fn * fn + 4 * fn * fk + fk * fk + 4 * fn + fk) * elem + 1024 + 4 * fn <= optin) {
     bool first = false;
     for (int64_t a = 0; a < p; ++a) {
       const bool fits = cls[a] >= 0 && need[a] + 1024 + 4 * n[a] <= optin;

@@ -339,7 +339,7 @@ class FactorRun:
                 max_k = int(k[sel].max())
                 if merged is not None and bi == 0:
                     max_n, max_k = merged
-                nd = (max_n * max_n + 4 * max_n * max_k + max_k * max_k + 3 * max_n) * elem
+                nd = (max_n * max_n + 4 * max_n * max_k + max_k * max_k + 4 * max_n + max_k) * elem   # fac_elems (factor.cu)
                 F.order, F.nrun = p_(t[f"order{bi}"]), sel.size
                 F.scratch, F.scratch_bytes = None, 0
                 if nd + 1024 + 4 * max_n > optin:

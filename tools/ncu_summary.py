@@ -29,3 +29,6 @@ for row in r[2:]:
     top = sorted(st.items(), key=lambda x: -x[1])[:6]
     print(d.get('ID'), d.get('Kernel Name', '')[:30], 'stalls/issue:', ', '.join(f"{k}={v:.2f}" for k, v in top),
           '| dram bytes', d.get('dram__bytes_read.sum'), d.get('dram__bytes_write.sum'))
+    extra = {k: v for k, v in d.items() if any(t in k for t in ('pipe_fp64', 'smsp__inst_executed.sum', 'bank_conflicts', 'sm__inst_executed_pipe_fp64', 'pipe_shared_cycles', 'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum', 'smsp__thread_inst_executed_per_inst_executed'))}
+    for k, v in sorted(extra.items()):
+        print(f"      {k} = {v}")
