@@ -240,9 +240,40 @@ def compress_system(system: BieSystem, eps, max_leaf_size=None, proxy: ProxyConf
 
 def solve_dirichlet(system: BieSystem, rhs, eps, max_leaf_size=None, shard=None):
     """compress, factor, solve (bie.py:275-279).  Returns (density, cm, fi)."""
+    pre = _prefetch_rhs(system, rhs)
     _, cm = compress_system(system, eps, max_leaf_size, shard=shard)
     fi = factor(cm)
+    if pre is not None and pre[0].dtype == _native.torch_dtype(int(fi.dtype == np.complex128)):
+        from .solver import solve_device
+        torch = _native.require_cuda()
+        torch.cuda.current_stream().wait_event(pre[1])
+        x = _native.to_host(solve_device(fi, pre[0], _private=True))
+        return (x[:, 0] if np.ndim(rhs) == 1 else x), cm, fi
     return solve(fi, rhs), cm, fi
+
+
+def _prefetch_rhs(system, rhs):
+    """A page-locked host RHS is copied to the device on a side stream while
+    the system is compressed and factored (the solve needs it only at the
+    very end); returns (device tensor, copy event) or None for anything else
+    (pageable memory, other dtypes or layouts: ``solve`` handles those)."""
+    if not isinstance(rhs, np.ndarray) or rhs.dtype not in (np.float64, np.complex128):
+        return None
+    if rhs.ndim not in (1, 2) or rhs.shape[0] != system.points.coords.shape[0] or not rhs.flags.c_contiguous:
+        return None
+    torch = _native.require_cuda()
+    h = torch.from_numpy(rhs.reshape(rhs.shape[0], -1))
+    if not h.is_pinned():
+        return None
+    from ._staging import side_streams
+    s = side_streams(1, "rhs")[0]
+    with torch.cuda.stream(s):
+        d = torch.empty(h.shape, dtype=h.dtype, device="cuda")
+        d.copy_(h, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+    d.record_stream(torch.cuda.current_stream())
+    return d, ev
 
 
 def dense_matvec(source, x):

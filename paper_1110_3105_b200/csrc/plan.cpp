@@ -47,19 +47,50 @@ int buckets_by_class(int64_t p, const int64_t* cls, const int64_t* key, int32_t*
   for (int64_t a = 0; a < p; ++a)
     if (cls[a] >= 0) order[pos[cls[a]]++] = (int32_t)a;
   int nb = 0;
-  std::vector<uint64_t> tmp;
+  // within a class: descending key, ties by position.  `order` is in position
+  // order already (stable counting sort above), so a stable LSD radix sort on
+  // d = kmax - key gives exactly that order (a comparison sort of the 30k-box
+  // finest levels cost ~1 ms of GPU-idle host time per level)
+  std::vector<uint32_t> d, d2;
+  std::vector<int32_t> o2;
   for (int64_t c = 0; c <= cmax; ++c) {
     const int64_t s = cnt[c], e = cnt[c + 1];
     if (e == s) continue;
     bstart[nb++] = (int32_t)s;
-    if (key && e - s > 1) {
-      int64_t kmax = 0;
-      for (int64_t i = s; i < e; ++i) kmax = std::max(kmax, key[order[i]]);
-      tmp.resize(e - s);
-      for (int64_t i = s; i < e; ++i)
-        tmp[i - s] = ((uint64_t)(kmax - key[order[i]]) << 32) | (uint32_t)order[i];
-      std::sort(tmp.begin(), tmp.end());
-      for (int64_t i = s; i < e; ++i) order[i] = (int32_t)(tmp[i - s] & 0xffffffffu);
+    const int64_t m = e - s;
+    if (key && m > 1) {
+      int64_t kmax = key[order[s]], kmin = kmax;
+      for (int64_t i = s; i < e; ++i) {
+        kmax = std::max(kmax, key[order[i]]);
+        kmin = std::min(kmin, key[order[i]]);
+      }
+      const uint64_t span = (uint64_t)(kmax - kmin);
+      if (span == 0) continue;
+      if (span >> 32) {                       // huge keys: comparison sort
+        std::vector<uint64_t> tmp(m);
+        std::stable_sort(order + s, order + e,
+                         [&](int32_t a, int32_t b) { return key[a] > key[b]; });
+        continue;
+      }
+      d.resize(m); d2.resize(m); o2.resize(m);
+      for (int64_t i = 0; i < m; ++i) d[i] = (uint32_t)(kmax - key[order[s + i]]);
+      int32_t* oa = order + s;
+      int32_t* ob = o2.data();
+      uint32_t* da = d.data();
+      uint32_t* db = d2.data();
+      for (int shift = 0; shift < 32 && (span >> shift); shift += 11) {
+        int64_t hist[2049] = {0};
+        for (int64_t i = 0; i < m; ++i) hist[((da[i] >> shift) & 2047u) + 1]++;
+        for (int b = 0; b < 2048; ++b) hist[b + 1] += hist[b];
+        for (int64_t i = 0; i < m; ++i) {
+          const int64_t q = hist[(da[i] >> shift) & 2047u]++;
+          ob[q] = oa[i];
+          db[q] = da[i];
+        }
+        std::swap(oa, ob);
+        std::swap(da, db);
+      }
+      if (oa != order + s) std::memcpy(order + s, oa, sizeof(int32_t) * m);
     }
   }
   bstart[nb] = (int32_t)cnt[cmax + 1];

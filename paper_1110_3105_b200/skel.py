@@ -436,6 +436,15 @@ def _level_geometry(tree, li, cfg, dim, k_wave):
                            n_unit=unit.shape[0], child_off=child_off, t=pk.upload())
 
 
+def _frozen(a):
+    """Read-only view: the tree, the compressed matrix and the factorization
+    share ONE permutation array instead of 8 N-byte copies per step (the
+    reference copies; nobody writes to it afterwards)."""
+    v = a.view()
+    v.flags.writeable = False
+    return v
+
+
 def _segment_sum(vals, off):
     cs = np.concatenate([[0], np.cumsum(vals)])
     return cs[off[1:]] - cs[off[:-1]]
@@ -565,6 +574,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             own_idx = np.nonzero(mine)[0].astype(np.int32)
             pk.add("own", own_idx)
         t = pk.upload()
+        _ht and _ht.mark("pack.upload")
         tg = geo.t
         Dt = torch.empty(max(int(d_off[-1]), 1), dtype=tdt, device=dev)
         Lt = torch.empty(max(int(l_off[-1]), 1), dtype=tdt, device=dev)
@@ -572,6 +582,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         rskel = torch.empty(max(int(rdof_off[-1]), 1), dtype=torch.int32, device=dev)
         cskel = torch.empty(max(int(cdof_off[-1]), 1), dtype=torch.int32, device=dev)
         kk = torch.zeros(3 * p, dtype=torch.int32, device=dev)     # kr | kc | flags
+        _ht and _ht.mark("pack.alloc")
         lvd = _native.SkelLevel()
         lvd.nbox, lvd.level, lvd.equalize, lvd.n_unit = p, li, int(bool(equalize_ranks)), geo.n_unit
         lvd.eps = float(eps)
@@ -655,6 +666,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             warnings.warn(f"interpolation matrix entries reach > 2 on {bad.size} block(s) at "
                           f"level {li} (first node {bad[0]}); pivoting quality degraded",
                           stacklevel=2)
+        _ht and _ht.mark("post.flags")
         # the sorted skeletons, compacted, are the next level's dof lists
         kro, kco = _off(kr), _off(kc)
         pk2 = Packer()
@@ -669,6 +681,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         t2["_buffer0"] = t["_buffer"]
         t2["_buffer_geo"] = tg["_buffer"]
         t2["_kk"] = kk
+        _ht and _ht.mark("post.upload")
         if mine is None:
             rsk = torch.empty(max(int(kro[-1]), 1), dtype=torch.int32, device=dev)
             csk = torch.empty(max(int(kco[-1]), 1), dtype=torch.int32, device=dev)
@@ -691,6 +704,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
             shard.gather_rows(rsk, kro, li)
             shard.gather_rows(csk, kco, li)
         rsk, csk = rsk[:int(kro[-1])], csk[:int(kco[-1])]
+        _ht and _ht.mark("post.compact")
         # L is stored nr x kr inside an nr x nr slot, R kc x nc inside nc x nc
         dl = DevLevel(li, nr, nc, kr, kc, d_off, l_off, r_off, Dt, Lt, Rt, rsk, csk, child_off,
                       dtype, t=t2, mine=mine)
@@ -720,7 +734,7 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
         cbox = up(np.repeat(np.arange(last.p), last.kc).astype(np.int32))
         _native.check(L.skel_assemble_S(desc, p_(last.rskel), p_(rbox), Kr, p_(last.cskel),
                                         p_(cbox), Kc, p_(S), field, st), "skel_assemble_S")
-    cm = CompressedMatrix(levels, None, n, eps, tree.perm.copy(), sfield, tree, S_dev=S)
+    cm = CompressedMatrix(levels, None, n, eps, _frozen(tree.perm), sfield, tree, S_dev=S)
     cm._eager = run
     cm.shard = shard
     return cm

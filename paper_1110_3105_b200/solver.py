@@ -18,7 +18,7 @@ from . import _native, _profile
 from .errors import InvalidInput, SingularBlock
 from ._plan import plan_factor_level
 from ._staging import Packer, fork, join, on_stream, size_buckets
-from .skel import CompressedMatrix, _dense_apply, _nullctx, _off
+from .skel import CompressedMatrix, _dense_apply, _frozen, _nullctx, _off
 
 _RCOND_WARN = 1e-14
 _BIG_FAC_N = 768          # boxes at least this wide are factored over the whole GPU
@@ -433,7 +433,7 @@ class FactorRun:
         status, _ = _invert_top(Sinv, self.regularize, self.field)
         if status:
             raise SingularBlock("top", 0, "S")
-        return FactoredInverse(flevels, Sh, Sinv, cm.n, cm.perm.copy(), cm.scalar_field, warns,
+        return FactoredInverse(flevels, Sh, Sinv, cm.n, _frozen(cm.perm), cm.scalar_field, warns,
                                shard=self.shard)
 
 

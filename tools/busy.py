@@ -24,14 +24,26 @@ iv = sorted((e0.elapsed_time(r.start), e0.elapsed_time(r.end), r.kind) for r in 
             if r.kind != "level")
 busy, cs, ce = 0.0, None, None
 per = {}
+gaps = []
 for a, b, k in iv:
     per[k] = per.get(k, 0.0) + (b - a)
     if cs is None or a > ce:
         if cs is not None:
             busy += ce - cs
+            gaps.append((ce, a - ce))
+        else:
+            gaps.append((0.0, a))
         cs, ce = a, b
     else:
         ce = max(ce, b)
 busy += ce - cs
 print(f"span {span:.1f} ms  GPU busy (union of kernels) {busy:.1f} ms  ({100 * busy / span:.0f}%)")
 print("  per kind (sum of launch durations, overlapping):", {k: round(v, 1) for k, v in per.items()})
+gaps.append((ce, span - ce))
+lev = sorted((e0.elapsed_time(r.start), r.meta.get("level")) for r in _profile.records if r.kind == "id_level")
+first = {}
+for tt, l in lev:
+    first.setdefault(l, tt)
+print("  first id_level launch per level (ms):", {l: round(t, 2) for l, t in sorted(first.items())})
+print("  idle gaps >= 0.15 ms (start ms, length ms):", [(round(a, 2), round(g, 2)) for a, g in gaps if g >= 0.15])
+print("  idle total %.1f ms in %d gaps" % (sum(g for _, g in gaps), len(gaps)))
