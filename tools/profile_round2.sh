@@ -18,7 +18,9 @@ SKEL_SOLVE_GRAPH=0 ncu -f --set full --import-source on --clock-control none -k 
     -o /tmp/ncu/sweep python tools/solvebench.py 1048576 16 1 > /tmp/ncu/sweep.log 2>&1
 SKEL_SOLVE_GRAPH=0 ncu -f --set full --import-source on --clock-control none -k regex:k_level_dmma_pipe --launch-skip 110 --launch-count 1 \
     -o /tmp/ncu/sweep1024 python tools/solvebench.py 1048576 1024 1 > /tmp/ncu/sweep1024.log 2>&1
-for r in id fac sweep sweep1024; do
+ncu -f --set full --import-source on --clock-control none -k regex:k_id_level --launch-skip 14 --launch-count 1 \
+    -o /tmp/ncu/idbig python tools/compress_once.py > /tmp/ncu/idbig.log 2>&1
+for r in id idbig fac sweep sweep1024; do
   python tools/ncu_summary.py /tmp/ncu/$r.ncu-rep > $O/${T}_ncu_${r}.txt 2>&1
   python tools/ncu_lines.py /tmp/ncu/$r.ncu-rep 30 > $O/${T}_ncu_${r}_lines.txt 2>&1
 done

@@ -1,6 +1,6 @@
 """Per-kernel SASS opcode counts of the built library (static instruction
 counts, not executed): DMMA (FP64 tensor pipe), DFMA/DADD/DMUL (FP64 CUDA
-cores), UTMALDG/UBLKCP (TMA), LDGSTS (cp.async), LDS/STS, BAR, SHFL.
+cores), UTMALDG/UBLKCP/UBLKPF (TMA copy / bulk L2 prefetch), CREDUX (warp reductions), LDGSTS (cp.async), LDS/STS, BAR, SHFL.
 
     python tools/sass_counts.py [lib.so] > profiles/rNN_sass_counts.txt
 """
@@ -9,7 +9,7 @@ import collections, os, re, subprocess, sys  # noqa: E401
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 lib = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "paper_1110_3105_b200", "libskel_sm100.so")
 txt = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True, check=True).stdout
-OPS = ["DMMA", "DFMA", "DADD", "DMUL", "UTMALDG", "UBLKCP", "SYNCS", "LDGSTS", "LDG", "STG", "LDS", "STS",
+OPS = ["DMMA", "DFMA", "DADD", "DMUL", "UTMALDG", "UBLKCP", "UBLKPF", "CREDUX", "SYNCS", "LDGSTS", "LDG", "STG", "LDS", "STS",
        "BAR", "SHFL", "MUFU"]
 cur, counts = None, collections.OrderedDict()
 for line in txt.splitlines():
