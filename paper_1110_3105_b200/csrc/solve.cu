@@ -357,6 +357,185 @@ __global__ void __launch_bounds__(256) k_level_dmma_few(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Few-RHS sweep with the factor blocks staged by the TMA unit (1-D bulk
+// copies).  Row-major blocks make the 8 rows of a warp's output tile ONE
+// contiguous chunk of A (8 q doubles) and one of B (8 r doubles): lane 0 of
+// the warp arms a warp-private mbarrier with the byte count and issues two
+// cp.async.bulk copies into the warp's shared-memory buffer (SASS UBLKCP);
+// the whole tile's factor bytes are then in flight at once without holding
+// registers, and the A fragments come from shared memory.  The X / Y slab is
+// staged as in k_level_dmma_few while the bulk copies fly.  Chunks start on
+// 8-byte boundaries: a misaligned chunk is fetched from the 16-byte boundary
+// below it (`lead` = 1 double of the previous row / block, inside the slab)
+// and an odd trailing double comes by a plain load, so no copy reads past
+// the slab.  Same DMMA schedule and arithmetic as k_level_dmma_few.
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(b))
+               : "memory");
+}
+
+// one chunk (cnt doubles at g, 8-byte aligned) -> dst (16-byte aligned);
+// returns the bytes the bulk copy will deliver; dst[lead + i] = g[i]
+__device__ __forceinline__ unsigned bulk_chunk(double* dst, const double* g, int cnt, uint64_t* b,
+                                               bool issue) {
+  const int lead = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);
+  const int total = lead + cnt;
+  const unsigned bytes = (unsigned)(total & ~1) * 8u;
+  if (issue && bytes) bulk_g2s(dst, g - lead, bytes, b);
+  return bytes;
+}
+
+template <int NT, bool ROWS>
+__global__ void __launch_bounds__(256) k_level_bulk_few(
+    const int32_t* __restrict__ pp, const int32_t* __restrict__ qq, const int32_t* __restrict__ rr,
+    const int64_t* __restrict__ a_off, const double* __restrict__ A,
+    const int64_t* __restrict__ b_off, const double* __restrict__ Bm,
+    const int64_t* __restrict__ x_off, const double* __restrict__ X,
+    const int64_t* __restrict__ y_off, const double* __restrict__ Y,
+    const int64_t* __restrict__ o_off, double* __restrict__ O, int R,
+    const int32_t* __restrict__ order, const int64_t* __restrict__ xrows,
+    const int64_t* __restrict__ orows, int buf_doubles) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int CW = 8 * NT, LDX = CW + 8;
+  const int a = order ? order[blockIdx.x] : blockIdx.x;
+  const int p = pp[a], q = qq[a], r = rr ? rr[a] : 0;
+  if (p == 0) return;
+  const int Qp = (q + 3) & ~3, Rp = (r + 3) & ~3, Kp = Qp + Rp;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem) + warp;
+  double* wbuf = reinterpret_cast<double*>(smem + 64) + (size_t)warp * buf_doubles;
+  double* sX = reinterpret_cast<double*>(smem + 64) + (size_t)nw * buf_doubles;
+  if (lane == 0) mbar_init(mbar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncwarp();
+  const double* Ab = A + a_off[a];
+  const double* Bb = r ? Bm + b_off[a] : nullptr;
+  const int ntile = (p + 7) >> 3;
+  // issue tile rt's copies (lane 0); every lane gets the chunk geometry
+  double tail_v = 0.0;
+  int tail_i = -1;
+  auto stage = [&](int rt, int& lead_a, int& off_b, int& lead_b) {
+    const int row0 = rt * 8, rows = (p - row0) < 8 ? (p - row0) : 8;
+    const double* ga = Ab + (int64_t)row0 * q;
+    lead_a = (int)((reinterpret_cast<uintptr_t>(ga) >> 3) & 1);
+    off_b = (lead_a + rows * q + 1) & ~1;
+    lead_b = 0;
+    const double* gb = nullptr;
+    if (r) {
+      gb = Bb + (int64_t)row0 * r;
+      lead_b = (int)((reinterpret_cast<uintptr_t>(gb) >> 3) & 1);
+    }
+    if (lane == 0) {
+      unsigned bytes = bulk_chunk(wbuf, ga, rows * q, mbar, false);
+      if (r) bytes += bulk_chunk(wbuf + off_b, gb, rows * r, mbar, false);
+      mbar_expect_tx(mbar, bytes);
+      bulk_chunk(wbuf, ga, rows * q, mbar, true);
+      if (r) bulk_chunk(wbuf + off_b, gb, rows * r, mbar, true);
+    }
+    // odd trailing doubles come by plain loads: lane 1 (A) and lane 2 (B)
+    // fetch them now and store them just before the tile is consumed
+    tail_v = 0.0;
+    tail_i = -1;
+    if (lane == 1 && ((lead_a + rows * q) & 1)) {
+      tail_i = lead_a + rows * q - 1;
+      tail_v = __ldg(ga + rows * q - 1);
+    }
+    if (lane == 2 && r && ((lead_b + rows * r) & 1)) {
+      tail_i = off_b + lead_b + rows * r - 1;
+      tail_v = __ldg(gb + rows * r - 1);
+    }
+  };
+  int lead_a = 0, off_b = 0, lead_b = 0;
+  if (warp < ntile) stage(warp, lead_a, off_b, lead_b);
+  const int64_t* xr = (ROWS && xrows) ? xrows + x_off[a] : nullptr;
+  const int64_t* orw = (ROWS && orows) ? orows + o_off[a] : nullptr;
+  constexpr int CP = CW / 2;
+  for (int e = tid; e < Kp * CP; e += nt) {
+    const int j = e / CP, c = 2 * (e - j * CP);
+    double* d = sX + j * LDX + c;
+    const double* src = nullptr;
+    if (j < q) src = (xr ? X + xr[j] * R : X + (x_off[a] + j) * R) + c;
+    else if (j >= Qp && j - Qp < r) src = Y + (y_off[a] + (j - Qp)) * R + c;
+    if (src && c + 1 < R && !(reinterpret_cast<uintptr_t>(src) & 15)) {
+      cp_async16(d, src);
+    } else {
+      d[0] = (src && c < R) ? __ldg(src) : 0.0;
+      d[1] = (src && c + 1 < R) ? __ldg(src + 1) : 0.0;
+    }
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const int g = lane >> 2, t4 = lane & 3;
+  unsigned phase = 0;
+  for (int rt = warp; rt < ntile; rt += nw) {
+    if (tail_i >= 0) wbuf[tail_i] = tail_v;
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    __syncwarp();
+    const int row = rt * 8 + g;
+    const bool ok = row < p;
+    double acc[NT][2];
+#pragma unroll
+    for (int u = 0; u < NT; ++u) acc[u][0] = acc[u][1] = 0.0;
+    const double* arow = wbuf + lead_a + (ok ? g : 0) * q;
+    const double* xs = sX + t4 * LDX + g;
+#pragma unroll 4
+    for (int k0 = 0; k0 < Qp; k0 += 4) {
+      const double av = (ok && k0 + t4 < q) ? arow[k0 + t4] : 0.0;
+#pragma unroll
+      for (int u = 0; u < NT; ++u) dmma884(acc[u][0], acc[u][1], av, xs[k0 * LDX + u * 8]);
+    }
+    if (r) {
+      const double* brow = wbuf + off_b + lead_b + (ok ? g : 0) * r;
+      const double* ys = xs + Qp * LDX;
+#pragma unroll 4
+      for (int k0 = 0; k0 < Rp; k0 += 4) {
+        const double bv = (ok && k0 + t4 < r) ? brow[k0 + t4] : 0.0;
+#pragma unroll
+        for (int u = 0; u < NT; ++u) dmma884(acc[u][0], acc[u][1], bv, ys[k0 * LDX + u * 8]);
+      }
+    }
+    __syncwarp();                       // every lane is done with the buffer
+    if (rt + nw < ntile) stage(rt + nw, lead_a, off_b, lead_b);
+    if (ok) {
+      double* orow = orw ? O + orw[row] * R : O + (o_off[a] + row) * R;
+#pragma unroll
+      for (int u = 0; u < NT; ++u) {
+        const int col = u * 8 + 2 * t4;
+        if (col + 1 < R && !(R & 1)) {
+          *reinterpret_cast<double2*>(orow + col) = make_double2(acc[u][0], acc[u][1]);
+        } else {
+          if (col < R) orow[col] = acc[u][0];
+          if (col + 1 < R) orow[col + 1] = acc[u][1];
+        }
+      }
+    }
+  }
+}
+
 // Pipelined DMMA variant for many RHS.  One CTA per (box, column range);
 // [A | B] is staged in shared memory once (row stride = 4 mod 16 doubles, so
 // an A-fragment load is conflict-free).  A warp task is up to MT 8-row tiles
@@ -513,6 +692,18 @@ static int dmma_many_mode() {
   return mode;
 }
 
+// TMA-staged few-RHS sweeps: measured at N = 2^20 against the direct-load
+// kernel, R = 1 / 4: -6 % / -8 % (on top of its L2 prefetch), R = 16: +4 %,
+// R = 32: -1 %.  Default: <= 8 RHS.  SKEL_SOLVE_BULK=0 / 1 forces it off / on
+// for every width (A/B runs).
+static bool bulk_few_enabled(int nt) {
+  static const int mode = [] {
+    const char* e = std::getenv("SKEL_SOLVE_BULK");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  return mode < 0 ? nt == 1 : mode == 1;
+}
+
 static bool dmma_few_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("SKEL_SOLVE_DMMA_FEW");
@@ -588,6 +779,21 @@ static int level_gemm(int nbox, const int32_t* p, const int32_t* q, const int32_
                                             (double*)O, R, order, xrows, orows);
           return skel_last_error();
         };
+        // TMA-staged variant: factor blocks by 1-D bulk copies into warp buffers
+        const int bufd = (8 * (max_q + max_r) + 4 + 1) & ~1;
+        const size_t bsmem = 64 + ((size_t)(threads / 32) * bufd + (size_t)kmax * (8 * nt + 8)) * sizeof(double);
+        if (bulk_few_enabled(nt) && bsmem <= optin) {
+          auto blaunch = [&](auto kern) -> int {
+            SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
+            kern<<<nbox, threads, bsmem, st>>>(p, q, r, a_off, (const double*)A, b_off, (const double*)B,
+                                               x_off, (const double*)X, y_off, (const double*)Y, o_off,
+                                               (double*)O, R, order, xrows, orows, bufd);
+            return skel_last_error();
+          };
+          if (nt == 1) return rows ? blaunch(k_level_bulk_few<1, true>) : blaunch(k_level_bulk_few<1, false>);
+          if (nt == 2) return rows ? blaunch(k_level_bulk_few<2, true>) : blaunch(k_level_bulk_few<2, false>);
+          return rows ? blaunch(k_level_bulk_few<4, true>) : blaunch(k_level_bulk_few<4, false>);
+        }
         if (nt == 1) return rows ? launch(k_level_dmma_few<1, true>) : launch(k_level_dmma_few<1, false>);
         if (nt == 2) return rows ? launch(k_level_dmma_few<2, true>) : launch(k_level_dmma_few<2, false>);
         return rows ? launch(k_level_dmma_few<4, true>) : launch(k_level_dmma_few<4, false>);

@@ -639,8 +639,13 @@ def compress_source(source, tree: OrthTree, eps, proxy: ProxyConfig | None = Non
                                   bool(equalize_ranks), seed, field)
         # host work overlapped with this level's ID kernels: the next level's
         # geometry and the deferred factor launch of the previous level
+        # (all remaining levels' geometry while the finest level's kernels run:
+        # that is the longest GPU stretch, and at the coarse levels -- a few
+        # hundred microseconds of kernel time each -- the host is the chain)
+        if li == 0:
+            geo_ahead = {l: _level_geometry(tree, l, cfg, dim, k_wave) for l in range(1, top_run)}
         if li + 1 < top_run:
-            geo_next = _level_geometry(tree, li + 1, cfg, dim, k_wave)
+            geo_next = geo_ahead.pop(li + 1)
         if pending is not None:
             run.stream.wait_event(pending[2])
             run.add_level(pending[0], pending[1])

@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
-timeout 300 python tools/solvebench.py 1048576 16,4,1,32 20 > gpurun_out/solve_new.log 2>&1; echo "rc=$?"; grep "^R=" gpurun_out/solve_new.log
-SKEL_LIB=$PWD/tools/ab/libskel_head.so timeout 300 python tools/solvebench.py 1048576 16,4,1,32 20 > gpurun_out/solve_head.log 2>&1; echo "rc=$?"; grep "^R=" gpurun_out/solve_head.log
+SKEL_SOLVE_BULK=1 timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_formats.py -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
+for b in 1 0; do
+SKEL_SOLVE_BULK=$b timeout 300 python tools/solvebench.py 1048576 16,4,1,32 20 > gpurun_out/solve_bulk$b.log 2>&1; echo "bulk=$b rc=$?"; grep "^R=" gpurun_out/solve_bulk$b.log
+done
