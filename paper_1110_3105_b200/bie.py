@@ -232,10 +232,46 @@ def compress_system(system: BieSystem, eps, max_leaf_size=None, proxy: ProxyConf
                     mode="proxy", seed=0, shard=None):
     """Tree over the curve nodes + GPU skeletonization (bie.py:265-272).
     ``shard`` (extension): see compress_source."""
-    tree = build_tree(system.points, max_leaf_size)
+    up = _upload_beside(system)
+    try:
+        tree = build_tree(system.points, max_leaf_size)
+    except BaseException:
+        up(False)                           # the tree's error wins
+        raise
+    up()
     cm = compress_source(BieSource(system, tree.perm), tree, eps, proxy=proxy, mode=mode,
                          seed=seed, shard=shard)
     return tree, cm
+
+
+def _upload_beside(system):
+    """Start the one-time upload of the system's geometry (host copies into
+    the pinned staging block + one async H2D copy) on a helper thread, so it
+    runs beside the native tree build instead of after it; returns the join
+    function (re-raises what the upload raised).  Both sides are a handful of
+    long GIL-free calls, unlike the per-level launch work."""
+    if getattr(system, "_res", 0) is not None or not hasattr(system, "resident"):
+        return lambda reraise=True: None
+    import threading
+    torch = _native.require_cuda()
+    dev = torch.cuda.current_device()
+    err = []
+
+    def work():
+        try:
+            torch.cuda.set_device(dev)      # the CUDA current device is per host thread
+            system.resident()
+        except BaseException as e:          # noqa: BLE001 -- re-raised by join()
+            err.append(e)
+
+    th = threading.Thread(target=work, name="skel-geometry-upload")
+    th.start()
+
+    def join(reraise=True):
+        th.join()
+        if err and reraise:
+            raise err[0]
+    return join
 
 
 def solve_dirichlet(system: BieSystem, rhs, eps, max_leaf_size=None, shard=None):
