@@ -300,6 +300,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
   __syncthreads();
   if (L.debug_skip == 2) { if (tid == 0) (side == 0 ? L.kr : L.kc)[a] = 0; return; }
   cpqr_run<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, L.eps, 0);
+  if (L.debug_skip == 4) { if (tid == 0) (side == 0 ? L.kr : L.kc)[a] = 0; return; }
   int min_rank = 0;
   if (eq) {
     cg::cluster_group cl = cg::this_cluster();
@@ -315,7 +316,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
       cpqr_run<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, L.eps, k, k);
     }
   }
+  if (L.debug_skip == 5) { if (tid == 0) (side == 0 ? L.kr : L.kc)[a] = 0; return; }
   interp_solve<T>(W, n, ld, piv, sh, min_rank, hd.red);
+  if (L.debug_skip == 6) { if (tid == 0) (side == 0 ? L.kr : L.kc)[a] = 0; return; }
   const int r = sh.rank;
   const int K = r + sh.pad;
   for (int s = tid; s < K; s += nt) {

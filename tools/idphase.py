@@ -1,5 +1,6 @@
 """Developer probe: phase breakdown of the level-0 k_id_level launches at config 2
-(debug_skip 3 = launch only, 1 = + K1 assembly, 2 = + initial norms, 0 = whole kernel),
+(debug_skip 3 = launch only, 1 = + K1 assembly, 2 = + initial norms, 4 = + CPQR, 5 = + equalisation run,
+6 = + interpolation solve, 0 = whole kernel),
 per bucket, from CUDA-event records.
 
     python tools/idphase.py
@@ -18,7 +19,8 @@ tree = sk.build_tree(system.points, 64)
 src = sk.bie.BieSource(system, tree.perm)
 skel._DEBUG_MAX_LEVELS[0] = 1
 res = {}
-for skip in (3, 1, 2, 0):
+ORDER = (3, 1, 2, 4, 5, 6, 0)
+for skip in ORDER:
     skel._DEBUG_SKIP[0] = skip
     for r in range(2):
         skel.compress_source(src, tree, 1e-12, eager_factor=False)
@@ -28,7 +30,7 @@ for skip in (3, 1, 2, 0):
     _profile.enabled = False
     res[skip] = [(r.meta.get("max_m"), r.meta.get("max_n"), r.meta["sel"].size if "sel" in r.meta else 0, r.ms())
                  for r in _profile.records if r.kind == "id_level"]
-print("bucket (max_m, max_n, boxes): launch-only / +assembly / +norms / all  [ms]")
+print("bucket (max_m, max_n, boxes): launch-only / +assembly / +norms / +cpqr / +equalise / +interp / all  [ms]")
 for i, b in enumerate(res[0]):
-    print(b[:3], " ".join(f"{res[s][i][3]:8.3f}" for s in (3, 1, 2, 0)))
-print("sum", " ".join(f"{sum(x[3] for x in res[s]):8.3f}" for s in (3, 1, 2, 0)))
+    print(b[:3], " ".join(f"{res[s][i][3]:8.3f}" for s in ORDER))
+print("sum", " ".join(f"{sum(x[3] for x in res[s]):8.3f}" for s in ORDER))
