@@ -173,6 +173,21 @@ int skel_id_batched(const void* A, const int64_t* a_off, const int32_t* m,
                     int64_t scratch_bytes, int32_t max_m, int32_t max_n,
                     void* stream);
 
+/* pivoted_qr (lowrank.py:48-119) for a batch: the same CPQR as skel_id_batched,
+ * returning per matrix the WHOLE pivot permutation (piv: n[b] entries at
+ * piv_off[b]), rank[b] = the completed CPQR steps (no min_rank padding), and
+ * the rank x n upper-trapezoidal factor R with its columns in pivot order
+ * (row-major at rfac_off[b]; capacity min(m,n) x n).  proj / bigP / ratio as
+ * for skel_id_batched (proj capacity n x n per matrix). */
+int skel_pivoted_qr_batched(const void* A, const int64_t* a_off, const int32_t* m,
+                            const int32_t* n, int32_t nmat, double eps,
+                            const int32_t* min_rank, int32_t* rank, int32_t* piv,
+                            const int64_t* piv_off, void* rfac, const int64_t* rfac_off,
+                            void* proj, const int64_t* proj_off, double* bigP,
+                            double* ratio, int32_t field, void* scratch,
+                            int64_t scratch_bytes, int32_t max_m, int32_t max_n,
+                            void* stream);
+
 /* ---- telescoping factorization (solver.py:187-276) --------------------- */
 
 typedef struct {

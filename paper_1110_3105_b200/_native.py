@@ -78,6 +78,8 @@ _SIGS = {
     "skel_eval_block": [_P(SkelSource), c_vp, c_i32, c_vp, c_i32, c_vp, c_i32, c_vp],
     "skel_id_batched": [c_vp, c_vp, c_vp, c_vp, c_i32, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp,
                         c_vp, c_vp, c_vp, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp],
+    "skel_pivoted_qr_batched": [c_vp, c_vp, c_vp, c_vp, c_i32, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp],
     "skel_factor_level": [_P(SkelFactorLevel), c_i32, c_i32, c_i32, c_vp],
     "skel_dense_inverse": [c_vp, c_vp, c_vp, c_i32, c_f64, c_vp, c_vp, c_i32, c_vp, c_vp],
     "skel_sweep_up_ex": [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32,
@@ -130,6 +132,7 @@ _lib = None
 
 # entry points that launch kernels (the tree builder / queries run on the host)
 _LAUNCHING = {"skel_id_level", "skel_assemble_D", "skel_assemble_S", "skel_eval_block", "skel_id_batched",
+              "skel_pivoted_qr_batched",
               "skel_factor_level", "skel_dense_inverse", "skel_sweep_up_ex",
               "skel_sweep_down_ex", "skel_dense_apply", "skel_permute_rows",
               "skel_compact_i32", "skel_dense_matvec", "skel_fp64_probe", "skel_big_target",

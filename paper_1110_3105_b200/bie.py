@@ -19,6 +19,13 @@ from .skel import ProxyConfig, _DeviceSourceMixin, compress_source
 from .solver import factor, solve
 
 QUAD_RULES = ("plain_trapezoid", "kapur_rokhlin_10")
+# Kapur-Rokhlin 10th-order endpoint corrections gamma_1..gamma_10 (bie.py:31-42);
+# the kernels hold the same table as c_kr10 (csrc/entries.cuh)
+KR10_GAMMA = np.array([
+    7.832432020568779e+00, -4.565161670374749e+01, 1.452168846354677e+02,
+    -2.901348302886379e+02, 3.870862162579900e+02, -3.523821383570681e+02,
+    2.172421547519342e+02, -8.707796087382991e+01, 2.053584266072635e+01,
+    -2.166984103403823e+00])
 
 
 @dataclass

@@ -52,6 +52,22 @@ int skel_id_batched(const void* A, const int64_t* a_off, const int32_t* m, const
                        proj_off, bigP, ratio, scratch, scratch_bytes, max_m, max_n, st);
 }
 
+int skel_pivoted_qr_batched(const void* A, const int64_t* a_off, const int32_t* m, const int32_t* n,
+                            int32_t nmat, double eps, const int32_t* min_rank, int32_t* rank,
+                            int32_t* piv, const int64_t* piv_off, void* rfac, const int64_t* rfac_off,
+                            void* proj, const int64_t* proj_off, double* bigP, double* ratio,
+                            int32_t field, void* scratch, int64_t scratch_bytes, int32_t max_m,
+                            int32_t max_n, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!rfac || !rfac_off) return -1;
+  if (field == 0)
+    return id_batched_impl<double>(A, a_off, m, n, nmat, eps, min_rank, rank, piv, piv_off, proj,
+                                   proj_off, bigP, ratio, scratch, scratch_bytes, max_m, max_n, st,
+                                   rfac, rfac_off);
+  return id_batched_zc(A, a_off, m, n, nmat, eps, min_rank, rank, piv, piv_off, proj, proj_off,
+                       bigP, ratio, scratch, scratch_bytes, max_m, max_n, st, rfac, rfac_off);
+}
+
 int skel_assemble_S(const SkelSource* src, const int32_t* rows, const int32_t* rbox, int32_t Kr,
                     const int32_t* cols, const int32_t* cbox, int32_t Kc, void* S, int32_t field,
                     void* stream) {

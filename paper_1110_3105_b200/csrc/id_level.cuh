@@ -424,7 +424,8 @@ __global__ void __launch_bounds__(128)
     k_id_batched(const T* __restrict__ A, const int64_t* a_off, const int32_t* mm,
                  const int32_t* nn, double eps, const int32_t* min_rank_arr, int32_t* rank_out,
                  int32_t* skel_out, const int64_t* skel_off, T* proj, const int64_t* proj_off,
-                 double* bigP_out, double* ratio_out, T* scratch, int max_m, int max_n) {
+                 double* bigP_out, double* ratio_out, T* scratch, int max_m, int max_n, T* rfac,
+                 const int64_t* rfac_off) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* p = smem;
   CpqrShared<T>& sh = *reinterpret_cast<CpqrShared<T>*>(p);
@@ -452,17 +453,29 @@ __global__ void __launch_bounds__(128)
   cpqr_init<T>(W, m, n, ld, nrm, ref, xn2, piv, sh);
   __syncthreads();
   cpqr_run<T, GL, RPL>(W, m, n, ld, nrm, ref, xn2, piv, sh, eps, min_rank);
+  if (rfac) {
+    // pivoted_qr (lowrank.py:48-119): the rank x n upper-trapezoidal factor with
+    // columns in pivot order, taken before the interpolation solve overwrites R12
+    T* Rf = rfac + rfac_off[b];
+    const int rr = sh.rank;
+    for (int e = tid; e < rr * n; e += nt) {
+      const int s = e / n, q = e - s * n;
+      Rf[e] = q >= s ? W[(int64_t)piv[q] * ld + s] : T(0.0);
+    }
+    __syncthreads();
+  }
   interp_solve<T>(W, n, ld, piv, sh, min_rank, red);
   const int r = sh.rank, K = r + sh.pad;
   int32_t* sk = skel_out + skel_off[b];
-  for (int s = tid; s < K; s += nt) sk[s] = piv[s];
+  // with the R factor requested the whole pivot permutation is returned
+  for (int s = tid; s < (rfac ? n : K); s += nt) sk[s] = piv[s];
   T* P = proj + proj_off[b];
   for (int e = tid; e < n * K; e += nt) {
     int s = e / n, q = e - s * n;
     P[(int64_t)s * n + piv[q]] = interp_entry<T>(W, ld, piv, r, K, s, q);
   }
   if (tid == 0) {
-    rank_out[b] = K;
+    rank_out[b] = rfac ? r : K;     // pivoted_qr reports the completed CPQR steps
     bigP_out[b] = sh.bigP;
     if (ratio_out) ratio_out[b] = sh.p0 > 0.0 ? sh.trail / sh.p0 : 0.0;
   }
@@ -616,11 +629,13 @@ static int launch_id_batched(const void* A, const int64_t* a_off, const int32_t*
                              const int32_t* n, int nmat, double eps, const int32_t* min_rank,
                              int32_t* rank, int32_t* skel, const int64_t* skel_off, void* proj,
                              const int64_t* proj_off, double* bigP, double* ratio, void* scratch,
-                             int max_m, int max_n, size_t smem, cudaStream_t st) {
+                             int max_m, int max_n, size_t smem, cudaStream_t st, void* rfac,
+                             const int64_t* rfac_off) {
   auto kern = k_id_batched<T, GL, RPL, GW>;
   SKEL_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<nmat, 128, smem, st>>>((const T*)A, a_off, m, n, eps, min_rank, rank, skel, skel_off,
-                                (T*)proj, proj_off, bigP, ratio, (T*)scratch, max_m, max_n);
+                                (T*)proj, proj_off, bigP, ratio, (T*)scratch, max_m, max_n,
+                                (T*)rfac, rfac_off);
   return skel_last_error();
 }
 
@@ -629,7 +644,8 @@ static int id_batched_impl(const void* A, const int64_t* a_off, const int32_t* m
                            int nmat, double eps, const int32_t* min_rank, int32_t* rank,
                            int32_t* skel, const int64_t* skel_off, void* proj,
                            const int64_t* proj_off, double* bigP, double* ratio, void* scratch,
-                           int64_t scratch_bytes, int max_m, int max_n, cudaStream_t st) {
+                           int64_t scratch_bytes, int max_m, int max_n, cudaStream_t st,
+                           void* rfac = nullptr, const int64_t* rfac_off = nullptr) {
   if (nmat <= 0) return 0;
   if (max_m < 1) max_m = 1;
   if (max_n < 1) max_n = 1;
@@ -641,14 +657,15 @@ static int id_batched_impl(const void* A, const int64_t* a_off, const int32_t* m
     if (max_m <= 128)
       return launch_id_batched<T, 8, 16, false>(A, a_off, m, n, nmat, eps, min_rank, rank, skel,
                                                 skel_off, proj, proj_off, bigP, ratio, scratch, max_m, max_n,
-                                                fixed + wbytes, st);
+                                                fixed + wbytes, st, rfac, rfac_off);
     return launch_id_batched<T, 32, 0, false>(A, a_off, m, n, nmat, eps, min_rank, rank, skel,
                                           skel_off, proj, proj_off, bigP, ratio, scratch, max_m, max_n,
-                                          fixed + wbytes, st);
+                                          fixed + wbytes, st, rfac, rfac_off);
   }
   if (!scratch || (size_t)scratch_bytes < (size_t)nmat * wbytes) return -2;
   return launch_id_batched<T, 32, 0, true>(A, a_off, m, n, nmat, eps, min_rank, rank, skel, skel_off,
-                                       proj, proj_off, bigP, ratio, scratch, max_m, max_n, fixed, st);
+                                       proj, proj_off, bigP, ratio, scratch, max_m, max_n, fixed, st, rfac,
+                                       rfac_off);
 }
 
 // complex (field 1) instantiations live in id_level_z.cu (a second
@@ -659,4 +676,4 @@ int id_batched_zc(const void* A, const int64_t* a_off, const int32_t* m, const i
                   double eps, const int32_t* min_rank, int32_t* rank, int32_t* skel,
                   const int64_t* skel_off, void* proj, const int64_t* proj_off, double* bigP,
                   double* ratio, void* scratch, int64_t scratch_bytes, int max_m, int max_n,
-                  cudaStream_t st);
+                  cudaStream_t st, void* rfac = nullptr, const int64_t* rfac_off = nullptr);

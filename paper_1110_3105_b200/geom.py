@@ -227,3 +227,71 @@ def level_neighbors(tree: OrthTree, level: int) -> list:
     """Adjacency lists of cover ``level`` (geom.py:205-219), native O(p)."""
     off, idx = tree.cover_neighbors(level)
     return [idx[off[a]:off[a + 1]].tolist() for a in range(off.size - 1)]
+
+
+# ---------------------------------------------------------------------------
+# point-set files (geom.py:225-277): the text and "SKPT" binary layouts
+
+ROOT_PAD = 1e-12          # relative root-box padding (geom.py:133-147), applied in csrc/tree.cpp
+_SKPT = b"SKPT"
+_SKPT_HEAD = "<IBB"       # N, dim, flags (bit 0: normals, bit 1: weights)
+
+
+def _columns(dim, has_normals, has_weights):
+    return dim * (2 if has_normals else 1) + (1 if has_weights else 0)
+
+
+def read_points_text(path, dim, has_normals=False, has_weights=False) -> PointSet:
+    """One point per row, whitespace separated: coordinates, then (optionally)
+    the normal, then (optionally) the weight (geom.py:225-241)."""
+    table = np.loadtxt(path, dtype=np.float64, ndmin=2)
+    ncol = _columns(dim, has_normals, has_weights)
+    if table.shape[1] != ncol:
+        raise InvalidInput(f"expected {ncol} columns, found {table.shape[1]}")
+    parts = np.split(table, [dim, 2 * dim] if has_normals else [dim], axis=1)
+    coords = parts[0]
+    normals = parts[1] if has_normals else None
+    weights = parts[-1][:, 0] if has_weights else None
+    return PointSet(coords, normals, weights)
+
+
+def write_points_text(ps: PointSet, path):
+    """Inverse of read_points_text, 17 significant digits (round-trip exact)."""
+    blocks = [a for a in (ps.coords, ps.normals) if a is not None]
+    if ps.weights is not None:
+        blocks.append(np.asarray(ps.weights).reshape(-1, 1))
+    np.savetxt(path, np.concatenate(blocks, axis=1), fmt="%.17g")
+
+
+def write_points_binary(ps: PointSet, path):
+    """"SKPT", u32 N, u8 dim, u8 flags, then little-endian float64 coordinates
+    (row-major), normals, weights (geom.py:250-263)."""
+    import struct
+    flags = int(ps.normals is not None) | (int(ps.weights is not None) << 1)
+    with open(path, "wb") as fh:
+        fh.write(_SKPT + struct.pack(_SKPT_HEAD, ps.n, ps.dim, flags))
+        for a in (ps.coords, ps.normals, ps.weights):
+            if a is not None:
+                fh.write(np.ascontiguousarray(a, dtype="<f8").tobytes())
+
+
+def read_points_binary(path) -> PointSet:
+    import struct
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    hs = struct.calcsize(_SKPT_HEAD)
+    if blob[:4] != _SKPT or len(blob) < 4 + hs:
+        raise InvalidInput(f"{path}: not a skelkit binary point file")
+    n, dim, flags = struct.unpack_from(_SKPT_HEAD, blob, 4)
+    shapes = [(n, dim)] + ([(n, dim)] if flags & 1 else []) + ([(n,)] if flags & 2 else [])
+    pos, arrays = 4 + hs, []
+    for shp in shapes:
+        cnt = int(np.prod(shp))
+        if pos + 8 * cnt > len(blob):
+            raise InvalidInput(f"{path}: truncated point file")
+        arrays.append(np.frombuffer(blob, dtype="<f8", count=cnt, offset=pos).reshape(shp).copy())
+        pos += 8 * cnt
+    coords = arrays.pop(0)
+    normals = arrays.pop(0) if flags & 1 else None
+    weights = arrays.pop(0) if flags & 2 else None
+    return PointSet(coords, normals, weights)

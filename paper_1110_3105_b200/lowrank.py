@@ -97,6 +97,48 @@ def id_rows(A, eps, min_rank=0) -> InterpDecomp:
     return id_fixed_precision(np.asarray(A).T, eps, min_rank=min_rank)
 
 
+def pivoted_qr(A, eps, min_rank=0):
+    """Column-pivoted Householder QR stopped at relative pivot size eps, but not
+    before min_rank columns (lowrank.py:48-119), on the GPU (the CPQR of
+    csrc/cpqr.cuh through ``skel_pivoted_qr_batched``).
+
+    Returns (piv, R, rank, trailing_ratio) as the reference does: the whole
+    pivot permutation, the rank x n upper-trapezoidal factor with its columns
+    in pivot order, the number of completed steps and the first rejected pivot
+    magnitude over the leading one."""
+    torch = _native.require_cuda()
+    A = _as_matrix(A)
+    m, n = A.shape
+    cplx = A.dtype.kind == "c"
+    dt = np.complex128 if cplx else np.float64
+    if m == 0 or n == 0:
+        return np.arange(n), np.zeros((0, n), dtype=dt), 0, 0.0
+    field = int(cplx)
+    dev = torch.device("cuda")
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    tdt = _native.torch_dtype(field)
+    dA = up(np.asarray(A, dtype=dt).ravel(order="F"))
+    zero = up(np.zeros(1, dtype=np.int64))
+    dm, dn = up(np.array([m], np.int32)), up(np.array([n], np.int32))
+    dmr = up(np.array([min_rank], np.int32))
+    rank = torch.zeros(1, dtype=torch.int32, device=dev)
+    piv = torch.zeros(n, dtype=torch.int32, device=dev)
+    rfac = torch.zeros(min(m, n) * n, dtype=tdt, device=dev)
+    proj = torch.zeros(n * n, dtype=tdt, device=dev)
+    big = torch.zeros(1, dtype=torch.float64, device=dev)
+    ratio = torch.zeros(1, dtype=torch.float64, device=dev)
+    need = (m + (0 if cplx else m % 2)) * n * (16 if cplx else 8)
+    scratch = torch.empty(max(need // 8, 1), dtype=torch.float64, device=dev)
+    p = _native.ptr
+    _native.check(_native.lib().skel_pivoted_qr_batched(
+        p(dA), p(zero), p(dm), p(dn), 1, float(eps), p(dmr), p(rank), p(piv), p(zero), p(rfac),
+        p(zero), p(proj), p(zero), p(big), p(ratio), field, p(scratch), scratch.numel() * 8, m, n,
+        _native.stream_ptr()), "skel_pivoted_qr_batched")
+    r = int(rank.cpu()[0])
+    R = rfac.cpu().numpy()[:r * n].reshape(r, n).astype(dt)
+    return piv.cpu().numpy().astype(np.int64), R, r, float(ratio.cpu()[0])
+
+
 def _big_side(A):
     """Upload an explicit matrix as a big-box side (column-major target)."""
     from . import _bigbox

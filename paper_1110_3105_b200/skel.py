@@ -892,3 +892,17 @@ def _dense_apply(M, x, field):
     elif K:
         y.zero_()
     return y
+
+
+# The reference keeps the SKLC container next to the data model
+# (skel.py:428-511); here it lives in container.py and is re-exported lazily
+# (container.py imports this module).
+_CONTAINER_NAMES = ("serialize_compressed", "deserialize_compressed", "save_compressed",
+                    "load_compressed")
+
+
+def __getattr__(name):
+    if name in _CONTAINER_NAMES:
+        from . import container
+        return getattr(container, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

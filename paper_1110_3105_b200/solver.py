@@ -712,3 +712,24 @@ def _solve_device_eager(fi: FactoredInverse, B):
     X = torch.empty_like(xt)
     _native.check(L.skel_permute_rows(p_(perm), fi.n, p_(xt), p_(X), Rn, 1, field, st), "permute")
     return X
+
+
+# Names the reference defines in solver.py (sparse embedding + Matrix Market
+# solver.py:91-140,414-433; GMRES 321-408; SKLC factorization files 439-529)
+# live in embedding.py / krylov.py / container.py here; re-exported lazily
+# (those modules import this one).
+_ELSEWHERE = {
+    "SparseEmbedding": "embedding", "assemble_embedding": "embedding",
+    "export_matrix_market": "embedding", "read_matrix_market": "embedding",
+    "gmres": "krylov",
+    "serialize_factored": "container", "deserialize_factored": "container",
+    "save_factored": "container", "load_factored": "container",
+}
+
+
+def __getattr__(name):
+    mod = _ELSEWHERE.get(name)
+    if mod is not None:
+        import importlib
+        return getattr(importlib.import_module(f"{__package__}.{mod}"), name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

@@ -208,3 +208,101 @@ def test_randomized_oversampling_argument():
         assert 0.0 <= got.achieved_error <= 3e-9
     with pytest.raises(sk.InvalidInput):
         sk.id_randomized(A, 1e-9, oversampling=3)
+
+
+# ---------------------------------------------------------------------------
+# module paths: every public name a reference user imports from a submodule
+# (`from skelkit.solver import gmres`, `from skelkit.skel import load_compressed` ...)
+# resolves at the same submodule here
+
+REFERENCE_MODULE_NAMES = {
+    "geom": ["PointSet", "TreeNode", "OrthTree", "build_tree", "neighbors", "level_neighbors",
+             "read_points_text", "write_points_text", "read_points_binary", "write_points_binary",
+             "ROOT_PAD"],
+    "kernels": ["KernelSpec", "eval_block", "bessel_h0"],
+    "lowrank": ["InterpDecomp", "pivoted_qr", "id_fixed_precision", "id_rows", "id_randomized"],
+    "skel": ["ProxyConfig", "KernelSource", "CompressedNode", "CompressedLevel", "CompressedMatrix",
+             "compress", "compress_source", "apply", "serialize_compressed", "deserialize_compressed",
+             "save_compressed", "load_compressed", "GLOBAL_MODE_LIMIT"],
+    "solver": ["FactoredNode", "FactoredInverse", "factor", "solve", "gmres", "SparseEmbedding",
+               "assemble_embedding", "export_matrix_market", "read_matrix_market",
+               "serialize_factored", "deserialize_factored", "save_factored", "load_factored"],
+    "bie": ["Curve2D", "ellipse", "trefoil", "BieSystem", "discretize_dirichlet", "compress_system",
+            "solve_dirichlet", "KR10_GAMMA", "QUAD_RULES"],
+    "errors": ["InvalidInput", "RefusedTooLarge", "SingularBlock", "NotConverged",
+               "AccuracyWarning"],
+}
+
+
+def test_reference_module_paths_resolve():
+    import importlib
+    missing = []
+    for mod, names in REFERENCE_MODULE_NAMES.items():
+        m = importlib.import_module(f"paper_1110_3105_b200.{mod}")
+        missing += [f"{mod}.{nm}" for nm in names if not hasattr(m, nm)]
+    assert not missing, missing
+
+
+def test_point_files_round_trip(tmp_path):
+    """Text and SKPT binary point files (geom.py:225-277): exact round trips,
+    the documented header bytes, column-count and magic checks."""
+    import struct
+
+    from paper_1110_3105_b200 import geom
+    from paper_1110_3105_b200.errors import InvalidInput
+    rng = np.random.default_rng(3)
+    c = rng.standard_normal((40, 3))
+    nrm = rng.standard_normal((40, 3))
+    nrm /= np.linalg.norm(nrm, axis=1)[:, None]
+    w = rng.random(40) + 0.1
+    for normals, weights in ((None, None), (nrm, None), (None, w), (nrm, w)):
+        ps = geom.PointSet(c, normals, weights)
+        geom.write_points_binary(ps, tmp_path / "p.bin")
+        raw = (tmp_path / "p.bin").read_bytes()
+        assert raw[:4] == b"SKPT"
+        assert struct.unpack("<IBB", raw[4:10]) == (40, 3, int(normals is not None) | 2 * int(weights is not None))
+        assert len(raw) == 10 + 8 * 40 * (3 + (3 if normals is not None else 0) + (1 if weights is not None else 0))
+        q = geom.read_points_binary(tmp_path / "p.bin")
+        geom.write_points_text(ps, tmp_path / "p.txt")
+        t = geom.read_points_text(tmp_path / "p.txt", 3, normals is not None, weights is not None)
+        for got in (q, t):
+            assert np.array_equal(got.coords, c)
+            assert (got.normals is None) == (normals is None) and (got.weights is None) == (weights is None)
+            if normals is not None:
+                assert np.array_equal(got.normals, ps.normals)
+            if weights is not None:
+                assert np.array_equal(got.weights, w)
+    with pytest.raises(InvalidInput):
+        geom.read_points_text(tmp_path / "p.txt", 3, False, False)      # 7 columns, 3 expected
+    (tmp_path / "bad.bin").write_bytes(b"NOPE" + raw[4:])
+    with pytest.raises(InvalidInput):
+        geom.read_points_binary(tmp_path / "bad.bin")
+    (tmp_path / "cut.bin").write_bytes(raw[:-8])
+    with pytest.raises(InvalidInput):
+        geom.read_points_binary(tmp_path / "cut.bin")
+
+
+@gpu
+def test_pivoted_qr_matches_oracle():
+    """pivoted_qr (lowrank.py:48-119) on the GPU: pivots, rank, trailing ratio and
+    |R| against the oracle's CPQR, real and complex, with and without min_rank."""
+    sk = _sk()
+    from oracle import lowrank as olr
+    from paper_1110_3105_b200.lowrank import pivoted_qr
+    rng = np.random.default_rng(5)
+    U, _ = np.linalg.qr(rng.standard_normal((90, 40)))
+    V, _ = np.linalg.qr(rng.standard_normal((60, 40)))
+    A = (U * 0.5 ** np.arange(40)) @ V.T
+    Az = A + 1j * ((U * 0.4 ** np.arange(40)) @ V.T)[:, ::-1]
+    for M, eps, mr in ((A, 1e-8, 0), (A, 1e-4, 25), (Az, 1e-6, 0), (rng.standard_normal((30, 30)), 1e-15, 0)):
+        piv, R, rank, ratio = pivoted_qr(M, eps, min_rank=mr)
+        opiv, oR, orank, oratio = olr.cpqr(M, eps, mr)
+        assert rank == orank and R.shape == (rank, M.shape[1])
+        assert sorted(piv.tolist()) == list(range(M.shape[1]))
+        assert np.array_equal(piv[:rank], np.asarray(opiv)[:rank])
+        assert abs(ratio - oratio) <= 1e-6 * max(oratio, 1e-300) + 1e-300
+        np.testing.assert_allclose(np.abs(R), np.abs(oR), rtol=0, atol=1e-12 * np.abs(oR).max())
+        assert np.all(np.tril(R[:, :rank], -1) == 0)
+        # the factor reproduces the pivoted columns' Gram matrix: R^H R = (A P)^H (A P) on the leading block
+        G = M[:, piv[:rank]].conj().T @ M[:, piv[:rank]]
+        np.testing.assert_allclose(R[:, :rank].conj().T @ R[:, :rank], G, atol=1e-12 * np.abs(G).max())
