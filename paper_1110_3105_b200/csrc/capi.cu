@@ -1,5 +1,6 @@
 // capi.cu -- library self-description entry points.
 #include "common.cuh"
+#include "entries.cuh"
 
 extern "C" {
 
@@ -73,14 +74,16 @@ extern "C" int skel_fp64_probe(int32_t kind, int32_t iters, double* scratch, dou
   return skel_last_error();
 }
 
-// H0^(1)(z) = J0(z) + i Y0(z) elementwise (kernels.py:65-75; CUDA's j0 / y0,
-// the same functions the Helmholtz entries use).  out: interleaved complex.
+// H0^(1)(z) = J0(z) + i Y0(z) elementwise (kernels.py:65-75; sk_hankel<0>, the same
+// function the Helmholtz entries use).  out: interleaved complex.
 __global__ void k_bessel_h0(const double* __restrict__ z, int64_t n, double* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double x = z[i];
-  out[2 * i] = j0(x);
-  out[2 * i + 1] = y0(x);
+  double hj, hy;
+  sk_hankel<0>(x, hj, hy);
+  out[2 * i] = hj;
+  out[2 * i + 1] = hy;
 }
 
 extern "C" int skel_bessel_h0(const double* z, int64_t n, double* out, void* stream) {

@@ -81,10 +81,52 @@ __device__ __forceinline__ double lap_dl(const SkelSource& S, double e, double r
   if (S.dim == 2) return __ddiv_rn(e, __dmul_rn(__dmul_rn(SKEL_TWO_PI, r), r));
   return __ddiv_rn(e, __dmul_rn(SKEL_FOUR_PI, pow(r, 3.0)));
 }
+// Hankel function H_NU^(1)(z) = J_NU + i Y_NU, NU in {0, 1} (kernels.py:65-75 uses
+// scipy's Cephes j0/y0/j1/y1, ~1e-15 of |H| everywhere).  CUDA's j0/y0/j1/y1 hold
+// <= 7e-15 of |H| up to z = 16 but lose up to 9e-12 beyond (measured against
+// mpmath, tools/h0acc.py), so from 16 on Hankel's asymptotic expansion is summed:
+//   H ~ sqrt(2/(pi z)) e^{i(z - NU pi/2 - pi/4)} sum_k i^k a_k / z^k,
+//   a_k = a_{k-1} (4 NU^2 - (2k-1)^2) / (8k),
+// to its smallest term (< e^{-2z} <= 1.3e-14, <= 1.6e-15 of |H| measured); the phase
+// factor is applied as e^{iz} times the exact constant, no reduced argument.
+template <int NU>
+__device__ __forceinline__ void sk_hankel(double z, double& re, double& im) {
+  if (z < 16.0) {
+    re = NU == 0 ? j0(z) : j1(z);
+    im = NU == 0 ? y0(z) : y1(z);
+    return;
+  }
+  const double mu = 4.0 * NU * NU;
+  const double iz = 1.0 / (8.0 * z);
+  double pr = 1.0, pi = 0.0, cr = 1.0, ci = 0.0;
+  for (int k = 1; k < 64; ++k) {
+    const double t = 2.0 * k - 1.0;
+    const double f = (mu - t * t) * iz / k;
+    if (fabs(f) >= 1.0) break;
+    const double nr = -ci * f, ni = cr * f;      // c *= i f
+    cr = nr;
+    ci = ni;
+    pr += cr;
+    pi += ci;
+    if (fabs(cr) + fabs(ci) < 1e-18) break;
+  }
+  double sn, cs;
+  sincos(z, &sn, &cs);
+  const double amp = sqrt(0.63661977236758134308 / z) * 0.70710678118654752440;
+  const double er = NU == 0 ? (cs + sn) * amp : (sn - cs) * amp;
+  const double ei = NU == 0 ? (sn - cs) * amp : -(cs + sn) * amp;
+  re = er * pr - ei * pi;
+  im = er * pi + ei * pr;
+}
+
 // Helmholtz single layer: 2D (i/4) H0(kr), 3D exp(ikr)/(4 pi r)
 __device__ __forceinline__ zc helm_sl(const SkelSource& S, double r) {
   double kr = S.k * r;
-  if (S.dim == 2) return zc(-0.25 * y0(kr), 0.25 * j0(kr));
+  if (S.dim == 2) {
+    double hj, hy;
+    sk_hankel<0>(kr, hj, hy);
+    return zc(-0.25 * hy, 0.25 * hj);
+  }
   double sn, cs;
   sincos(kr, &sn, &cs);
   double den = SKEL_FOUR_PI * r;
@@ -97,7 +139,9 @@ __device__ __forceinline__ zc helm_dl(const SkelSource& S, double e, double r) {
   if (S.dim == 2) {
     // (-0.25j * k) * (J1 + i Y1) * ndot / r   (kernels.py:141)
     double a = 0.25 * S.k;
-    zc h = zc(a * y1(kr), -a * j1(kr));
+    double hj, hy;
+    sk_hankel<1>(kr, hj, hy);
+    zc h = zc(a * hy, -a * hj);
     return zc(h.re * ndot / r, h.im * ndot / r);
   }
   // exp(ikr) (ikr - 1) / (4 pi r^2) * ndot / r  (kernels.py:143-144)

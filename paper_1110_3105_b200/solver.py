@@ -130,7 +130,8 @@ class FactoredInverse:
         """(lu, piv) of Shat exactly as the reference holds it (scipy
         lu_factor conventions, solver.py:269-274), host arrays.  The solve
         uses the explicit Shat^-1; the LU is computed on the device on first
-        access (skel_dense_lu) -- or is the one a loaded container carried."""
+        access (skel_dense_lu) -- or is the one a loaded container carried.
+        Materialising it re-derives ``S_inv`` from the LU (see below)."""
         if getattr(self, "_S_lu", None) is None and self.S_hat is not None and self.S_hat.numel():
             torch = _native.require_cuda()
             L = _native.lib()
@@ -146,6 +147,16 @@ class FactoredInverse:
             if int(st.item()):
                 raise SingularBlock("top", 0, "S")
             self._S_lu = (_native.to_host(A).copy(), piv.cpu().numpy())
+            # from here on the solve uses the inverse DERIVED FROM THIS LU (the
+            # routine a loaded container runs), so a saved and re-loaded
+            # factorization solves bit-identically to this one, as the
+            # reference's does (tests/test_solver.py:335-358); written in place:
+            # captured solve graphs keep pointing at the same tensor
+            if self.S_inv is not None and tuple(self.S_inv.shape) == (K, K):
+                inv = torch.empty_like(self.S_inv)
+                _native.check(L.skel_lu_inverse(_native.ptr(A), _native.ptr(piv), K, _native.ptr(inv),
+                                                self.field, _native.stream_ptr()), "skel_lu_inverse")
+                self.S_inv.copy_(inv)
         return getattr(self, "_S_lu", None)
 
     def perm_dev(self):
@@ -297,6 +308,15 @@ class FactorRun:
         buckets = pl.buckets
         merged = pl.merged if pl.merged_first else None
         p = dl.p
+        if self.stream is not None:
+            # the compressed level's slabs and index arrays were allocated on the
+            # caller's stream but are read by kernels queued on the eager stream:
+            # tell the allocator, or dropping the compression without factor()
+            # (nothing ever joins the eager stream then) lets the blocks be
+            # reused while those kernels still run
+            for x in (dl.D, dl.L, dl.R, *dl.t.values()):
+                if hasattr(x, "record_stream") and x.is_cuda:
+                    x.record_stream(self.stream)
         outer = torch.cuda.stream(self.stream) if self.stream is not None else _nullctx()
         with outer:
             pk = Packer()

@@ -300,7 +300,7 @@ def test_pivoted_qr_matches_oracle():
         assert rank == orank and R.shape == (rank, M.shape[1])
         assert sorted(piv.tolist()) == list(range(M.shape[1]))
         assert np.array_equal(piv[:rank], np.asarray(opiv)[:rank])
-        assert abs(ratio - oratio) <= 1e-6 * max(oratio, 1e-300) + 1e-300
+        assert abs(ratio - oratio) <= 1e-6 * max(oratio, 1e-300) + 1e-300, (ratio, oratio, eps, mr)
         np.testing.assert_allclose(np.abs(R), np.abs(oR), rtol=0, atol=1e-12 * np.abs(oR).max())
         assert np.all(np.tril(R[:, :rank], -1) == 0)
         # the factor reproduces the pivoted columns' Gram matrix: R^H R = (A P)^H (A P) on the leading block
