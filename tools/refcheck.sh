@@ -7,6 +7,6 @@ set -u
 mkdir -p gpurun_out
 T=${1:-refcheck}
 PYTHONPATH=$PWD/_refcheck:$PWD timeout 2400 python -m pytest _refcheck/tests -q -p no:cacheprovider \
-    --timeout 600 -rfE --tb=short > gpurun_out/${T}.log 2>&1
+    --timeout 600 -v -rfE --tb=short > gpurun_out/${T}.log 2>&1
 echo "refcheck rc=$?"
 tail -40 gpurun_out/${T}.log
