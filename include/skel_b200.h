@@ -410,6 +410,10 @@ int skel_tree_cover(void* handle, int32_t li, int64_t* count, int64_t* ids);
  * the number of adjacency entries; pass idx = NULL to query it. */
 int skel_tree_neighbors(void* handle, int32_t li, int64_t* off, int64_t* count,
                         int64_t* idx);
+/* Borrowed pointer to the tree permutation (n int64, tree position -> original
+ * index; read-only, valid until skel_tree_free): lets the caller wrap it without
+ * the 8 n-byte copy skel_tree_nodes makes when given a perm buffer. */
+int skel_tree_perm_ptr(void* handle, const int64_t** perm);
 int skel_tree_free(void* handle);
 /* PointSet validation (geom.py:42 and the unit-normal rule): 0 ok, -3 a
  * non-finite coordinate, -4 a normal with | |n| - 1 | > 1e-12 (normals may be

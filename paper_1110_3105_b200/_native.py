@@ -101,6 +101,7 @@ _SIGS = {
     "skel_tree_nodes": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "skel_tree_cover": [c_vp, c_i32, _P(c_i64), c_vp],
     "skel_tree_neighbors": [c_vp, c_i32, c_vp, _P(c_i64), c_vp],
+    "skel_tree_perm_ptr": [c_vp, c_vp],
     "skel_tree_free": [c_vp],
     "skel_device_query": [_P(c_i32), _P(c_i32), _P(c_i32), _P(c_i32)],
     "skel_fp64_probe": [c_i32, c_i32, c_vp, _P(c_f64), c_vp],

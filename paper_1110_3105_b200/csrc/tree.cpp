@@ -747,6 +747,13 @@ int skel_tree_nodes(void* handle, double* center, double* hw, int64_t* lo, int64
   return 0;
 }
 
+int skel_tree_perm_ptr(void* handle, const int64_t** perm) {
+  Tree* T = (Tree*)handle;
+  if (!T || !perm) return -1;
+  *perm = T->perm.data();       // n entries, never written after the build, valid until skel_tree_free
+  return 0;
+}
+
 int skel_tree_cover(void* handle, int32_t li, int64_t* count, int64_t* ids) {
   Tree* T = (Tree*)handle;
   if (!T || li < 0 || li >= (int32_t)T->covers.size()) return -1;

@@ -91,6 +91,22 @@ class TreeNode:
         return self.hi - self.lo
 
 
+class _TreeHandle:
+    """Owns one native tree (csrc/tree.cpp); freed when the OrthTree AND every
+    array that borrows native memory (the permutation) are gone."""
+
+    def __init__(self, handle):
+        self.ptr = ctypes.c_void_p(handle)
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                _native.lib().skel_tree_free(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
 class OrthTree:
     """Adaptive 2^d tree.  ``levels[0]`` is the finest cover, ``levels[-1]``
     the root alone; ``perm`` maps tree positions to original indices.  Node
@@ -99,7 +115,8 @@ class OrthTree:
 
     def __init__(self, handle, dim, n):
         L = _native.lib()
-        self._handle = ctypes.c_void_p(handle)
+        self._owner = _TreeHandle(handle)
+        self._handle = self._owner.ptr
         self.dim = dim
         nn = ctypes.c_int64()
         nc = ctypes.c_int32()
@@ -113,11 +130,22 @@ class OrthTree:
         self.node_depth = np.empty(nn, dtype=np.int64)
         self.parent = np.empty(nn, dtype=np.int64)
         self.nchild = np.empty(nn, dtype=np.int64)
-        self.perm = np.empty(n, dtype=np.int64)
         a = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
         _native.check(L.skel_tree_nodes(self._handle, a(self.center), a(self.hw), a(self.lo),
                                         a(self.hi), a(self.node_depth), a(self.parent),
-                                        a(self.nchild), a(self.perm)), "skel_tree_nodes")
+                                        a(self.nchild), None), "skel_tree_nodes")
+        # the permutation is the native array itself (no 8 n-byte copy per
+        # build): a read-only view whose base keeps the tree handle alive, so
+        # it stays valid for cm.perm / fi.perm after this object is gone
+        pp = ctypes.c_void_p()
+        _native.check(L.skel_tree_perm_ptr(self._handle, ctypes.byref(pp)), "skel_tree_perm_ptr")
+        if n > 0 and pp.value:
+            buf = (ctypes.c_int64 * n).from_address(pp.value)
+            buf._owner = self._owner
+            self.perm = np.ctypeslib.as_array(buf)
+            self.perm.flags.writeable = False
+        else:
+            self.perm = np.empty(n, dtype=np.int64)
         self.levels = []
         for li in range(nc):
             cnt = ctypes.c_int64()
@@ -129,14 +157,6 @@ class OrthTree:
             self.levels.append(ids)
         self._nodes = None
         self._nbr_cache = {}
-
-    def __del__(self):
-        try:
-            if self._handle:
-                _native.lib().skel_tree_free(self._handle)
-                self._handle = None
-        except Exception:
-            pass
 
     @property
     def nodes(self):
