@@ -316,3 +316,29 @@ def test_pivoted_qr_matches_oracle():
         # the factor reproduces the pivoted columns' Gram matrix: R^H R = (A P)^H (A P) on the leading block
         G = M[:, piv[:rank]].conj().T @ M[:, piv[:rank]]
         np.testing.assert_allclose(R[:, :rank].conj().T @ R[:, :rank], G, atol=1e-12 * np.abs(G).max())
+
+
+def test_skelkit_alias_imports_like_the_reference():
+    """tools/refcheck/skelkit: `import skelkit` / `from skelkit.X import name` resolve to this
+    package (the alias the reference's own test modules are run through)."""
+    import importlib
+    import os
+    import sys
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "refcheck")
+    sys.path.insert(0, root)
+    try:
+        for m in [k for k in sys.modules if k == "skelkit" or k.startswith("skelkit.")]:
+            del sys.modules[m]
+        skelkit = importlib.import_module("skelkit")
+        from skelkit.geom import PointSet, build_tree, read_points_binary      # noqa: F401
+        from skelkit.lowrank import id_fixed_precision, pivoted_qr             # noqa: F401
+        from skelkit.skel import compress, serialize_compressed                # noqa: F401
+        from skelkit.solver import assemble_embedding, factor, gmres, solve    # noqa: F401
+        from skelkit import bie                                                # noqa: F401
+        import paper_1110_3105_b200 as pkg
+        assert skelkit.compress is pkg.compress and bie is pkg.bie
+        assert gmres is pkg.gmres
+    finally:
+        sys.path.remove(root)
+        for m in [k for k in sys.modules if k == "skelkit" or k.startswith("skelkit.")]:
+            del sys.modules[m]
