@@ -270,14 +270,21 @@ __device__ int sm_invert_any(T* A, int lda, int p, T* scratch, int* ipiv, FacSha
   if (p <= 64) return sm_invert_rows<T, 2>(A, lda, p, scratch, ipiv, sh);
   if (p <= 96) return sm_invert_rows<T, 3>(A, lda, p, scratch, ipiv, sh);
   if (p <= 128) return sm_invert_rows<T, 4>(A, lda, p, scratch, ipiv, sh);
-  // real blocks that still fit shared memory (p <= 168: the 2^20 top level, K = 160):
-  // same pivots and arithmetic, 0.88 -> 0.64 ms at K = 160; wider blocks run out of a
-  // global scratch slab, where the flat walk of sm_invert is the faster one
-  if constexpr (sizeof(T) == sizeof(double)) {
-    if (p <= 160) return sm_invert_rows<T, 5>(A, lda, p, scratch, ipiv, sh);
-    if (p <= 168) return sm_invert_rows<T, 6>(A, lda, p, scratch, ipiv, sh);
-  }
   return sm_invert<T>(A, lda, p, scratch, ipiv, sh);
+}
+
+// Top-level variant (k_dense_inverse only -- instantiating these in k_factor_level costs
+// that kernel 5-12 % through its 64-register cap): real blocks that still fit shared memory
+// (p <= 168: the 2^20 top level, K = 160) also take the row-parallel elimination; same
+// pivots and arithmetic, 0.88 -> 0.64 ms at K = 160.  Wider blocks run out of a global
+// scratch slab, where the flat walk of sm_invert is the faster one.
+template <class T>
+__device__ int sm_invert_top(T* A, int lda, int p, T* scratch, int* ipiv, FacShared<T>& sh) {
+  if constexpr (sizeof(T) == sizeof(double)) {
+    if (p > 128 && p <= 160) return sm_invert_rows<T, 5>(A, lda, p, scratch, ipiv, sh);
+    if (p > 160 && p <= 168) return sm_invert_rows<T, 6>(A, lda, p, scratch, ipiv, sh);
+  }
+  return sm_invert_any<T>(A, lda, p, scratch, ipiv, sh);
 }
 
 // ---------------------------------------------------------------------------
@@ -781,7 +788,7 @@ __global__ void __launch_bounds__(1024) k_dense_inverse(T* Ag, int K, double reg
     __syncthreads();
   }
   double nA = sm_norm1<T>(A, K, K, K, sh);
-  int bad = sm_invert_any<T>(A, K, K, colk, ipiv, sh);
+  int bad = sm_invert_top<T>(A, K, K, colk, ipiv, sh);
   if (bad) {
     if (threadIdx.x == 0) { *status = 1; *rcond = 0.0; }
     return;
